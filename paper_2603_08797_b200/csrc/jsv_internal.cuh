@@ -1,0 +1,317 @@
+// jsv_internal.cuh -- device-side data layout and shared device functions.
+//
+// Numerics contract: every floating-point expression below
+// reproduces the reference's CPython operation order.  The library is built
+// with -fmad=false so no a*b+c is ever contracted into an FMA, and IEEE
+// division (the nvcc default -prec-div=true) is used everywhere.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/jsv.h"
+
+#define MAXT JSV_MAX_TASKS
+#define MAXE JSV_MAX_EDGES
+#define MAXP JSV_MAX_PATHS
+#define MAXI JSV_MAX_ITEMS
+#define NONE16 0xFFFFu
+#define N_LEVELS 14
+#define MAXD (4 + MAXE)
+
+// Small fixed-size graph description, one per problem, in global memory.
+struct DGraph {
+  int T, E, P, entry, maxout, sum_path;
+  int topo[MAXT];
+  int pos_of[MAXT];
+  int decl[MAXT];
+  int succ_off[MAXT + 1];
+  int edge_dst[MAXE];
+  int edge_src[MAXE];
+  int pred_off[MAXT + 1];
+  int pred_edge[MAXE];
+  int path_off[MAXP + 1];
+  uint32_t path_mask[MAXP];
+  int path_task[MAXP * MAXT];
+  double path_frac[MAXP];
+  int var_off[MAXT + 1];
+  int most_acc[MAXT];
+  int key_off[MAXT + 1];
+  double a_max;
+};
+
+// Variable-size tables of a problem (device pointers).
+struct DTables {
+  const double* var_acc;
+  const int* var_fac_off;
+  const double* var_fac;
+  const int* key_var;
+  const int* key_cost;
+  const double* key_lat;
+  const double* key_thr;
+  const int* sub_off;   // [4T+1]
+  const int* sub_key;
+  const int* grp_off;   // [4T+1]
+  const int* grp_rep;   // [2*groups]
+};
+
+// Request scalars shared by all probes of one call.
+struct DReq {
+  int S;
+  unsigned space;
+  double slack;
+  double eps;
+  int W;
+  int n_mix;
+  double mix[JSV_MAX_MIX];
+  int feasible_only;
+  int has_ov[MAXE];
+  double ov[MAXE];
+};
+
+// Per-probe scalars (host-computed demand bounds + the caller's probe).
+struct DProbe {
+  double demand, slo_eff, acc_slo, alpha, beta;
+  double r_upper[2][MAXT];   // _demand_upper_bound for A' = off / on (planner.py:674-680)
+  uint32_t could_zero;       // low[t] == 0.0 with min factors (planner.py:772-774)
+  // plan_uninformed
+  double lat_budget[MAXT], floor_[MAXT], weight[MAXT], best_hput[MAXT];
+  int best_slices[MAXT], min_cost[MAXT];
+  double star[MAXT];         // demand_star (planner.py:1014-1015)
+  double slice_budget[MAXT]; // planner.py:1017-1037
+};
+
+// Stage-1 generation descriptor: one per (task, enabled sub-space).
+struct GenDesc {
+  int task, sub, a, mode;   // mode 0 = exhaustive, 1 = structured
+  int n_tuples, key_base;   // tuples = sub_key[key_base .. key_base+n_tuples)
+  int grp_base, n_groups;
+  int w_off;                // exhaustive: offset of the suffix ways table [(n+1) x (S+1)]
+  int unit_off;             // first unit of this descriptor inside a probe
+  int n_tuple_units, n_mix_units;  // structured: per-tuple units, then mix units
+  int n_units;
+};
+
+// Best-so-far record per probe for the Stage-2 reduction.
+struct BestRec {
+  int lock;
+  int has;
+  int found;        // a feasible leaf exists (feasible_only early exit)
+  int has_leaf;     // some leaf was reached (failed-leaf diagnostics)
+  double obj;
+  int sl;
+  int pad_;
+  unsigned long long tie[4];     // packed m-ranks (task-id order), 16 bits each
+  unsigned long long leafkey[4]; // packed topo-order choices of the max reached leaf
+  uint16_t choice[MAXT];
+  uint16_t leaf_choice[MAXT];
+  int deepest;      // deepest blocked level (-1)
+  int kills[MAXT][5];
+  unsigned long long nodes, leaves;
+};
+
+__device__ __forceinline__ double d_max(double a, double b) {
+  // Python max(a, b): keeps a unless b > a
+  return (b > a) ? b : a;
+}
+
+// CPython >= 3.12 builtin sum() over floats, starting from int 0 (Neumaier).
+struct PySum {
+  double f, c;
+  bool any;
+  __device__ __forceinline__ PySum() : f(0.0), c(0.0), any(false) {}
+  __device__ __forceinline__ void add(double x) {
+    if (!any) {
+      f = 0.0 + x;
+      any = true;
+      return;
+    }
+    double t = f + x;
+    if (fabs(f) >= fabs(x))
+      c += (f - t) + x;
+    else
+      c += (x - t) + f;
+    f = t;
+  }
+  __device__ __forceinline__ double result() const {
+    if (!any) return 0.0;
+    double r = f;
+    if (c != 0.0 && isfinite(c)) r += c;
+    return r;
+  }
+};
+
+// _stats_for_counts (planner.py:178-213) over packed items (key << 16 | count).
+struct Stat {
+  double lat, cap, acc;
+  int sl;
+  double fan[MAXE];  // only [0, outdeg) used
+};
+
+__device__ inline void bundle_stats(const DGraph& g, const DTables& tb, int t, const uint32_t* items,
+                                    int n, Stat& s) {
+  int outd = g.succ_off[t + 1] - g.succ_off[t];
+  if (n == 0) {
+    s.lat = 0.0; s.cap = 0.0; s.acc = 1.0; s.sl = 0;
+    for (int j = 0; j < outd; ++j) s.fan[j] = 0.0;
+    return;
+  }
+  const int kb = g.key_off[t];
+  const int vb = g.var_off[t];
+  double lat = 0.0, cap = 0.0;
+  int sl = 0;
+  // weighted means with the all-equal short circuit (planner.py:155-166)
+  int v0 = tb.key_var[kb + (items[0] >> 16)];
+  double a0 = tb.var_acc[vb + v0];
+  bool acc_eq = true;
+  for (int i = 0; i < n; ++i) {
+    int k = kb + (items[i] >> 16);
+    double c = (double)(items[i] & 0xFFFFu);
+    double h = c * tb.key_thr[k];
+    lat = d_max(lat, tb.key_lat[k]);
+    cap += h;
+    sl += (int)(items[i] & 0xFFFFu) * tb.key_cost[k];
+    double a = tb.var_acc[vb + tb.key_var[k]];
+    if (!(a == a0)) acc_eq = false;
+  }
+  s.lat = lat; s.cap = cap; s.sl = sl;
+  if (acc_eq) {
+    s.acc = a0;
+  } else {
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < n; ++i) {
+      int k = kb + (items[i] >> 16);
+      double h = (double)(items[i] & 0xFFFFu) * tb.key_thr[k];
+      num += tb.var_acc[vb + tb.key_var[k]] * h;
+      den += h;
+    }
+    s.acc = num / den;
+  }
+  for (int j = 0; j < outd; ++j) {
+    double f0 = tb.var_fac[tb.var_fac_off[vb + v0] + j];
+    bool eq = true;
+    for (int i = 1; i < n; ++i) {
+      double f = tb.var_fac[tb.var_fac_off[vb + tb.key_var[kb + (items[i] >> 16)]] + j];
+      if (!(f == f0)) { eq = false; break; }
+    }
+    if (eq) {
+      s.fan[j] = f0;
+    } else {
+      double num = 0.0, den = 0.0;
+      for (int i = 0; i < n; ++i) {
+        int k = kb + (items[i] >> 16);
+        double h = (double)(items[i] & 0xFFFFu) * tb.key_thr[k];
+        num += tb.var_fac[tb.var_fac_off[vb + tb.key_var[k]] + j] * h;
+        den += h;
+      }
+      s.fan[j] = num / den;
+    }
+  }
+}
+
+// Fraction-weighted path accuracy (model.py:267-282).
+__device__ inline double weighted_paths(const DGraph& g, const double* acc) {
+  double total = 0.0;
+  for (int p = 0; p < g.P; ++p) {
+    double prod = 1.0;
+    for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) prod *= acc[g.path_task[k]];
+    total += g.path_frac[p] * prod;
+  }
+  return total;
+}
+
+// Full derive_configuration + validate_configuration of one assignment
+// (planner.py:243-361).  Inputs per task index; fan_in per edge is the chosen
+// bundle's fan-out (0 for an empty task).  present = tasks with items.
+struct EvalOut {
+  double dem[MAXT];
+  double fan[MAXE];
+  double a_obj, objective;
+  int total_sl;
+  uint32_t uncovered;
+  bool feasible;
+  int first_fail;  // binding from verdicts (planner.py:717-725), -1 if none
+};
+
+template <bool MARGINS>
+__device__ inline void evaluate(const DGraph& g, const DReq& rq, const DProbe& pr, const double* lat,
+                                const double* cap, const double* acc, const int* sl,
+                                const double* fan_in, uint32_t present, EvalOut& ev,
+                                double* lat_margin, double* thr_margin, double* res_margin,
+                                double* acc_margin) {
+  for (int e = 0; e < g.E; ++e) ev.fan[e] = rq.has_ov[e] ? rq.ov[e] : fan_in[e];
+  // propagate_demand (model.py:239-264)
+  for (int i = 0; i < g.T; ++i) {
+    int t = g.topo[i];
+    if (t == g.entry) {
+      ev.dem[t] = pr.demand;
+    } else {
+      double s = 0.0;
+      for (int k = g.pred_off[t]; k < g.pred_off[t + 1]; ++k) {
+        int e = g.pred_edge[k];
+        s += ev.dem[g.edge_src[e]] * ev.fan[e];
+      }
+      ev.dem[t] = s;
+    }
+  }
+  bool ok = true;
+  bool lat_fail = false, thr_fail = false;
+  // latency verdicts: sum(2.0 * L_t for t in p) with CPython 3.12 sum
+  for (int p = 0; p < g.P; ++p) {
+    PySum ps;
+    for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) ps.add(2.0 * lat[g.path_task[k]]);
+    double m = pr.slo_eff - ps.result();
+    if (MARGINS) lat_margin[p] = m;
+    if (!(m >= 0)) { ok = false; lat_fail = true; }
+  }
+  for (int i = 0; i < g.T; ++i) {
+    int t = g.topo[i];
+    double m = cap[t] - ev.dem[t] * (1.0 + rq.slack);
+    if (MARGINS) thr_margin[t] = m;
+    if (!(m >= 0)) { ok = false; thr_fail = true; }
+  }
+  int tot = 0;
+  for (int t = 0; t < g.T; ++t) tot += sl[t];
+  ev.total_sl = tot;
+  double rm = (double)(rq.S - tot);
+  if (MARGINS) *res_margin = rm;
+  bool res_fail = !(rm >= 0);
+  double a_obj = weighted_paths(g, acc) / g.a_max;
+  ev.a_obj = a_obj;
+  double am = a_obj - pr.acc_slo;
+  if (MARGINS) *acc_margin = am;
+  bool acc_fail = !(am >= 0);
+  uint32_t unc = 0;
+  for (int t = 0; t < g.T; ++t)
+    if (ev.dem[t] > 0 && !((present >> t) & 1u)) unc |= 1u << t;
+  ev.uncovered = unc;
+  ok = ok && !res_fail && !acc_fail && unc == 0;
+  ev.feasible = ok;
+  ev.objective = pr.alpha * a_obj - pr.beta * (double)tot;
+  // priority throughput > latency > resources > accuracy > coverage(->throughput)
+  if (ok) ev.first_fail = -1;
+  else if (thr_fail) ev.first_fail = JSV_BIND_THROUGHPUT;
+  else if (lat_fail) ev.first_fail = JSV_BIND_LATENCY;
+  else if (res_fail) ev.first_fail = JSV_BIND_RESOURCES;
+  else if (acc_fail) ev.first_fail = JSV_BIND_ACCURACY;
+  else ev.first_fail = JSV_BIND_THROUGHPUT;  // coverage reported as throughput
+}
+
+// Lexicographic compare of packed word vectors (n words).
+__device__ __forceinline__ int cmp_words(const unsigned long long* a, const unsigned long long* b,
+                                         int n) {
+  for (int i = 0; i < n; ++i) {
+    if (a[i] < b[i]) return -1;
+    if (a[i] > b[i]) return 1;
+  }
+  return 0;
+}
+
+__device__ __forceinline__ void spin_lock(int* l) {
+  while (atomicCAS(l, 0, 1) != 0) {
+    __nanosleep(32);
+  }
+  __threadfence();
+}
+__device__ __forceinline__ void spin_unlock(int* l) {
+  __threadfence();
+  atomicExch(l, 0);
+}
