@@ -1,0 +1,1255 @@
+// jsv_api.cu -- host runtime of libjsv.so: context, lowered problems, batch
+// orchestration of the Stage-1 / Stage-2 kernels, and the max_demand driver.
+//
+// Host-side scalar set-up (demand upper bounds, could_zero, exhaustive vs
+// structured decision, plan_uninformed slice budgets) mirrors the reference's
+// Python float order exactly; the file is compiled with -ffp-contract=off so
+// no host expression is contracted into an FMA.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "jsv_internal.cuh"
+#include "jsv_kernels.h"
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(JSV_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= n) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t want = bytes + bytes / 4 + 256;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) n = want;
+    return e;
+  }
+  template <class T>
+  T* as() const { return reinterpret_cast<T*>(p); }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+enum BufId {
+  B_REQ, B_PROBES, B_DESC, B_WAYS, B_TILE_TASK, B_TILE_START, B_ITEMS, B_NITEMS, B_ARR, B_SL, B_FLAG,
+  B_CNT, B_FRONT, B_FCNT, B_FPOS, B_FCR, B_SORTED, B_SCR, B_POOLC, B_POOLN, B_POOLT, B_PSL,
+  B_PCAP, B_PACC, B_PLAT, B_PFAN, B_RANKP, B_RANKM, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
+  B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
+  B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
+  B_COUNT
+};
+
+struct jsv_context {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[4] = {};
+  DevBuf buf[B_COUNT];
+  jsv_stats stats{};
+};
+
+struct S1Plan {
+  std::vector<GenDesc> desc;
+  std::vector<unsigned> ways;
+  std::vector<long long> task_cap;
+  std::vector<int> tile_task, tile_start;
+  int U = 0, maxi = 2;
+  long long C_probe = 0;
+  long long max_cap = 0;
+};
+
+struct jsv_problem {
+  jsv_context* ctx = nullptr;
+  int T = 0, E = 0, P = 0, entry = 0, maxout = 0;
+  std::vector<int> topo, decl, succ_off, edge_dst, edge_src, pred_off, pred_edge, path_off,
+      path_task;
+  std::vector<double> path_frac;
+  std::vector<int> var_off, var_fac_off, most_acc;
+  std::vector<double> var_acc, var_fac;
+  std::vector<int> key_off, key_var, key_cost;
+  std::vector<double> key_lat, key_thr;
+  std::vector<int> sub_off, sub_key, grp_off, grp_rep;
+  double a_max = 0.0;
+  DGraph hg{};
+  DevBuf dgraph, d_var_acc, d_var_fac_off, d_var_fac, d_key_var, d_key_cost, d_key_lat, d_key_thr,
+      d_sub_off, d_sub_key, d_grp_off, d_grp_rep;
+  DTables dt{};
+  std::map<std::tuple<int, unsigned, int, int>, std::shared_ptr<S1Plan>> s1cache;
+};
+
+template <class T>
+static cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
+  size_t bytes = sizeof(T) * (v.empty() ? 1 : v.size());
+  cudaError_t e = b.ensure(bytes);
+  if (e != cudaSuccess) return e;
+  if (!v.empty()) e = cudaMemcpy(b.p, v.data(), sizeof(T) * v.size(), cudaMemcpyHostToDevice);
+  return e;
+}
+
+extern "C" const char* jsv_last_error(void) { return g_err.c_str(); }
+extern "C" int jsv_version(void) { return 1; }
+extern "C" int jsv_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+extern "C" int jsv_context_create(int device, jsv_context** out) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+    return fail(JSV_ERR_NODEV, "no CUDA device visible: the sm_100a planner has no CPU fallback");
+  if (device < 0 || device >= n) return fail(JSV_ERR_ARG, "device index out of range");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    return fail(JSV_ERR_NODEV, std::string("libjsv is built for sm_100a, device is ") + prop.name);
+  auto* c = new jsv_context();
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  for (auto& e : c->ev) CK(cudaEventCreate(&e));
+  *out = c;
+  return JSV_OK;
+}
+
+extern "C" void jsv_context_destroy(jsv_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->st) cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+// ---------------------------------------------------------------- problems
+
+extern "C" int jsv_problem_create(jsv_context* ctx, const jsv_problem_desc* d, jsv_problem** out) {
+  if (!ctx || !d || !out) return fail(JSV_ERR_ARG, "null argument");
+  const int T = d->n_tasks, E = d->n_edges, P = d->n_paths;
+  if (T < 1 || T > MAXT) return fail(JSV_ERR_ARG, "task count outside [1, 16]");
+  if (E < 0 || E > MAXE) return fail(JSV_ERR_ARG, "edge count outside [0, 32]");
+  if (P < 1 || P > MAXP) return fail(JSV_ERR_ARG, "path count outside [1, 64]");
+  CK(cudaSetDevice(ctx->device));
+  auto pr = std::make_unique<jsv_problem>();
+  jsv_problem& p = *pr;
+  p.ctx = ctx;
+  p.T = T; p.E = E; p.P = P; p.entry = d->entry;
+  p.topo.assign(d->topo, d->topo + T);
+  p.decl.assign(d->decl, d->decl + T);
+  p.succ_off.assign(d->succ_off, d->succ_off + T + 1);
+  p.edge_dst.assign(d->edge_dst, d->edge_dst + E);
+  p.pred_off.assign(d->pred_off, d->pred_off + T + 1);
+  p.pred_edge.assign(d->pred_edge, d->pred_edge + E);
+  p.path_off.assign(d->path_off, d->path_off + P + 1);
+  p.path_task.assign(d->path_task, d->path_task + p.path_off[P]);
+  p.path_frac.assign(d->path_frac, d->path_frac + P);
+  p.var_off.assign(d->var_off, d->var_off + T + 1);
+  const int V = p.var_off[T];
+  p.var_acc.assign(d->var_acc, d->var_acc + V);
+  p.var_fac_off.assign(d->var_fac_off, d->var_fac_off + V);
+  int nfac = 0;
+  for (int t = 0; t < T; ++t)
+    nfac += (p.var_off[t + 1] - p.var_off[t]) * (p.succ_off[t + 1] - p.succ_off[t]);
+  p.var_fac.assign(d->var_fac, d->var_fac + nfac);
+  p.most_acc.assign(d->most_acc, d->most_acc + T);
+  p.key_off.assign(d->key_off, d->key_off + T + 1);
+  const int K = p.key_off[T];
+  p.key_var.assign(d->key_var, d->key_var + K);
+  p.key_cost.assign(d->key_cost, d->key_cost + K);
+  p.key_lat.assign(d->key_lat, d->key_lat + K);
+  p.key_thr.assign(d->key_thr, d->key_thr + K);
+  p.sub_off.assign(d->sub_off, d->sub_off + 4 * T + 1);
+  p.sub_key.assign(d->sub_key, d->sub_key + p.sub_off[4 * T]);
+  p.grp_off.assign(d->grp_off, d->grp_off + 4 * T + 1);
+  p.grp_rep.assign(d->grp_rep, d->grp_rep + 2 * p.grp_off[4 * T]);
+  p.a_max = d->a_max;
+  for (int t = 0; t < T; ++t) {
+    if (p.key_off[t + 1] - p.key_off[t] > 65535) return fail(JSV_ERR_ARG, "too many profile keys");
+  }
+  p.edge_src.assign(E, 0);
+  for (int t = 0; t < T; ++t)
+    for (int e = p.succ_off[t]; e < p.succ_off[t + 1]; ++e) p.edge_src[e] = t;
+  p.maxout = 1;
+  for (int t = 0; t < T; ++t) p.maxout = std::max(p.maxout, p.succ_off[t + 1] - p.succ_off[t]);
+  if (p.path_off[P] > MAXP * MAXT) return fail(JSV_ERR_ARG, "paths too long");
+  DGraph& g = p.hg;
+  memset(&g, 0, sizeof(g));
+  g.T = T; g.E = E; g.P = P; g.entry = p.entry; g.maxout = p.maxout; g.sum_path = p.path_off[P];
+  for (int i = 0; i < T; ++i) {
+    g.topo[i] = p.topo[i];
+    g.pos_of[p.topo[i]] = i;
+    g.decl[i] = p.decl[i];
+    g.most_acc[i] = p.most_acc[i];
+  }
+  for (int i = 0; i <= T; ++i) {
+    g.succ_off[i] = p.succ_off[i];
+    g.pred_off[i] = p.pred_off[i];
+    g.var_off[i] = p.var_off[i];
+    g.key_off[i] = p.key_off[i];
+  }
+  for (int e = 0; e < E; ++e) {
+    g.edge_dst[e] = p.edge_dst[e];
+    g.edge_src[e] = p.edge_src[e];
+    g.pred_edge[e] = p.pred_edge[e];
+  }
+  for (int i = 0; i <= P; ++i) g.path_off[i] = p.path_off[i];
+  for (int i = 0; i < p.path_off[P]; ++i) g.path_task[i] = p.path_task[i];
+  for (int q = 0; q < P; ++q) {
+    g.path_frac[q] = p.path_frac[q];
+    uint32_t m = 0;
+    for (int k = p.path_off[q]; k < p.path_off[q + 1]; ++k) m |= 1u << p.path_task[k];
+    g.path_mask[q] = m;
+  }
+  g.a_max = p.a_max;
+  CK(p.dgraph.ensure(sizeof(DGraph)));
+  CK(cudaMemcpy(p.dgraph.p, &g, sizeof(DGraph), cudaMemcpyHostToDevice));
+  CK(upload(p.d_var_acc, p.var_acc));
+  CK(upload(p.d_var_fac_off, p.var_fac_off));
+  CK(upload(p.d_var_fac, p.var_fac));
+  CK(upload(p.d_key_var, p.key_var));
+  CK(upload(p.d_key_cost, p.key_cost));
+  CK(upload(p.d_key_lat, p.key_lat));
+  CK(upload(p.d_key_thr, p.key_thr));
+  CK(upload(p.d_sub_off, p.sub_off));
+  CK(upload(p.d_sub_key, p.sub_key));
+  CK(upload(p.d_grp_off, p.grp_off));
+  CK(upload(p.d_grp_rep, p.grp_rep));
+  p.dt.var_acc = p.d_var_acc.as<double>();
+  p.dt.var_fac_off = p.d_var_fac_off.as<int>();
+  p.dt.var_fac = p.d_var_fac.as<double>();
+  p.dt.key_var = p.d_key_var.as<int>();
+  p.dt.key_cost = p.d_key_cost.as<int>();
+  p.dt.key_lat = p.d_key_lat.as<double>();
+  p.dt.key_thr = p.d_key_thr.as<double>();
+  p.dt.sub_off = p.d_sub_off.as<int>();
+  p.dt.sub_key = p.d_sub_key.as<int>();
+  p.dt.grp_off = p.d_grp_off.as<int>();
+  p.dt.grp_rep = p.d_grp_rep.as<int>();
+  *out = pr.release();
+  return JSV_OK;
+}
+
+extern "C" void jsv_problem_destroy(jsv_problem* prob) { delete prob; }
+
+// ------------------------------------------------------ host scalar set-up
+
+// propagate_demand (model.py:239-264) with per-edge factors
+static void host_rates(const jsv_problem& p, double demand, const double* fac, double* out) {
+  for (int i = 0; i < p.T; ++i) {
+    const int t = p.topo[i];
+    if (t == p.entry) {
+      out[t] = demand;
+      continue;
+    }
+    double s = 0.0;
+    for (int k = p.pred_off[t]; k < p.pred_off[t + 1]; ++k) {
+      const int e = p.pred_edge[k];
+      s += out[p.edge_src[e]] * fac[e];
+    }
+    out[t] = s;
+  }
+}
+
+// _max_factors / _min_factors (planner.py:638-671)
+static void host_factors(const jsv_problem& p, const jsv_request& rq, bool a, bool want_max,
+                         double* fac) {
+  for (int t = 0; t < p.T; ++t) {
+    for (int e = p.succ_off[t]; e < p.succ_off[t + 1]; ++e) {
+      const int j = e - p.succ_off[t];
+      if (rq.has_override && rq.has_override[e]) {
+        fac[e] = rq.override_val[e];
+        continue;
+      }
+      const int v0 = p.var_off[t], v1 = p.var_off[t + 1];
+      double best = 0.0;
+      bool first = true;
+      for (int v = v0; v < v1; ++v) {
+        if (!a && v - v0 != p.most_acc[t]) continue;
+        const double f = p.var_fac[p.var_fac_off[v] + j];
+        if (first || (want_max ? f > best : f < best)) best = f;
+        first = false;
+      }
+      fac[e] = best;
+    }
+  }
+}
+
+// CPython 3.12 sum() of floats
+static double host_pysum(const double* x, int n) {
+  if (n == 0) return 0.0;
+  double f = 0.0 + x[0], c = 0.0;
+  for (int i = 1; i < n; ++i) {
+    double t = f + x[i];
+    if (std::fabs(f) >= std::fabs(x[i])) c += (f - t) + x[i];
+    else c += (x[i] - t) + f;
+    f = t;
+  }
+  if (c != 0.0 && std::isfinite(c)) f += c;
+  return f;
+}
+
+static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_probe& in,
+                       DProbe& o) {
+  memset(&o, 0, sizeof(o));
+  o.demand = in.demand;
+  o.slo_eff = in.slo_eff;
+  o.acc_slo = in.acc_slo;
+  o.alpha = in.alpha;
+  o.beta = in.beta;
+  double fac[MAXE], r[MAXT];
+  for (int a = 0; a < 2; ++a) {
+    host_factors(p, rq, a == 1, true, fac);
+    host_rates(p, in.demand, fac, r);
+    for (int t = 0; t < p.T; ++t) o.r_upper[a][t] = r[t];
+  }
+  host_factors(p, rq, (rq.space & JSV_SPACE_A) != 0, false, fac);
+  host_rates(p, in.demand, fac, r);
+  o.could_zero = 0;
+  for (int t = 0; t < p.T; ++t)
+    if (r[t] == 0.0) o.could_zero |= 1u << t;
+  for (int t = 0; t < p.T; ++t) {
+    o.lat_budget[t] = in.uni_lat_budget[t];
+    o.floor_[t] = in.uni_floor[t];
+    o.weight[t] = in.uni_weight[t];
+    o.best_hput[t] = in.uni_best_hput[t];
+    o.best_slices[t] = in.uni_best_slices[t];
+    o.min_cost[t] = in.uni_min_cost[t];
+  }
+  if (!(rq.space & JSV_SPACE_T)) {
+    // plan_uninformed demand-dependent budgets (planner.py:1014-1037)
+    host_factors(p, rq, false, true, fac);
+    host_rates(p, in.demand, fac, r);
+    double est[MAXT], est_decl[MAXT];
+    for (int t = 0; t < p.T; ++t) {
+      o.star[t] = r[t];
+      est[t] = r[t] / o.best_hput[t] * (double)o.best_slices[t];
+    }
+    for (int i = 0; i < p.T; ++i) est_decl[i] = est[p.decl[i]];
+    const double tot = host_pysum(est_decl, p.T);
+    for (int t = 0; t < p.T; ++t) {
+      double sb = tot > 0 ? (double)rq.budget * est[t] / tot : (double)rq.budget / (double)p.T;
+      if ((double)o.min_cost[t] > sb) sb = (double)o.min_cost[t];
+      o.slice_budget[t] = sb;
+    }
+  }
+}
+
+static void fill_req(const jsv_problem& p, const jsv_request& rq, DReq& o) {
+  memset(&o, 0, sizeof(o));
+  o.S = rq.budget;
+  o.space = rq.space;
+  o.slack = rq.slack;
+  o.eps = rq.eps;
+  o.W = rq.pareto_width;
+  o.n_mix = rq.n_mix;
+  for (int i = 0; i < rq.n_mix && i < JSV_MAX_MIX; ++i) o.mix[i] = rq.mix[i];
+  o.feasible_only = rq.feasible_only;
+  for (int e = 0; e < p.E; ++e) {
+    o.has_ov[e] = rq.has_override ? rq.has_override[e] : 0;
+    o.ov[e] = (rq.has_override && rq.has_override[e]) ? rq.override_val[e] : 0.0;
+  }
+}
+
+// _enumeration_size (planner.py:435-457): count vectors within budget, early exit
+static long long enumeration_size(const std::vector<int>& costs, int S, int limit) {
+  std::vector<long long> ways(S + 1, 0), nw(S + 1);
+  ways[0] = 1;
+  for (int cost : costs) {
+    std::fill(nw.begin(), nw.end(), 0);
+    for (int used = 0; used <= S; ++used) {
+      if (!ways[used]) continue;
+      for (int spent = used; spent <= S; spent += cost) nw[spent] += ways[used];
+    }
+    ways.swap(nw);
+    long long s = 0;
+    for (long long w : ways) s += w;
+    if (s > limit) return (long long)limit + 1;
+  }
+  long long s = 0;
+  for (long long w : ways) s += w;
+  return s;
+}
+
+static int build_s1plan(const jsv_problem& p, const jsv_request& rq, S1Plan& pl) {
+  const int S = rq.budget;
+  const bool A = rq.space & JSV_SPACE_A, Sp = rq.space & JSV_SPACE_S;
+  pl.task_cap.assign(p.T, 0);
+  pl.maxi = 2;
+  int unit = 0;
+  for (int t = 0; t < p.T; ++t) {
+    for (int a = 0; a <= (A ? 1 : 0); ++a) {
+      for (int s = 0; s <= (Sp ? 1 : 0); ++s) {
+        const int sub = t * 4 + 2 * a + s;
+        const int n = p.sub_off[sub + 1] - p.sub_off[sub];
+        if (n == 0) continue;
+        GenDesc d{};
+        d.task = t; d.sub = sub; d.a = a;
+        d.n_tuples = n; d.key_base = p.sub_off[sub];
+        d.grp_base = p.grp_off[sub];
+        d.n_groups = p.grp_off[sub + 1] - p.grp_off[sub];
+        d.unit_off = unit;
+        std::vector<int> costs(n);
+        for (int i = 0; i < n; ++i)
+          costs[i] = p.key_cost[p.key_off[t] + p.sub_key[p.sub_off[sub] + i]];
+        const long long size = enumeration_size(costs, S, rq.exhaustive_limit);
+        if (size <= rq.exhaustive_limit) {
+          d.mode = 0;
+          d.w_off = (int)pl.ways.size();
+          // suffix ways W[i][l] and max item count
+          std::vector<unsigned> W((size_t)(n + 1) * (S + 1), 0);
+          std::vector<int> mx((size_t)(n + 1) * (S + 1), 0);
+          for (int l = 0; l <= S; ++l) W[(size_t)n * (S + 1) + l] = 1;
+          for (int i = n - 1; i >= 0; --i)
+            for (int l = 0; l <= S; ++l) {
+              unsigned long long acc = 0;
+              int best = 0;
+              for (int c = 0; c * costs[i] <= l; ++c) {
+                acc += W[(size_t)(i + 1) * (S + 1) + l - c * costs[i]];
+                best = std::max(best, (c > 0) + mx[(size_t)(i + 1) * (S + 1) + l - c * costs[i]]);
+              }
+              W[(size_t)i * (S + 1) + l] = (unsigned)std::min<unsigned long long>(acc, 0xFFFFFFFFull);
+              mx[(size_t)i * (S + 1) + l] = best;
+            }
+          if (W[S] != (unsigned)size) return fail(JSV_ERR_CONFIG, "enumeration size mismatch");
+          const int items = mx[S];
+          if (items > MAXI) return fail(JSV_ERR_CONFIG, "exhaustive bundles exceed 16 items");
+          pl.maxi = std::max(pl.maxi, items);
+          pl.ways.insert(pl.ways.end(), W.begin(), W.end());
+          d.n_units = (int)size - 1;
+          d.n_tuple_units = 0;
+          d.n_mix_units = 0;
+          pl.task_cap[t] += size - 1;
+        } else {
+          d.mode = 1;
+          d.n_tuple_units = n;
+          const int G = d.n_groups;
+          d.n_mix_units = (G * (G - 1) / 2) * rq.n_mix * N_LEVELS * 4;
+          d.n_units = d.n_tuple_units + d.n_mix_units;
+          pl.task_cap[t] += (long long)n * (N_LEVELS + 1) + d.n_mix_units;
+        }
+        unit += d.n_units;
+        pl.desc.push_back(d);
+      }
+    }
+  }
+  pl.U = unit;
+  pl.C_probe = 0;
+  pl.max_cap = 0;
+  pl.tile_task.clear();
+  pl.tile_start.clear();
+  for (int t = 0; t < p.T; ++t) {
+    pl.C_probe += pl.task_cap[t];
+    pl.max_cap = std::max(pl.max_cap, pl.task_cap[t]);
+    for (long long s0 = 0; s0 < pl.task_cap[t]; s0 += 256) {
+      pl.tile_task.push_back(t);
+      pl.tile_start.push_back((int)s0);
+    }
+  }
+  if (pl.ways.empty()) pl.ways.push_back(0);
+  return JSV_OK;
+}
+
+static int get_s1plan(jsv_problem& p, const jsv_request& rq, std::shared_ptr<S1Plan>& out) {
+  auto key = std::make_tuple(rq.budget, rq.space & 3u, rq.exhaustive_limit, rq.n_mix);
+  auto it = p.s1cache.find(key);
+  if (it != p.s1cache.end()) {
+    out = it->second;
+    return JSV_OK;
+  }
+  auto pl = std::make_shared<S1Plan>();
+  int rc = build_s1plan(p, rq, *pl);
+  if (rc) return rc;
+  p.s1cache[key] = pl;
+  out = pl;
+  return JSV_OK;
+}
+
+// ------------------------------------------------------------- batch solve
+
+struct BatchState {
+  int n = 0;
+  std::shared_ptr<S1Plan> pl;
+  S1Args s1{};
+  std::vector<int> pool_n;
+  std::vector<int> dead;
+  std::vector<DProbe> probes;
+};
+
+static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe* probes,
+                      BatchState& bs) {
+  jsv_context& c = *p.ctx;
+  cudaStream_t st = c.st;
+  int rc = get_s1plan(p, rq, bs.pl);
+  if (rc) return rc;
+  const S1Plan& pl = *bs.pl;
+  const int T = p.T;
+  const int W = rq.pareto_width;
+  const int D = stage1_padded_dims(4 + p.maxout);
+  const long long Ctot = (long long)n * pl.C_probe;
+  const long long jobs = (long long)n * T;
+  DReq hreq;
+  fill_req(p, rq, hreq);
+  auto& B = c.buf;
+  CK(B[B_REQ].ensure(sizeof(DReq)));
+  CK(cudaMemcpyAsync(B[B_REQ].p, &hreq, sizeof(DReq), cudaMemcpyHostToDevice, st));
+  CK(B[B_PROBES].ensure(sizeof(DProbe) * n));
+  CK(cudaMemcpyAsync(B[B_PROBES].p, probes, sizeof(DProbe) * n, cudaMemcpyHostToDevice, st));
+  CK(B[B_DESC].ensure(sizeof(GenDesc) * std::max<size_t>(1, pl.desc.size())));
+  if (!pl.desc.empty())
+    CK(cudaMemcpyAsync(B[B_DESC].p, pl.desc.data(), sizeof(GenDesc) * pl.desc.size(),
+                       cudaMemcpyHostToDevice, st));
+  CK(B[B_WAYS].ensure(sizeof(unsigned) * pl.ways.size()));
+  CK(cudaMemcpyAsync(B[B_WAYS].p, pl.ways.data(), sizeof(unsigned) * pl.ways.size(),
+                     cudaMemcpyHostToDevice, st));
+  CK(B[B_TILE_TASK].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_task.size())));
+  CK(B[B_TILE_START].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_start.size())));
+  if (!pl.tile_task.empty()) {
+    CK(cudaMemcpyAsync(B[B_TILE_TASK].p, pl.tile_task.data(), sizeof(int) * pl.tile_task.size(),
+                       cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size(),
+                       cudaMemcpyHostToDevice, st));
+  }
+  const size_t C1 = (size_t)std::max<long long>(1, Ctot);
+  CK(B[B_ITEMS].ensure(sizeof(uint32_t) * C1 * pl.maxi));
+  CK(B[B_NITEMS].ensure(sizeof(int) * C1));
+  CK(B[B_ARR].ensure(sizeof(double) * C1 * D));
+  CK(B[B_SL].ensure(sizeof(int) * C1));
+  CK(B[B_FLAG].ensure(sizeof(unsigned) * C1));
+  CK(B[B_FRONT].ensure(sizeof(int) * C1));
+  CK(B[B_FPOS].ensure(sizeof(int) * C1));
+  CK(B[B_FCR].ensure(sizeof(int) * C1));
+  CK(B[B_SORTED].ensure(sizeof(int) * C1));
+  CK(B[B_SCR].ensure(sizeof(int) * C1));
+  CK(B[B_CNT].ensure(sizeof(int) * jobs));
+  CK(B[B_FCNT].ensure(sizeof(int) * jobs));
+  CK(B[B_POOLC].ensure(sizeof(int) * jobs * W));
+  CK(B[B_POOLN].ensure(sizeof(int) * jobs));
+  CK(B[B_POOLT].ensure(sizeof(int) * jobs));
+  CK(B[B_PSL].ensure(sizeof(int) * jobs * W));
+  CK(B[B_PCAP].ensure(sizeof(double) * jobs * W));
+  CK(B[B_PACC].ensure(sizeof(double) * jobs * W));
+  CK(B[B_PLAT].ensure(sizeof(double) * jobs * W));
+  CK(B[B_PFAN].ensure(sizeof(double) * jobs * W * p.maxout));
+  CK(B[B_RANKP].ensure(sizeof(uint16_t) * jobs * (W + 1)));
+  CK(B[B_RANKM].ensure(sizeof(uint16_t) * jobs * (W + 1)));
+  CK(B[B_S1LAT2].ensure(sizeof(double) * jobs));
+  CK(B[B_S1SL].ensure(sizeof(int) * jobs));
+  CK(B[B_S1ACC].ensure(sizeof(double) * jobs));
+  CK(B[B_ERR].ensure(sizeof(int)));
+  CK(cudaMemsetAsync(B[B_CNT].p, 0, sizeof(int) * jobs, st));
+  CK(cudaMemsetAsync(B[B_ERR].p, 0, sizeof(int), st));
+  S1Args& a = bs.s1;
+  memset(&a, 0, sizeof(a));
+  a.g = p.dgraph.as<DGraph>();
+  a.tb = p.dt;
+  a.rq = B[B_REQ].as<DReq>();
+  a.probes = B[B_PROBES].as<DProbe>();
+  a.n_probes = n; a.T = T; a.maxi = pl.maxi; a.D = D; a.W = W; a.maxout = p.maxout;
+  a.C_probe = pl.C_probe;
+  long long acc = 0;
+  for (int t = 0; t < T; ++t) {
+    a.task_base[t] = acc;
+    a.task_cap[t] = pl.task_cap[t];
+    acc += pl.task_cap[t];
+  }
+  a.task_base[T] = acc;
+  a.desc = B[B_DESC].as<GenDesc>();
+  a.n_desc = (int)pl.desc.size();
+  a.U = pl.U;
+  a.ways = B[B_WAYS].as<unsigned>();
+  a.items = B[B_ITEMS].as<uint32_t>();
+  a.nitems = B[B_NITEMS].as<int>();
+  a.arr = B[B_ARR].as<double>();
+  a.sl = B[B_SL].as<int>();
+  a.flag = B[B_FLAG].as<unsigned>();
+  a.cnt = B[B_CNT].as<int>();
+  a.front = B[B_FRONT].as<int>();
+  a.fcnt = B[B_FCNT].as<int>();
+  a.fpos = B[B_FPOS].as<int>();
+  a.fcr = B[B_FCR].as<int>();
+  a.sorted = B[B_SORTED].as<int>();
+  a.scr = B[B_SCR].as<int>();
+  a.pool_cand = B[B_POOLC].as<int>();
+  a.pool_n = B[B_POOLN].as<int>();
+  a.pool_trunc = B[B_POOLT].as<int>();
+  a.p_sl = B[B_PSL].as<int>();
+  a.p_cap = B[B_PCAP].as<double>();
+  a.p_acc = B[B_PACC].as<double>();
+  a.p_lat = B[B_PLAT].as<double>();
+  a.p_fan = B[B_PFAN].as<double>();
+  a.rank_p = B[B_RANKP].as<uint16_t>();
+  a.rank_m = B[B_RANKM].as<uint16_t>();
+  a.pool_min_lat2 = B[B_S1LAT2].as<double>();
+  a.pool_min_sl = B[B_S1SL].as<int>();
+  a.pool_acc_ub = B[B_S1ACC].as<double>();
+  a.err = B[B_ERR].as<int>();
+  S1Launch L{};
+  L.tile_task = B[B_TILE_TASK].as<int>();
+  L.tile_start = B[B_TILE_START].as<int>();
+  L.tiles_pp = (int)pl.tile_task.size();
+  L.jchunk_a = 1024;
+  L.jchunks_a = (int)std::max<long long>(1, (pl.max_cap + L.jchunk_a - 1) / L.jchunk_a);
+  L.jchunk_b = 1024;
+  L.jchunks_b = L.jchunks_a;
+  c.stats.kernel_launches += launch_stage1(a, L, st);
+  CK(cudaGetLastError());
+  bs.n = n;
+  bs.pool_n.resize(jobs);
+  CK(cudaMemcpyAsync(bs.pool_n.data(), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, a.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err) return fail(JSV_ERR_CAPACITY, "stage-1 candidate capacity exceeded (code " +
+                                             std::to_string(err) + ")");
+  bs.dead.assign(n, 0);
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < T; ++k) {
+      const int t = p.topo[k];
+      if (bs.pool_n[(size_t)i * T + t] == 0 && !((probes[i].could_zero >> t) & 1u)) {
+        bs.dead[i] = 1;
+        break;
+      }
+    }
+  return JSV_OK;
+}
+
+static void s2_base(jsv_problem& p, BatchState& bs, S2Args& a) {
+  jsv_context& c = *p.ctx;
+  auto& B = c.buf;
+  memset(&a, 0, sizeof(a));
+  a.g = p.dgraph.as<DGraph>();
+  a.rq = B[B_REQ].as<DReq>();
+  a.probes = B[B_PROBES].as<DProbe>();
+  a.n_probes = bs.n;
+  a.T = p.T;
+  a.W = bs.s1.W;
+  a.maxout = p.maxout;
+  a.pool_n = bs.s1.pool_n;
+  a.p_sl = bs.s1.p_sl;
+  a.p_cap = bs.s1.p_cap;
+  a.p_acc = bs.s1.p_acc;
+  a.p_lat = bs.s1.p_lat;
+  a.p_fan = bs.s1.p_fan;
+  a.rank_p = bs.s1.rank_p;
+  a.rank_m = bs.s1.rank_m;
+  a.min_lat2 = B[B_S2LAT2].as<double>();
+  a.min_sl = B[B_S2SL].as<int>();
+  a.acc_ub = B[B_S2ACC].as<double>();
+  a.future = B[B_FUT].as<int>();
+  a.best = B[B_BEST].as<BestRec>();
+  a.err = B[B_ERR].as<int>();
+}
+
+// Level-synchronous search over the active probes (T-informed plans).
+static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_config,
+                      const std::vector<int>& active, long long* nodes_out) {
+  jsv_context& c = *p.ctx;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  const int n = bs.n, T = p.T;
+  S2Args a;
+  s2_base(p, bs, a);
+  a.diag = diag ? 1 : 0;
+  a.want_config = want_config ? 1 : 0;
+  std::vector<long long> fcount(n, 0);
+  for (int i = 0; i < n; ++i) fcount[i] = (active[i] && !bs.dead[i]) ? 1 : 0;
+  std::vector<long long> foff(n), woff(n + 1), nxt_off(n), nxt_cap(n);
+  std::vector<int> width(n);
+  // level-0 frontier: one empty prefix per active probe
+  long long F = 0;
+  for (int i = 0; i < n; ++i) { foff[i] = F; F += fcount[i]; }
+  CK(B[B_FR0].ensure(sizeof(uint16_t) * std::max<long long>(1, F) * T));
+  CK(cudaMemsetAsync(B[B_FR0].p, 0xFF, sizeof(uint16_t) * std::max<long long>(1, F) * T, st));
+  DevBuf* cur = &B[B_FR0];
+  DevBuf* nxt = &B[B_FR1];
+  long long nodes = 0;
+  for (int L = 0; L < T; ++L) {
+    const bool last = (L == T - 1);
+    const int t = p.topo[L];
+    long long total = 0;
+    for (int i = 0; i < n; ++i) {
+      width[i] = std::max(1, bs.pool_n[(size_t)i * T + t]);
+      woff[i] = total;
+      total += fcount[i] * width[i];
+      nodes += fcount[i];
+    }
+    woff[n] = total;
+    if (total == 0) break;
+    long long NO = 0;
+    for (int i = 0; i < n; ++i) {
+      nxt_off[i] = NO;
+      nxt_cap[i] = last ? 0 : fcount[i] * width[i];
+      NO += nxt_cap[i];
+    }
+    CK(B[B_WOFF].ensure(sizeof(long long) * (n + 1)));
+    CK(B[B_FOFF].ensure(sizeof(long long) * n));
+    CK(B[B_WIDTH].ensure(sizeof(int) * n));
+    CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
+    CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
+    CK(B[B_NXTCNT].ensure(sizeof(unsigned long long) * n));
+    CK(cudaMemcpyAsync(B[B_WOFF].p, woff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_FOFF].p, foff.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_WIDTH].p, width.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_NXTOFF].p, nxt_off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_NXTCAP].p, nxt_cap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(B[B_NXTCNT].p, 0, sizeof(unsigned long long) * n, st));
+    if (!last) CK(nxt->ensure(sizeof(uint16_t) * std::max<long long>(1, NO) * T));
+    if (diag) {
+      CK(B[B_FLAGS].ensure(sizeof(int) * std::max<long long>(1, F)));
+      CK(cudaMemsetAsync(B[B_FLAGS].p, 0, sizeof(int) * std::max<long long>(1, F), st));
+    }
+    a.level = L;
+    a.last = last ? 1 : 0;
+    a.woff = B[B_WOFF].as<long long>();
+    a.foff = B[B_FOFF].as<long long>();
+    a.width = B[B_WIDTH].as<int>();
+    a.cur = cur->as<uint16_t>();
+    a.cur_flag = B[B_FLAGS].as<int>();
+    a.nxt = last ? nullptr : nxt->as<uint16_t>();
+    a.nxt_cnt = B[B_NXTCNT].as<unsigned long long>();
+    a.nxt_off = B[B_NXTOFF].as<long long>();
+    a.nxt_cap = B[B_NXTCAP].as<long long>();
+    a.total_work = total;
+    c.stats.kernel_launches += launch_stage2_level(a, st);
+    CK(cudaGetLastError());
+    if (diag && F > 0) {
+      std::vector<int> pp(F);
+      for (int i = 0; i < n; ++i)
+        for (long long k = 0; k < fcount[i]; ++k) pp[foff[i] + k] = i;
+      CK(B[B_PPROBE].ensure(sizeof(int) * F));
+      CK(cudaMemcpyAsync(B[B_PPROBE].p, pp.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st));
+      c.stats.kernel_launches += launch_stage2_blocked(a, F, B[B_PPROBE].as<int>(), st);
+      CK(cudaStreamSynchronize(st));  // pp is host-local
+    }
+    if (last) break;
+    std::vector<unsigned long long> cnt(n);
+    CK(cudaMemcpyAsync(cnt.data(), B[B_NXTCNT].p, sizeof(unsigned long long) * n,
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // compact the next frontier in place: regions are [nxt_off, nxt_off + cnt)
+    F = 0;
+    for (int i = 0; i < n; ++i) {
+      fcount[i] = (long long)cnt[i];
+      foff[i] = nxt_off[i];
+      F = std::max(F, nxt_off[i] + fcount[i]);
+    }
+    std::swap(cur, nxt);
+  }
+  int err = 0;
+  CK(cudaMemcpyAsync(&err, B[B_ERR].p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (err) return fail(JSV_ERR_CAPACITY, "stage-2 frontier capacity exceeded");
+  if (nodes_out) *nodes_out += nodes;
+  return JSV_OK;
+}
+
+static int stage2_prep(jsv_problem& p, BatchState& bs) {
+  jsv_context& c = *p.ctx;
+  auto& B = c.buf;
+  const long long jobs = (long long)bs.n * p.T;
+  CK(B[B_S2LAT2].ensure(sizeof(double) * jobs));
+  CK(B[B_S2SL].ensure(sizeof(int) * jobs));
+  CK(B[B_S2ACC].ensure(sizeof(double) * jobs));
+  CK(B[B_FUT].ensure(sizeof(int) * bs.n * (p.T + 1)));
+  CK(B[B_BEST].ensure(sizeof(BestRec) * bs.n));
+  S2Args a;
+  s2_base(p, bs, a);
+  a.min_lat2 = bs.s1.pool_min_lat2;
+  a.min_sl = bs.s1.pool_min_sl;
+  a.acc_ub = bs.s1.pool_acc_ub;
+  c.stats.kernel_launches += launch_stage2_prep(a, B[B_S2LAT2].as<double>(), B[B_S2SL].as<int>(),
+                                                B[B_S2ACC].as<double>(), B[B_FUT].as<int>(), c.st);
+  CK(cudaGetLastError());
+  return JSV_OK;
+}
+
+static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_out* out,
+                    const std::vector<long long>* nodes) {
+  jsv_context& c = *p.ctx;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  const int n = bs.n;
+  CK(B[B_DEAD].ensure(sizeof(int) * n));
+  CK(cudaMemcpyAsync(B[B_DEAD].p, bs.dead.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  CK(B[B_OUT].ensure(sizeof(jsv_plan_out) * n));
+  FinArgs f{};
+  f.g = p.dgraph.as<DGraph>();
+  f.tb = p.dt;
+  f.rq = B[B_REQ].as<DReq>();
+  f.probes = B[B_PROBES].as<DProbe>();
+  f.n_probes = n; f.T = p.T; f.W = bs.s1.W; f.maxi = bs.s1.maxi; f.maxout = p.maxout;
+  f.C_probe = bs.s1.C_probe;
+  for (int t = 0; t <= p.T; ++t) f.task_base[t] = bs.s1.task_base[t];
+  f.pool_n = bs.s1.pool_n;
+  f.pool_trunc = bs.s1.pool_trunc;
+  f.pool_cand = bs.s1.pool_cand;
+  f.items = bs.s1.items;
+  f.nitems = bs.s1.nitems;
+  f.p_sl = bs.s1.p_sl;
+  f.p_cap = bs.s1.p_cap;
+  f.p_acc = bs.s1.p_acc;
+  f.p_lat = bs.s1.p_lat;
+  f.p_fan = bs.s1.p_fan;
+  f.best = B[B_BEST].as<BestRec>();
+  f.dead = B[B_DEAD].as<int>();
+  f.uninformed = uninformed ? 1 : 0;
+  f.pick = B[B_PICK].as<int>();
+  f.uni_kills = B[B_UKILL].as<int>();
+  f.out = B[B_OUT].as<jsv_plan_out>();
+  if (uninformed) {
+    const long long jobs = (long long)n * p.T;
+    CK(B[B_PICK].ensure(sizeof(int) * jobs));
+    CK(B[B_UKILL].ensure(sizeof(int) * jobs * 5));
+    CK(B[B_BEST].ensure(sizeof(BestRec) * n));
+    CK(cudaMemsetAsync(B[B_BEST].p, 0, sizeof(BestRec) * n, st));
+    f.pick = B[B_PICK].as<int>();
+    f.uni_kills = B[B_UKILL].as<int>();
+    f.best = B[B_BEST].as<BestRec>();
+    S2Args a;
+    s2_base(p, bs, a);
+    c.stats.kernel_launches +=
+        launch_uninformed(a, f, B[B_PICK].as<int>(), B[B_UKILL].as<int>(), st);
+  }
+  c.stats.kernel_launches += launch_finalize(f, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, f.out, sizeof(jsv_plan_out) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (nodes)
+    for (int i = 0; i < n; ++i) out[i].nodes = (*nodes)[i];
+  return JSV_OK;
+}
+
+// plan() for a batch of probes sharing one request
+static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, const jsv_probe* in,
+                               jsv_plan_out* out, bool want_config) {
+  jsv_context& c = *p.ctx;
+  cudaStream_t st = c.st;
+  if (rq.pareto_width < 1 || rq.pareto_width > 32766) return fail(JSV_ERR_ARG, "pareto_width");
+  if (rq.n_mix < 0 || rq.n_mix > JSV_MAX_MIX) return fail(JSV_ERR_ARG, "too many mix fractions");
+  BatchState bs;
+  bs.probes.resize(n);
+  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], bs.probes[i]);
+  CK(cudaEventRecord(c.ev[0], st));
+  int rc = run_stage1(p, rq, n, bs.probes.data(), bs);
+  if (rc) return rc;
+  CK(cudaEventRecord(c.ev[1], st));
+  const bool informed = (rq.space & JSV_SPACE_T) != 0;
+  std::vector<long long> nodes(n, 0);
+  if (informed) {
+    rc = stage2_prep(p, bs);
+    if (rc) return rc;
+    std::vector<int> active(n, 1);
+    long long nn = 0;
+    rc = run_stage2(p, bs, false, want_config, active, &nn);
+    if (rc) return rc;
+    c.stats.nodes += nn;
+    // infeasible full plans: diagnostic re-run for the binding constraint
+    std::vector<BestRec> best(n);
+    CK(cudaMemcpyAsync(best.data(), c.buf[B_BEST].p, sizeof(BestRec) * n, cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> redo(n, 0);
+    bool any = false;
+    for (int i = 0; i < n; ++i) {
+      if (!best[i].has && !bs.dead[i] && want_config) {
+        redo[i] = 1;
+        any = true;
+      }
+      c.stats.leaves += (long long)best[i].leaves;
+    }
+    if (any) {
+      rc = run_stage2(p, bs, true, want_config, redo, nullptr);
+      if (rc) return rc;
+    }
+  }
+  CK(cudaEventRecord(c.ev[2], st));
+  rc = finalize(p, bs, !informed, out, &nodes);
+  if (rc) return rc;
+  CK(cudaEventRecord(c.ev[3], st));
+  CK(cudaEventSynchronize(c.ev[3]));
+  float ms1 = 0, ms2 = 0, mst = 0;
+  cudaEventElapsedTime(&ms1, c.ev[0], c.ev[1]);
+  cudaEventElapsedTime(&ms2, c.ev[1], c.ev[2]);
+  cudaEventElapsedTime(&mst, c.ev[0], c.ev[3]);
+  c.stats.ms_stage1 += ms1;
+  c.stats.ms_stage2 += ms2;
+  c.stats.ms_total += mst;
+  long long gen = 0;
+  {
+    std::vector<int> cnt((size_t)n * p.T);
+    CK(cudaMemcpy(cnt.data(), bs.s1.cnt, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost));
+    for (int v : cnt) gen += v;
+  }
+  c.stats.candidates_generated += gen;
+  return JSV_OK;
+}
+
+extern "C" int jsv_plan_batch(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                              int32_t n, const jsv_probe* probes, jsv_plan_out* out) {
+  if (!ctx || !prob || !req || !probes || !out || n < 0) return fail(JSV_ERR_ARG, "null argument");
+  if (n == 0) return JSV_OK;
+  CK(cudaSetDevice(ctx->device));
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  return plan_batch_internal(*const_cast<jsv_problem*>(prob), *req, n, probes, out, true);
+}
+
+extern "C" int jsv_last_stats(jsv_context* ctx, jsv_stats* out) {
+  if (!ctx || !out) return fail(JSV_ERR_ARG, "null argument");
+  *out = ctx->stats;
+  return JSV_OK;
+}
+
+// ------------------------------------------------------------- max_demand
+
+struct PointState {
+  double lo = 0, hi = 0;
+  int phase = 0;  // 0 start, 1 doubling, 2 bisection, 3 done
+  int probes = 0;
+  int status = 0;
+};
+
+extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
+                                    const jsv_request* req, int32_t n, const jsv_probe* points,
+                                    double rel_tol, jsv_demand_out* out, jsv_plan_out* plans) {
+  if (!ctx || !prob || !req || !points || !out || n < 0) return fail(JSV_ERR_ARG, "null argument");
+  if (req->budget <= 0) return fail(JSV_ERR_CONFIG, "slice budget must be positive");
+  if (n == 0) return JSV_OK;
+  CK(cudaSetDevice(ctx->device));
+  memset(&ctx->stats, 0, sizeof(ctx->stats));
+  jsv_problem& p = *const_cast<jsv_problem*>(prob);
+  jsv_request preq = *req;
+  preq.feasible_only = 1;
+  std::vector<PointState> ps(n);
+  std::vector<long long> gpu_probes(n, 0);
+  const double tiny = 1e-6;
+  // speculative evaluation helper: run the listed (point, demand) probes
+  auto run = [&](const std::vector<std::pair<int, double>>& work, std::vector<int>& feas) -> int {
+    std::vector<jsv_probe> pr(work.size());
+    for (size_t k = 0; k < work.size(); ++k) {
+      pr[k] = points[work[k].first];
+      pr[k].demand = work[k].second;
+      gpu_probes[work[k].first]++;
+    }
+    std::vector<jsv_plan_out> res(work.size());
+    int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.data(), false);
+    if (rc) return rc;
+    feas.resize(work.size());
+    for (size_t k = 0; k < work.size(); ++k) feas[k] = res[k].feasible;
+    return JSV_OK;
+  };
+  // step 1: tiny and 1.0 (planner.py:1152-1157)
+  {
+    std::vector<std::pair<int, double>> w;
+    for (int i = 0; i < n; ++i) {
+      w.push_back({i, tiny});
+      w.push_back({i, 1.0});
+    }
+    std::vector<int> f;
+    int rc = run(w, f);
+    if (rc) return rc;
+    for (int i = 0; i < n; ++i) {
+      PointState& s = ps[i];
+      s.probes = 1;
+      if (!f[2 * i]) {
+        s.status = 1;
+        s.phase = 3;
+        s.lo = 0.0;
+        continue;
+      }
+      s.probes = 2;
+      if (f[2 * i + 1]) {
+        s.lo = 1.0; s.hi = 2.0; s.phase = 1;
+      } else {
+        s.lo = tiny; s.hi = 1.0; s.phase = 2;
+      }
+    }
+  }
+  const int budget_probes = 4096;
+  while (true) {
+    int active = 0;
+    for (auto& s : ps) active += (s.phase == 1 || s.phase == 2);
+    if (!active) break;
+    int depth = 1;
+    while (depth < 8 && (long long)active * ((1 << (depth + 1)) - 1) <= budget_probes) ++depth;
+    std::vector<std::pair<int, double>> w;
+    std::vector<std::vector<double>> tree(n);
+    for (int i = 0; i < n; ++i) {
+      PointState& s = ps[i];
+      if (s.phase == 1) {
+        // speculative doubling: hi, 2hi, 4hi, ...
+        const int k = std::max(2, depth + 2);
+        double h = s.hi;
+        for (int j = 0; j < k && h <= std::ldexp(1.0, 61); ++j) {
+          w.push_back({i, h});
+          tree[i].push_back(h);
+          h *= 2.0;
+        }
+      } else if (s.phase == 2) {
+        // complete bisection subtree of the given depth (heap order)
+        std::vector<std::pair<double, double>> nodes{{s.lo, s.hi}};
+        std::vector<double>& mids = tree[i];
+        mids.clear();
+        for (int lvl = 0; lvl < depth; ++lvl) {
+          std::vector<std::pair<double, double>> nxtn;
+          for (auto& nd : nodes) {
+            double lo = nd.first, hi = nd.second;
+            double mid = NAN;
+            if (!std::isnan(lo) && hi - lo > rel_tol * lo) {
+              mid = (lo + hi) / 2.0;
+              if (mid <= lo || mid >= hi) mid = NAN;
+            }
+            mids.push_back(mid);
+            if (!std::isnan(mid)) w.push_back({i, mid});
+            // children: feasible -> (mid, hi), infeasible -> (lo, mid)
+            if (std::isnan(mid)) {
+              nxtn.push_back({NAN, NAN});
+              nxtn.push_back({NAN, NAN});
+            } else {
+              nxtn.push_back({mid, hi});
+              nxtn.push_back({lo, mid});
+            }
+          }
+          nodes.swap(nxtn);
+        }
+      }
+    }
+    std::vector<int> f;
+    int rc = run(w, f);
+    if (rc) return rc;
+    // replay decisions exactly (planner.py:1157-1173)
+    size_t cursor = 0;
+    for (int i = 0; i < n; ++i) {
+      PointState& s = ps[i];
+      if (s.phase == 1) {
+        const size_t cnt = tree[i].size();
+        size_t k = 0;
+        bool stopped = false;
+        for (; k < cnt; ++k) {
+          s.probes++;
+          if (f[cursor + k]) {
+            s.lo = s.hi;
+            s.hi *= 2.0;
+            if (s.hi > std::ldexp(1.0, 60)) {
+              s.status = 2;
+              s.phase = 3;
+              stopped = true;
+              break;
+            }
+          } else {
+            s.phase = 2;
+            stopped = true;
+            break;
+          }
+        }
+        (void)stopped;
+        cursor += cnt;
+      } else if (s.phase == 2) {
+        // walk the heap-ordered subtree
+        std::vector<double>& mids = tree[i];
+        std::vector<int> fv(mids.size(), 0);
+        size_t q = cursor;
+        for (size_t k = 0; k < mids.size(); ++k)
+          if (!std::isnan(mids[k])) fv[k] = f[q++];
+        cursor = q;
+        size_t node = 0;
+        while (node < mids.size()) {
+          if (!(s.hi - s.lo > rel_tol * s.lo)) { s.phase = 3; break; }
+          const double mid = (s.lo + s.hi) / 2.0;
+          if (mid <= s.lo || mid >= s.hi) { s.phase = 3; break; }
+          s.probes++;
+          if (fv[node]) {
+            s.lo = mid;
+            node = 2 * node + 1;
+          } else {
+            s.hi = mid;
+            node = 2 * node + 2;
+          }
+        }
+        if (s.phase == 2 && !(s.hi - s.lo > rel_tol * s.lo)) s.phase = 3;
+        if (s.phase == 2) {
+          const double mid = (s.lo + s.hi) / 2.0;
+          if (mid <= s.lo || mid >= s.hi) s.phase = 3;
+        }
+      }
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    if (ps[i].status == 2)
+      return fail(JSV_ERR_CONFIG, "demand search diverged; profile throughput looks unbounded");
+  }
+  // final plans with the caller's options (planner.py:1155, 1174)
+  if (plans) {
+    std::vector<jsv_probe> fin(n);
+    for (int i = 0; i < n; ++i) {
+      fin[i] = points[i];
+      fin[i].demand = ps[i].status == 1 ? tiny : ps[i].lo;
+    }
+    int rc = plan_batch_internal(p, *req, n, fin.data(), plans, true);
+    if (rc) return rc;
+  }
+  for (int i = 0; i < n; ++i) {
+    out[i].demand = ps[i].status == 1 ? 0.0 : ps[i].lo;
+    out[i].probes = ps[i].probes;
+    out[i].status = ps[i].status;
+    out[i].gpu_probes = gpu_probes[i];
+  }
+  return JSV_OK;
+}
+
+// --------------------------------------------------------- derive / validate
+
+extern "C" int jsv_derive(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                          const jsv_probe* probe, const int32_t* n_items, const uint32_t* items,
+                          jsv_plan_out* out) {
+  if (!ctx || !prob || !req || !probe || !n_items || !items || !out)
+    return fail(JSV_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jsv_problem& p = *const_cast<jsv_problem*>(prob);
+  auto& B = ctx->buf;
+  cudaStream_t st = ctx->st;
+  DReq hreq;
+  fill_req(p, *req, hreq);
+  DProbe hp;
+  fill_probe(p, *req, *probe, hp);
+  CK(B[B_REQ].ensure(sizeof(DReq)));
+  CK(B[B_PROBES].ensure(sizeof(DProbe)));
+  CK(B[B_DN].ensure(sizeof(int) * MAXT));
+  CK(B[B_DITEMS].ensure(sizeof(uint32_t) * MAXT * MAXI));
+  CK(B[B_OUT].ensure(sizeof(jsv_plan_out)));
+  CK(cudaMemcpyAsync(B[B_REQ].p, &hreq, sizeof(DReq), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_PROBES].p, &hp, sizeof(DProbe), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_DN].p, n_items, sizeof(int) * p.T, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_DITEMS].p, items, sizeof(uint32_t) * p.T * MAXI, cudaMemcpyHostToDevice, st));
+  DeriveArgs a{};
+  a.g = p.dgraph.as<DGraph>();
+  a.tb = p.dt;
+  a.rq = B[B_REQ].as<DReq>();
+  a.probe = B[B_PROBES].as<DProbe>();
+  a.n_items = B[B_DN].as<int>();
+  a.items = B[B_DITEMS].as<uint32_t>();
+  a.out = B[B_OUT].as<jsv_plan_out>();
+  launch_derive(a, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, a.out, sizeof(jsv_plan_out), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return JSV_OK;
+}
+
+extern "C" int jsv_validate(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                            const jsv_probe* probe, const double* latency, const double* capacity,
+                            const double* demand, int32_t total_slices, double a_obj,
+                            uint32_t uncovered_mask, jsv_plan_out* out) {
+  if (!ctx || !prob || !req || !probe || !latency || !capacity || !demand || !out)
+    return fail(JSV_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jsv_problem& p = *const_cast<jsv_problem*>(prob);
+  auto& B = ctx->buf;
+  cudaStream_t st = ctx->st;
+  DReq hreq;
+  fill_req(p, *req, hreq);
+  DProbe hp;
+  fill_probe(p, *req, *probe, hp);
+  CK(B[B_REQ].ensure(sizeof(DReq)));
+  CK(B[B_PROBES].ensure(sizeof(DProbe)));
+  CK(B[B_VAL].ensure(sizeof(double) * 3 * MAXT));
+  CK(B[B_OUT].ensure(sizeof(jsv_plan_out)));
+  double vals[3 * MAXT];
+  for (int t = 0; t < p.T; ++t) {
+    vals[t] = latency[t];
+    vals[MAXT + t] = capacity[t];
+    vals[2 * MAXT + t] = demand[t];
+  }
+  CK(cudaMemcpyAsync(B[B_REQ].p, &hreq, sizeof(DReq), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_PROBES].p, &hp, sizeof(DProbe), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_VAL].p, vals, sizeof(vals), cudaMemcpyHostToDevice, st));
+  ValidateArgs a{};
+  a.g = p.dgraph.as<DGraph>();
+  a.rq = B[B_REQ].as<DReq>();
+  a.probe = B[B_PROBES].as<DProbe>();
+  a.lat = B[B_VAL].as<double>();
+  a.cap = B[B_VAL].as<double>() + MAXT;
+  a.dem = B[B_VAL].as<double>() + 2 * MAXT;
+  a.total_sl = total_slices;
+  a.a_obj = a_obj;
+  a.uncovered = uncovered_mask;
+  a.out = B[B_OUT].as<jsv_plan_out>();
+  launch_validate(a, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, a.out, sizeof(jsv_plan_out), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return JSV_OK;
+}
+
+extern "C" int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                             const jsv_probe* probe, int32_t task, int32_t cap, int32_t* n_out,
+                             int32_t* n_items, uint32_t* items, double* stats, int32_t* truncated) {
+  if (!ctx || !prob || !req || !probe || !n_out) return fail(JSV_ERR_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  jsv_problem& p = *const_cast<jsv_problem*>(prob);
+  if (task < 0 || task >= p.T) return fail(JSV_ERR_ARG, "task index");
+  BatchState bs;
+  bs.probes.resize(1);
+  fill_probe(p, *req, *probe, bs.probes[0]);
+  int rc = run_stage1(p, *req, 1, bs.probes.data(), bs);
+  if (rc) return rc;
+  const S1Args& a = bs.s1;
+  const int P = bs.pool_n[task];
+  *n_out = P;
+  if (truncated) CK(cudaMemcpy(truncated, a.pool_trunc + task, sizeof(int), cudaMemcpyDeviceToHost));
+  if (P > cap) return fail(JSV_ERR_CAPACITY, "output capacity too small");
+  const int W = a.W;
+  const int outd = p.succ_off[task + 1] - p.succ_off[task];
+  std::vector<int> pc(P), sl(P);
+  std::vector<double> capv(P), acc(P), lat(P), fan((size_t)P * p.maxout);
+  const long long q0 = (long long)task * W;
+  if (P > 0) {
+    CK(cudaMemcpy(pc.data(), a.pool_cand + q0, sizeof(int) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sl.data(), a.p_sl + q0, sizeof(int) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(capv.data(), a.p_cap + q0, sizeof(double) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(acc.data(), a.p_acc + q0, sizeof(double) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(lat.data(), a.p_lat + q0, sizeof(double) * P, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(fan.data(), a.p_fan + q0 * p.maxout, sizeof(double) * P * p.maxout,
+                  cudaMemcpyDeviceToHost));
+  }
+  const long long base = a.task_base[task];
+  for (int k = 0; k < P; ++k) {
+    const long long cnd = base + pc[k];
+    int ni = 0;
+    CK(cudaMemcpy(&ni, a.nitems + cnd, sizeof(int), cudaMemcpyDeviceToHost));
+    if (n_items) n_items[k] = ni;
+    if (items) {
+      uint32_t tmp[MAXI] = {0};
+      CK(cudaMemcpy(tmp, a.items + cnd * a.maxi, sizeof(uint32_t) * ni, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < MAXI; ++i) items[(size_t)k * MAXI + i] = tmp[i];
+    }
+    if (stats) {
+      double* s = stats + (size_t)k * (4 + outd);
+      s[0] = (double)sl[k];
+      s[1] = capv[k];
+      s[2] = acc[k];
+      s[3] = lat[k];
+      for (int j = 0; j < outd; ++j) s[4 + j] = fan[(size_t)k * p.maxout + j];
+    }
+  }
+  return JSV_OK;
+}

@@ -1,0 +1,152 @@
+// jsv_kernels.h -- kernel argument blocks and launchers shared by the host runtime.
+#pragma once
+#include "jsv_internal.cuh"
+
+struct S1Args {
+  const DGraph* g;
+  DTables tb;
+  const DReq* rq;
+  const DProbe* probes;
+  int n_probes, T, maxi, D, W, maxout;
+  long long C_probe;
+  long long task_base[MAXT + 1];
+  long long task_cap[MAXT];
+  const GenDesc* desc;
+  int n_desc, U;
+  const unsigned* ways;
+  uint32_t* items;
+  int* nitems;
+  double* arr;
+  int* sl;
+  unsigned* flag;
+  int* cnt;
+  int* front;
+  int* fcnt;
+  int* fpos;
+  int* fcr;
+  int* sorted;
+  int* scr;
+  int* pool_cand;
+  int* pool_n;
+  int* pool_trunc;
+  int* p_sl;
+  double* p_cap;
+  double* p_acc;
+  double* p_lat;
+  double* p_fan;
+  uint16_t* rank_p;
+  uint16_t* rank_m;
+  double* pool_min_lat2;
+  int* pool_min_sl;
+  double* pool_acc_ub;
+  int* err;
+};
+
+struct S1Launch {
+  const int* tile_task;   // device [tiles_pp]
+  const int* tile_start;  // device [tiles_pp]
+  int tiles_pp;
+  int jchunks_a, jchunk_a;
+  int jchunks_b, jchunk_b;
+};
+
+int stage1_padded_dims(int D);
+int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st);
+
+// ------------------------------------------------------------------ stage 2
+
+struct S2Args {
+  const DGraph* g;
+  const DReq* rq;
+  const DProbe* probes;
+  int n_probes, T, W, maxout;
+  // pools (job = probe*T + task, entry = job*W + k)
+  const int* pool_n;
+  const int* p_sl;
+  const double* p_cap;
+  const double* p_acc;
+  const double* p_lat;
+  const double* p_fan;
+  const uint16_t* rank_p;
+  const uint16_t* rank_m;
+  const double* min_lat2;  // [jobs] (0 for could_zero tasks, set by stage2 prep)
+  const int* min_sl;
+  const double* acc_ub;
+  const int* future;       // [n_probes*(T+1)] future_slices by topo position
+  BestRec* best;
+  int* active;             // [n_probes] 1 = search this probe
+  // level expansion
+  int level, last, diag, want_config;
+  const long long* woff;   // [n_probes+1] work offsets
+  const long long* foff;   // [n_probes] frontier base of the current level
+  const int* width;        // [n_probes] options per prefix
+  const uint16_t* cur;     // current frontier choices [*, T] (topo positions)
+  int* cur_flag;           // [*] bit0 = r > 0, bit1 = some child survived
+  uint16_t* nxt;
+  unsigned long long* nxt_cnt;  // [n_probes]
+  const long long* nxt_off;     // [n_probes]
+  const long long* nxt_cap;     // [n_probes]
+  long long total_work;
+  int* err;
+};
+
+int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
+                       cudaStream_t st);
+int launch_stage2_level(const S2Args& a, cudaStream_t st);
+int launch_stage2_blocked(const S2Args& a, long long n_prefix_total, const int* prefix_probe,
+                          cudaStream_t st);
+
+struct FinArgs {
+  const DGraph* g;
+  DTables tb;
+  const DReq* rq;
+  const DProbe* probes;
+  int n_probes, T, W, maxi, maxout;
+  long long C_probe;
+  long long task_base[MAXT + 1];
+  const int* pool_n;
+  const int* pool_trunc;
+  const int* pool_cand;
+  const uint32_t* items;
+  const int* nitems;
+  const int* p_sl;
+  const double* p_cap;
+  const double* p_acc;
+  const double* p_lat;
+  const double* p_fan;
+  const BestRec* best;
+  const int* dead;         // [n_probes]
+  const int* pick;         // [n_probes*T] plan_uninformed picks (-1 none), or null
+  const int* uni_kills;    // [n_probes*T*5]
+  int uninformed;
+  jsv_plan_out* out;
+};
+
+int launch_finalize(const FinArgs& a, cudaStream_t st);
+int launch_uninformed(const S2Args& a, const FinArgs& f, int* pick, int* kills, cudaStream_t st);
+
+// explicit assignment (derive_configuration) and verdicts on given fields
+struct DeriveArgs {
+  const DGraph* g;
+  DTables tb;
+  const DReq* rq;
+  const DProbe* probe;
+  const int* n_items;      // [T]
+  const uint32_t* items;   // [T*MAXI]
+  jsv_plan_out* out;
+};
+int launch_derive(const DeriveArgs& a, cudaStream_t st);
+
+struct ValidateArgs {
+  const DGraph* g;
+  const DReq* rq;
+  const DProbe* probe;
+  const double* lat;
+  const double* cap;
+  const double* dem;
+  int total_sl;
+  double a_obj;
+  uint32_t uncovered;
+  jsv_plan_out* out;
+};
+int launch_validate(const ValidateArgs& a, cudaStream_t st);

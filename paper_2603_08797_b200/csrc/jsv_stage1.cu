@@ -1,0 +1,534 @@
+// jsv_stage1.cu -- Stage 1 on sm_100a: candidate bundles per (probe, task).
+//
+// Replaces reference planner.py:406-635 (_tuples_for, _enumeration_size,
+// _exhaustive_counts, _structured_counts, _stats_for_counts, _pareto_filter,
+// _candidate_pool).  A "job" is one (probe, task) pair; all jobs of a batch run
+// in the same launches:
+//
+//   k_generate   one thread per enumeration unit: exhaustive count vectors are
+//                unranked from a suffix-ways table; structured covers and
+//                2-variant mixes are decoded from the unit index.
+//   k_stats      one thread per candidate: latency / capacity / slices /
+//                weighted accuracy + fan-out (all-equal short circuit).
+//   k_pairs_a    tiled all-pairs skyline: candidate i dies if another
+//                candidate weakly dominates it with a different row, or has an
+//                identical row and smaller items (the reference's dedup).  By
+//                transitivity this equals the reference's sequential
+//                "not dominated by an earlier kept row" filter.
+//   k_compact    survivors -> frontier list.
+//   k_pairs_b    frontier position (lexicographic row order) and capacity
+//                rank (-cap, slices, items) by counting.
+//   k_truncate   frontier order, pareto_width truncation (planner.py:574-583),
+//                pool SoA + per-pool bounds for Stage 2.
+//   k_mrank      per-pool ranks of the item lists with end = -inf / +inf; the
+//                Stage-2 tie-break on m compares these.
+#include <cub/block/block_scan.cuh>
+#include "jsv_internal.cuh"
+#include "jsv_kernels.h"
+
+__constant__ double c_grid[N_LEVELS] = {1.0,    0.75,    0.5,       0.375,    0.25,
+                                        0.1875, 0.125,   0.09375,   0.0625,   0.046875,
+                                        0.03125, 0.0234375, 0.015625, 0.01171875};
+
+// cover(i, dem) of planner.py:503-508: max(1, ceil(dem / H - 1e-12)) if it fits.
+__device__ __forceinline__ int cover_count(double dem, double h, int cost, int S) {
+  double q = dem / h - 1e-12;
+  if (!(q <= (double)S)) return 0;
+  double cq = ceil(q);
+  long long c = (long long)cq;
+  if (c < 1) c = 1;
+  if (c * (long long)cost > S) return 0;
+  return (int)c;
+}
+
+__device__ __forceinline__ long long job_base(const S1Args& a, int probe, int t) {
+  return (long long)probe * a.C_probe + a.task_base[t];
+}
+
+__device__ inline void append_candidate(const S1Args& a, int probe, int t, const uint32_t* it,
+                                        int n) {
+  int job = probe * a.T + t;
+  int pos = atomicAdd(&a.cnt[job], 1);
+  if (pos >= a.task_cap[t]) {
+    atomicExch(a.err, 1);
+    return;
+  }
+  long long c = job_base(a, probe, t) + pos;
+  a.nitems[c] = n;
+  for (int k = 0; k < n; ++k) a.items[c * a.maxi + k] = it[k];
+}
+
+__global__ void k_generate(S1Args a) {
+  long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gtid >= (long long)a.n_probes * a.U) return;
+  const int probe = (int)(gtid / a.U);
+  const int u = (int)(gtid % a.U);
+  int d = 0;
+  while (d + 1 < a.n_desc && a.desc[d + 1].unit_off <= u) ++d;
+  const GenDesc D = a.desc[d];
+  const int lu = u - D.unit_off;
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const int t = D.task;
+  const int S = rq.S;
+  const int kb = g.key_off[t];
+  const int* tup = a.tb.sub_key + D.key_base;
+  uint32_t it[MAXI];
+  int n = 0;
+  if (D.mode == 0) {
+    // unrank count vector lu+1 (0 is the empty vector) -- _exhaustive_counts
+    unsigned long long idx = (unsigned long long)lu + 1ull;
+    int left = S;
+    const unsigned* W = a.ways + D.w_off;
+    for (int i = 0; i < D.n_tuples; ++i) {
+      const int cost = a.tb.key_cost[kb + tup[i]];
+      int c = 0;
+      while (true) {
+        unsigned long long w = W[(i + 1) * (S + 1) + (left - c * cost)];
+        if (idx < w) break;
+        idx -= w;
+        ++c;
+      }
+      if (c > 0) {
+        if (n >= MAXI) { atomicExch(a.err, 2); return; }
+        it[n++] = ((uint32_t)tup[i] << 16) | (uint32_t)c;
+      }
+      left -= c * cost;
+    }
+    append_candidate(a, probe, t, it, n);
+    return;
+  }
+  const DProbe& pr = a.probes[probe];
+  const double target = pr.r_upper[D.a][t] * (1.0 + rq.slack);
+  const bool has_lv = target > 0;
+  if (lu < D.n_tuple_units) {
+    // singleton + homogeneous covers of one tuple, distinct counts only
+    const int key = tup[lu];
+    const int cost = a.tb.key_cost[kb + key];
+    const double h = a.tb.key_thr[kb + key];
+    int counts[N_LEVELS + 1];
+    int m = 0;
+    if (cost <= S) counts[m++] = 1;
+    if (has_lv) {
+      for (int k = 0; k < N_LEVELS; ++k) {
+        int c = cover_count(target * c_grid[k], h, cost, S);
+        if (c > 0) counts[m++] = c;
+      }
+    }
+    for (int x = 0; x < m; ++x) {
+      bool dup = false;
+      for (int y = 0; y < x; ++y) dup |= counts[y] == counts[x];
+      if (dup) continue;
+      uint32_t one = ((uint32_t)key << 16) | (uint32_t)counts[x];
+      append_candidate(a, probe, t, &one, 1);
+    }
+    return;
+  }
+  if (!has_lv) return;
+  // two-variant mix unit: (pair, phi, level, rep_a, rep_b)
+  int mu = lu - D.n_tuple_units;
+  const int per_pair = rq.n_mix * N_LEVELS * 4;
+  int pi = mu / per_pair;
+  int rem = mu % per_pair;
+  const int rsel = rem & 3;
+  rem >>= 2;
+  const int lvk = rem % N_LEVELS;
+  const int ph = rem / N_LEVELS;
+  int ga = 0, gb = 1;
+  {
+    // pair index -> (ga < gb) in row-major order
+    int G = D.n_groups;
+    int acc = 0;
+    for (ga = 0; ga < G; ++ga) {
+      int cnt = G - 1 - ga;
+      if (pi < acc + cnt) { gb = ga + 1 + (pi - acc); break; }
+      acc += cnt;
+    }
+  }
+  const int ia = a.tb.grp_rep[2 * (D.grp_base + ga) + (rsel & 1)];
+  const int ib = a.tb.grp_rep[2 * (D.grp_base + gb) + (rsel >> 1)];
+  if (ia < 0 || ib < 0) return;
+  const double phi = rq.mix[ph];
+  const double lvl = target * c_grid[lvk];
+  const int ka = tup[ia], kbb = tup[ib];
+  const int costa = a.tb.key_cost[kb + ka], costb = a.tb.key_cost[kb + kbb];
+  int ca = cover_count(phi * lvl, a.tb.key_thr[kb + ka], costa, S);
+  int cb = cover_count((1.0 - phi) * lvl, a.tb.key_thr[kb + kbb], costb, S);
+  if (ca == 0 || cb == 0) return;
+  if (ca * costa + cb * costb > S) return;
+  it[0] = ((uint32_t)ka << 16) | (uint32_t)ca;
+  it[1] = ((uint32_t)kbb << 16) | (uint32_t)cb;
+  append_candidate(a, probe, t, it, 2);
+}
+
+__device__ __forceinline__ int locate_task(const S1Args& a, long long local) {
+  int t = 0;
+  while (t + 1 < a.T && a.task_base[t + 1] <= local) ++t;
+  return t;
+}
+
+__global__ void k_stats(S1Args a) {
+  long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  if (c >= tot) return;
+  const int probe = (int)(c / a.C_probe);
+  const long long local = c % a.C_probe;
+  const int t = locate_task(a, local);
+  const int pos = (int)(local - a.task_base[t]);
+  if (pos >= a.cnt[probe * a.T + t]) return;
+  const DGraph& g = *a.g;
+  Stat s;
+  uint32_t it[MAXI];
+  const int n = a.nitems[c];
+  for (int k = 0; k < n; ++k) it[k] = a.items[c * a.maxi + k];
+  bundle_stats(g, a.tb, t, it, n, s);
+  const int outd = g.succ_off[t + 1] - g.succ_off[t];
+  a.sl[c] = s.sl;
+  a.arr[0 * tot + c] = (double)s.sl;
+  a.arr[1 * tot + c] = -s.cap;
+  a.arr[2 * tot + c] = -s.acc;
+  a.arr[3 * tot + c] = s.lat;
+  for (int j = 0; j < a.D - 4; ++j) a.arr[(4 + j) * tot + c] = j < outd ? s.fan[j] : 0.0;
+  a.flag[c] = 0u;
+}
+
+// items(c1) < items(c2) lexicographically over ((key, count), ...) tuples
+__device__ __forceinline__ int cmp_items(const S1Args& a, long long c1, long long c2) {
+  const int n1 = a.nitems[c1], n2 = a.nitems[c2];
+  const int n = n1 < n2 ? n1 : n2;
+  for (int k = 0; k < n; ++k) {
+    uint32_t x = a.items[c1 * a.maxi + k], y = a.items[c2 * a.maxi + k];
+    if (x != y) return x < y ? -1 : 1;
+  }
+  return n1 < n2 ? -1 : (n1 > n2 ? 1 : 0);
+}
+
+#define TJ 128
+
+template <int D>
+__global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
+                                                 const int* tile_start, int tiles_pp, int jchunk) {
+  __shared__ double sh[D * TJ];
+  const int probe = blockIdx.x / tiles_pp;
+  const int tl = blockIdx.x % tiles_pp;
+  const int t = tile_task[tl];
+  const int i0 = tile_start[tl];
+  const int n = a.cnt[probe * a.T + t];
+  if (i0 >= n) return;
+  const int j0 = blockIdx.y * jchunk;
+  if (j0 >= n) return;
+  const int j1 = min(n, j0 + jchunk);
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  const int i = i0 + threadIdx.x;
+  const bool act = i < n;
+  double xi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) xi[d] = act ? a.arr[d * tot + base + i] : 0.0;
+  unsigned fl = 0;
+  for (int jt = j0; jt < j1; jt += TJ) {
+    const int nj = min(TJ, j1 - jt);
+    for (int x = threadIdx.x; x < D * TJ; x += blockDim.x) {
+      int d = x / TJ, jj = x % TJ;
+      sh[x] = jj < nj ? a.arr[d * tot + base + jt + jj] : 0.0;
+    }
+    __syncthreads();
+    if (act && !fl) {
+      for (int jj = 0; jj < nj; ++jj) {
+        bool le = true, eq = true;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double xj = sh[d * TJ + jj];
+          le = le && (xj <= xi[d]);
+          eq = eq && (xj == xi[d]);
+        }
+        if (le) {
+          if (!eq) {
+            fl |= 1u;
+            break;
+          }
+          const int j = jt + jj;
+          if (j != i) {
+            int c = cmp_items(a, base + j, base + i);
+            if (c < 0 || (c == 0 && j < i)) {
+              fl |= 2u;
+              break;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (act && fl) atomicOr(&a.flag[base + i], fl);
+}
+
+__global__ void __launch_bounds__(1024) k_compact(S1Args a) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int n = a.cnt[job];
+  const long long base = job_base(a, probe, t);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int s0 = 0; s0 < n; s0 += 1024) {
+    int i = s0 + threadIdx.x;
+    int alive = (i < n && a.flag[base + i] == 0u) ? 1 : 0;
+    int off, total;
+    Scan(tmp).ExclusiveSum(alive, off, total);
+    if (alive) {
+      a.front[base + carry + off] = i;
+      a.fpos[base + carry + off] = 0;
+      a.fcr[base + carry + off] = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) a.fcnt[job] = carry;
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_pairs_b(S1Args a, const int* tile_task,
+                                                 const int* tile_start, int tiles_pp, int jchunk) {
+  __shared__ double sh[D * TJ];
+  __shared__ int shc[TJ];
+  const int probe = blockIdx.x / tiles_pp;
+  const int tl = blockIdx.x % tiles_pp;
+  const int t = tile_task[tl];
+  const int i0 = tile_start[tl];
+  const int job = probe * a.T + t;
+  const int F = a.fcnt[job];
+  if (i0 >= F) return;
+  const int j0 = blockIdx.y * jchunk;
+  if (j0 >= F) return;
+  const int j1 = min(F, j0 + jchunk);
+  const bool need_cap = F > a.W;
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  const int i = i0 + threadIdx.x;
+  const bool act = i < F;
+  const int ci = act ? a.front[base + i] : 0;
+  double xi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) xi[d] = act ? a.arr[d * tot + base + ci] : 0.0;
+  int pos = 0, cr = 0;
+  for (int jt = j0; jt < j1; jt += TJ) {
+    const int nj = min(TJ, j1 - jt);
+    for (int x = threadIdx.x; x < TJ; x += blockDim.x) shc[x] = x < nj ? a.front[base + jt + x] : 0;
+    __syncthreads();
+    for (int x = threadIdx.x; x < D * TJ; x += blockDim.x) {
+      int d = x / TJ, jj = x % TJ;
+      sh[x] = jj < nj ? a.arr[d * tot + base + shc[jj]] : 0.0;
+    }
+    __syncthreads();
+    if (act) {
+      for (int jj = 0; jj < nj; ++jj) {
+        // lexicographic row order (planner.py:556-559; rows are distinct here)
+        int lt = 0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          double xj = sh[d * TJ + jj];
+          if (lt == 0) {
+            if (xj < xi[d]) lt = 1;
+            else if (xj > xi[d]) lt = -1;
+          }
+        }
+        pos += lt == 1;
+        if (need_cap) {
+          // (-capacity, slices, items) order (planner.py:576)
+          double cj = sh[1 * TJ + jj], c0 = xi[1];
+          bool less;
+          if (cj != c0) less = cj < c0;
+          else if (sh[jj] != xi[0]) less = sh[jj] < xi[0];
+          else less = cmp_items(a, base + shc[jj], base + ci) < 0;
+          cr += less;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (act) {
+    if (pos) atomicAdd(&a.fpos[base + i], pos);
+    if (cr) atomicAdd(&a.fcr[base + i], cr);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_truncate(S1Args a) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry_nontop, carry_kept;
+  __shared__ double red_lat[1024];
+  __shared__ int red_sl[1024];
+  __shared__ double red_acc[1024];
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int F = a.fcnt[job];
+  const int W = a.W;
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  const DGraph& g = *a.g;
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    int p = a.fpos[base + i];
+    a.sorted[base + p] = a.front[base + i];
+    a.scr[base + p] = a.fcr[base + i];
+  }
+  __syncthreads();
+  int* pool = a.pool_cand + (long long)job * W;
+  int P;
+  if (F <= W) {
+    for (int k = threadIdx.x; k < F; k += blockDim.x) pool[k] = a.sorted[base + k];
+    P = F;
+    if (threadIdx.x == 0) a.pool_trunc[job] = 0;
+  } else {
+    if (threadIdx.x == 0) { carry_nontop = 0; carry_kept = 0; }
+    __syncthreads();
+    const int top_n = W / 2, rest = W - W / 2;
+    for (int s0 = 0; s0 < F; s0 += 1024) {
+      int k = s0 + threadIdx.x;
+      int nontop = (k < F && a.scr[base + k] >= top_n) ? 1 : 0;
+      int before, tot_nt;
+      Scan(tmp).ExclusiveSum(nontop, before, tot_nt);
+      __syncthreads();
+      int keep = 0;
+      if (k < F) keep = (!nontop) || (carry_nontop + before < rest);
+      int kpos, tot_k;
+      Scan(tmp).ExclusiveSum(keep, kpos, tot_k);
+      if (keep) pool[carry_kept + kpos] = a.sorted[base + k];
+      __syncthreads();
+      if (threadIdx.x == 0) { carry_nontop += tot_nt; carry_kept += tot_k; }
+      __syncthreads();
+    }
+    P = carry_kept;
+    if (threadIdx.x == 0) a.pool_trunc[job] = 1;
+  }
+  __syncthreads();
+  const int outd = g.succ_off[t + 1] - g.succ_off[t];
+  double mlat = 1e308;
+  int msl = 0x7fffffff;
+  double macc = -1.0;
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    long long c = base + pool[k];
+    long long q = (long long)job * W + k;
+    double lat = a.arr[3 * tot + c];
+    double acc = -a.arr[2 * tot + c];
+    int sl = (int)a.arr[0 * tot + c];
+    a.p_sl[q] = sl;
+    a.p_cap[q] = -a.arr[1 * tot + c];
+    a.p_acc[q] = acc;
+    a.p_lat[q] = lat;
+    for (int j = 0; j < outd; ++j) a.p_fan[q * a.maxout + j] = a.arr[(4 + j) * tot + c];
+    double l2 = 2.0 * lat;
+    if (l2 < mlat) mlat = l2;
+    if (sl < msl) msl = sl;
+    if (acc > macc) macc = acc;
+  }
+  red_lat[threadIdx.x] = mlat;
+  red_sl[threadIdx.x] = msl;
+  red_acc[threadIdx.x] = macc;
+  __syncthreads();
+  for (int s = 512; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      int o = threadIdx.x + s;
+      if (red_lat[o] < red_lat[threadIdx.x]) red_lat[threadIdx.x] = red_lat[o];
+      if (red_sl[o] < red_sl[threadIdx.x]) red_sl[threadIdx.x] = red_sl[o];
+      if (red_acc[o] > red_acc[threadIdx.x]) red_acc[threadIdx.x] = red_acc[o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.pool_n[job] = P;
+    a.pool_min_lat2[job] = red_lat[0];
+    a.pool_min_sl[job] = red_sl[0];
+    a.pool_acc_ub[job] = red_acc[0];
+  }
+}
+
+// Rank of (items, end-sign) among the 2*(P+1) elements of one pool (+ empty).
+__device__ __forceinline__ uint32_t item_word(const S1Args& a, long long c, int n, int k, int sign) {
+  if (k < n) return a.items[c * a.maxi + k];
+  return sign ? 0xFFFFFFFFu : 0u;
+}
+
+__global__ void k_mrank(S1Args a) {
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int P = a.pool_n[job];
+  const int E = 2 * (P + 1);
+  const int e = blockIdx.y * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const long long base = job_base(a, probe, t);
+  const int* pool = a.pool_cand + (long long)job * a.W;
+  const int ke = e >> 1, se = e & 1;
+  const long long ce = ke < P ? base + pool[ke] : -1;
+  const int ne = ke < P ? a.nitems[ce] : 0;
+  int rank = 0;
+  for (int f = 0; f < E; ++f) {
+    const int kf = f >> 1, sf = f & 1;
+    const long long cf = kf < P ? base + pool[kf] : -1;
+    const int nf = kf < P ? a.nitems[cf] : 0;
+    int r = 0;
+    for (int k = 0; k <= MAXI && r == 0; ++k) {
+      uint32_t x = item_word(a, cf, nf, k, sf), y = item_word(a, ce, ne, k, se);
+      if (x != y) r = x < y ? -1 : 1;
+      if (k >= nf && k >= ne) break;
+    }
+    rank += r < 0;
+  }
+  const long long q = (long long)job * (a.W + 1) + ke;
+  if (se) a.rank_p[q] = (uint16_t)rank;
+  else a.rank_m[q] = (uint16_t)rank;
+}
+
+// ------------------------------------------------------------------ launchers
+
+static int pick_D(int D) {
+  if (D <= 4) return 4;
+  if (D <= 5) return 5;
+  if (D <= 6) return 6;
+  if (D <= 8) return 8;
+  if (D <= 12) return 12;
+  if (D <= 16) return 16;
+  return MAXD;
+}
+
+int stage1_padded_dims(int D) { return pick_D(D); }
+
+#define DISPATCH_D(D, KERNEL, GRID, ...)                     \
+  switch (D) {                                               \
+    case 4: KERNEL<4><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;   \
+    case 5: KERNEL<5><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;   \
+    case 6: KERNEL<6><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;   \
+    case 8: KERNEL<8><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;   \
+    case 12: KERNEL<12><<<GRID, 256, 0, st>>>(__VA_ARGS__); break; \
+    case 16: KERNEL<16><<<GRID, 256, 0, st>>>(__VA_ARGS__); break; \
+    default: KERNEL<MAXD><<<GRID, 256, 0, st>>>(__VA_ARGS__); break; \
+  }
+
+int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
+  int launches = 0;
+  long long gen = (long long)a.n_probes * a.U;
+  if (gen > 0) {
+    k_generate<<<(unsigned)((gen + 255) / 256), 256, 0, st>>>(a);
+    ++launches;
+  }
+  long long tot = (long long)a.n_probes * a.C_probe;
+  k_stats<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
+  ++launches;
+  dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
+  DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a);
+  ++launches;
+  k_compact<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+  ++launches;
+  dim3 gb((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_b);
+  DISPATCH_D(a.D, k_pairs_b, gb, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_b);
+  ++launches;
+  k_truncate<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+  ++launches;
+  dim3 gm((unsigned)(a.n_probes * a.T), (unsigned)((2 * (a.W + 1) + 255) / 256));
+  k_mrank<<<gm, 256, 0, st>>>(a);
+  ++launches;
+  return launches;
+}

@@ -1,0 +1,703 @@
+// jsv_stage2.cu -- Stage 2 on sm_100a: exact search over the Stage-1 pools.
+//
+// Replaces reference planner.py:731-912 (_Search), 243-361 (derive +
+// validate at every leaf) and 973-1110 (plan_uninformed's per-task argmax).
+//
+// The reference explores a depth-first branch-and-bound tree over tasks in
+// topological order.  Here the same tree is expanded level-synchronously: a
+// work item is (surviving prefix, pool bundle) and applies exactly the
+// reference's filters in its order (throughput, resources, partial-path
+// latency, accuracy upper bound, objective bound against the incumbent).
+// Leaves are derived from scratch and validated in the reference's float
+// order, then folded into a per-probe lexicographic reduction
+//   (objective desc, total slices asc, m asc)                 full plans
+//   (first leaf in DFS order)                                  feasible_only
+// which equals the reference's answer because every filter is admissible and
+// ties are broken on the canonical m.  For an
+// infeasible plan there is no incumbent, so the set of visited prefixes is
+// order-independent and the diagnostic re-run reproduces the reference's kill
+// counts, deepest blocked level and last failed leaf (H5).
+#include "jsv_internal.cuh"
+#include "jsv_kernels.h"
+
+__global__ void k_s2_prep(S2Args a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
+                          const double* s1_lat2, const int* s1_sl, const double* s1_acc) {
+  const int probe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (probe >= a.n_probes) return;
+  const DGraph& g = *a.g;
+  const DProbe& pr = a.probes[probe];
+  const int T = a.T;
+  for (int t = 0; t < T; ++t) {
+    const int job = probe * T + t;
+    const bool cz = (pr.could_zero >> t) & 1u;
+    min_lat2[job] = cz ? 0.0 : s1_lat2[job];
+    min_sl[job] = cz ? 0 : s1_sl[job];
+    acc_ub[job] = cz ? 1.0 : s1_acc[job];
+  }
+  int* fut = future + probe * (T + 1);
+  fut[T] = 0;
+  for (int i = T - 1; i >= 0; --i) fut[i] = fut[i + 1] + min_sl[probe * T + g.topo[i]];
+  BestRec* B = a.best + probe;
+  B->lock = 0;
+  B->has = 0;
+  B->found = 0;
+  B->has_leaf = 0;
+  B->deepest = -1;
+  for (int i = 0; i < MAXT; ++i)
+    for (int k = 0; k < 5; ++k) B->kills[i][k] = 0;
+  B->nodes = 0;
+  B->leaves = 0;
+}
+
+__device__ __forceinline__ void pack16(unsigned long long* w, int k, unsigned v) {
+  w[k >> 2] |= (unsigned long long)(v & 0xFFFFu) << ((3 - (k & 3)) * 16);
+}
+
+// m-rank tie key of one leaf (task-id order)
+__device__ inline void tie_key(const S2Args& a, int probe, const uint16_t* cb,
+                               unsigned long long* w) {
+  w[0] = w[1] = w[2] = w[3] = 0ull;
+  bool later = false;
+  for (int u = a.T - 1; u >= 0; --u) {
+    const int job = probe * a.T + u;
+    const int c = cb[u];
+    const int idx = (c == NONE16) ? a.pool_n[job] : c;
+    const long long q = (long long)job * (a.W + 1) + idx;
+    const unsigned rk = later ? a.rank_p[q] : a.rank_m[q];
+    pack16(w, u, rk);
+    if (c != NONE16) later = true;
+  }
+}
+
+__device__ inline void leaf_key(int T, const uint16_t* ch_topo, unsigned long long* w) {
+  w[0] = w[1] = w[2] = w[3] = 0ull;
+  for (int k = 0; k < T; ++k) pack16(w, k, ch_topo[k] == NONE16 ? 0u : ch_topo[k]);
+}
+
+__device__ inline void load_leaf(const S2Args& a, int probe, const uint16_t* ch_topo, double* lat,
+                                 double* cap, double* acc, int* sl, double* fan, uint32_t& present) {
+  const DGraph& g = *a.g;
+  present = 0;
+  for (int u = 0; u < a.T; ++u) {
+    const int c = ch_topo[g.pos_of[u]];
+    const int job = probe * a.T + u;
+    const int outd = g.succ_off[u + 1] - g.succ_off[u];
+    if (c == NONE16) {
+      lat[u] = 0.0; cap[u] = 0.0; acc[u] = 1.0; sl[u] = 0;
+      for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = 0.0;
+    } else {
+      const long long q = (long long)job * a.W + c;
+      lat[u] = a.p_lat[q]; cap[u] = a.p_cap[q]; acc[u] = a.p_acc[q]; sl[u] = a.p_sl[q];
+      for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = a.p_fan[q * a.maxout + j];
+      present |= 1u << u;
+    }
+  }
+}
+
+__device__ inline void with_lock(int* lock, bool& done) { done = atomicCAS(lock, 0, 1) == 0; }
+
+__device__ void leaf_visit(const S2Args& a, int probe, const uint16_t* ch_topo) {
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const DProbe& pr = a.probes[probe];
+  BestRec* B = a.best + probe;
+  double lat[MAXT], cap[MAXT], acc[MAXT], fan[MAXE];
+  int sl[MAXT];
+  uint32_t present;
+  load_leaf(a, probe, ch_topo, lat, cap, acc, sl, fan, present);
+  EvalOut ev;
+  evaluate<false>(g, rq, pr, lat, cap, acc, sl, fan, present, ev, nullptr, nullptr, nullptr,
+                  nullptr);
+  atomicAdd(&B->leaves, 1ull);
+  if (a.diag) {
+    // last reached leaf in DFS order = lexicographically largest choice vector
+    unsigned long long lk[4];
+    leaf_key(a.T, ch_topo, lk);
+    volatile BestRec* VB = B;
+    if (!(VB->has_leaf && lk[0] < VB->leafkey[0])) {
+      bool done = false;
+      while (!done) {
+        with_lock(&B->lock, done);
+        if (done) {
+          __threadfence();
+          if (!B->has_leaf || cmp_words(lk, B->leafkey, 4) > 0) {
+            for (int k = 0; k < 4; ++k) B->leafkey[k] = lk[k];
+            for (int k = 0; k < a.T; ++k) B->leaf_choice[k] = ch_topo[k];
+            B->has_leaf = 1;
+          }
+          __threadfence();
+          atomicExch(&B->lock, 0);
+        }
+      }
+    }
+  }
+  if (!ev.feasible) return;
+  if (rq.feasible_only) {
+    if (!a.want_config) {
+      if (!B->found) {
+        bool done = false;
+        while (!done) {
+          with_lock(&B->lock, done);
+          if (done) {
+            __threadfence();
+            if (!B->has) {
+              for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
+              B->obj = ev.objective;
+              B->sl = ev.total_sl;
+              B->has = 1;
+              B->found = 1;
+            }
+            __threadfence();
+            atomicExch(&B->lock, 0);
+          }
+        }
+      }
+      return;
+    }
+    // first feasible leaf in DFS order = lexicographically smallest choice vector
+    unsigned long long lk[4];
+    leaf_key(a.T, ch_topo, lk);
+    volatile BestRec* VB = B;
+    if (VB->has && lk[0] > VB->tie[0]) return;
+    bool done = false;
+    while (!done) {
+      with_lock(&B->lock, done);
+      if (done) {
+        __threadfence();
+        if (!B->has || cmp_words(lk, B->tie, 4) < 0) {
+          for (int k = 0; k < 4; ++k) B->tie[k] = lk[k];
+          for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
+          B->obj = ev.objective;
+          B->sl = ev.total_sl;
+          B->has = 1;
+          B->found = 1;
+        }
+        __threadfence();
+        atomicExch(&B->lock, 0);
+      }
+    }
+    return;
+  }
+  {
+    volatile BestRec* VB = B;
+    if (VB->has) {
+      double bo = VB->obj;
+      int bs = VB->sl;
+      if (ev.objective < bo || (ev.objective == bo && ev.total_sl > bs)) return;
+    }
+  }
+  uint16_t cb[MAXT];
+  for (int u = 0; u < a.T; ++u) cb[u] = ch_topo[g.pos_of[u]];
+  unsigned long long tk[4];
+  tie_key(a, probe, cb, tk);
+  bool done = false;
+  while (!done) {
+    with_lock(&B->lock, done);
+    if (done) {
+      __threadfence();
+      bool better;
+      if (!B->has) better = true;
+      else if (ev.objective != B->obj) better = ev.objective > B->obj;
+      else if (ev.total_sl != B->sl) better = ev.total_sl < B->sl;
+      else better = cmp_words(tk, B->tie, 4) < 0;
+      if (better) {
+        B->obj = ev.objective;
+        B->sl = ev.total_sl;
+        for (int k = 0; k < 4; ++k) B->tie[k] = tk[k];
+        for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
+        B->has = 1;
+        B->found = 1;
+      }
+      __threadfence();
+      atomicExch(&B->lock, 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_s2_level(S2Args a) {
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const int T = a.T, L = a.level;
+  const int t = g.topo[L];
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < a.total_work;
+       w += stride) {
+    int lo = 0, hi = a.n_probes - 1;
+    while (lo < hi) {
+      int mid = (lo + hi + 1) >> 1;
+      if (a.woff[mid] <= w) lo = mid;
+      else hi = mid - 1;
+    }
+    const int probe = lo;
+    BestRec* B = a.best + probe;
+    if (!a.diag && rq.feasible_only && !a.want_config && ((volatile BestRec*)B)->found) continue;
+    const long long lw = w - a.woff[probe];
+    const int width = a.width[probe];
+    const long long p = lw / width;
+    const int b = (int)(lw % width);
+    const long long pidx = a.foff[probe] + p;
+    uint16_t ch[MAXT];
+    for (int k = 0; k < L; ++k) ch[k] = a.cur[pidx * T + k];
+    const DProbe& pr = a.probes[probe];
+    const int jb = probe * T;
+    // demand reaching each task so far (_demand_at, planner.py:821-833)
+    double r[MAXT];
+    int used = 0;
+    for (int k = 0; k <= L; ++k) {
+      const int u = g.topo[k];
+      double ru;
+      if (u == g.entry) {
+        ru = pr.demand;
+      } else {
+        ru = 0.0;
+        for (int qq = g.pred_off[u]; qq < g.pred_off[u + 1]; ++qq) {
+          const int e = g.pred_edge[qq];
+          const int s = g.edge_src[e];
+          const int cs = ch[g.pos_of[s]];
+          if (cs == NONE16 || r[s] == 0.0) continue;
+          const double fan = rq.has_ov[e]
+                                 ? rq.ov[e]
+                                 : a.p_fan[((long long)(jb + s) * a.W + cs) * a.maxout +
+                                           (e - g.succ_off[s])];
+          ru += r[s] * fan;
+        }
+      }
+      r[u] = ru;
+      if (k < L && ch[k] != NONE16) used += a.p_sl[(long long)(jb + u) * a.W + ch[k]];
+    }
+    const double rt = r[t];
+    if (rt == 0.0) {
+      // nothing flows here: the empty assignment is the only child (planner.py:868-875)
+      if (b != 0) continue;
+      ch[L] = NONE16;
+      if (a.last) {
+        leaf_visit(a, probe, ch);
+      } else {
+        unsigned long long pos = atomicAdd(&a.nxt_cnt[probe], 1ull);
+        if ((long long)pos >= a.nxt_cap[probe]) { atomicExch(a.err, 3); continue; }
+        uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
+        for (int k = 0; k <= L; ++k) dst[k] = ch[k];
+      }
+      continue;
+    }
+    if (a.diag && b == 0) atomicOr(&a.cur_flag[pidx], 1);
+    const int P = a.pool_n[jb + t];
+    if (b >= P) continue;
+    const long long q = (long long)(jb + t) * a.W + b;
+    const int* fut = a.future + probe * (T + 1);
+    const double need = rt * (1.0 + rq.slack);
+    const double eps = rq.eps;
+    int why = -1;
+    double ub = 0.0;
+    const int bsl = a.p_sl[q];
+    if (a.p_cap[q] + eps < need) {
+      why = JSV_BIND_THROUGHPUT;
+    } else if ((double)(used + bsl + fut[L + 1]) > (double)rq.S + eps) {
+      why = JSV_BIND_RESOURCES;
+    } else {
+      // partial-path latency with lower bounds for open tasks (_latency_ok, 805-819)
+      const double lat2 = 2.0 * a.p_lat[q];
+      bool ok = true;
+      for (int pp = 0; pp < g.P && ok; ++pp) {
+        if (!((g.path_mask[pp] >> t) & 1u)) continue;
+        double tot = 0.0;
+        for (int k = g.path_off[pp]; k < g.path_off[pp + 1]; ++k) {
+          const int u = g.path_task[k];
+          if (u == t) {
+            tot += lat2;
+          } else if (g.pos_of[u] < L) {
+            const int c = ch[g.pos_of[u]];
+            tot += (c == NONE16) ? 0.0 : 2.0 * a.p_lat[(long long)(jb + u) * a.W + c];
+          } else {
+            tot += a.min_lat2[jb + u];
+          }
+        }
+        if (tot > pr.slo_eff + eps) ok = false;
+      }
+      if (!ok) {
+        why = JSV_BIND_LATENCY;
+      } else {
+        double acc[MAXT];
+        for (int u = 0; u < T; ++u) {
+          const int pu = g.pos_of[u];
+          if (pu < L) {
+            const int c = ch[pu];
+            acc[u] = (c == NONE16) ? 1.0 : a.p_acc[(long long)(jb + u) * a.W + c];
+          } else if (u == t) {
+            acc[u] = a.p_acc[q];
+          } else {
+            acc[u] = a.acc_ub[jb + u];
+          }
+        }
+        ub = weighted_paths(g, acc) / g.a_max;
+        if (ub < pr.acc_slo - eps) why = JSV_BIND_ACCURACY;
+      }
+    }
+    if (why >= 0) {
+      if (a.diag) atomicAdd(&B->kills[L][why], 1);
+      continue;
+    }
+    if (a.diag) atomicOr(&a.cur_flag[pidx], 2);
+    if (!rq.feasible_only) {
+      volatile BestRec* VB = B;
+      if (VB->has) {
+        const double obj_ub = pr.alpha * ub - pr.beta * (double)(used + bsl + fut[L + 1]);
+        if (obj_ub < VB->obj - eps) continue;  // bound prune (counts as a survivor)
+      }
+    }
+    ch[L] = (uint16_t)b;
+    if (a.last) {
+      leaf_visit(a, probe, ch);
+    } else {
+      unsigned long long pos = atomicAdd(&a.nxt_cnt[probe], 1ull);
+      if ((long long)pos >= a.nxt_cap[probe]) { atomicExch(a.err, 3); continue; }
+      uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
+      for (int k = 0; k <= L; ++k) dst[k] = ch[k];
+    }
+  }
+}
+
+// deepest blocked level: a prefix with r > 0 whose children all died (planner.py:910-911)
+__global__ void k_s2_blocked(S2Args a, long long n_prefix, const int* prefix_probe) {
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n_prefix) return;
+  const int f = a.cur_flag[i];
+  if ((f & 1) && !(f & 2)) atomicMax(&a.best[prefix_probe[i]].deepest, a.level);
+}
+
+int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
+                       cudaStream_t st) {
+  // S2Args.min_lat2 etc. point at Stage-1 per-pool values on entry
+  k_s2_prep<<<(a.n_probes + 127) / 128, 128, 0, st>>>(a, min_lat2, min_sl, acc_ub, future,
+                                                       a.min_lat2, a.min_sl, a.acc_ub);
+  return 1;
+}
+
+int launch_stage2_level(const S2Args& a, cudaStream_t st) {
+  if (a.total_work <= 0) return 0;
+  long long blocks = (a.total_work + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_s2_level<<<(unsigned)blocks, 256, 0, st>>>(a);
+  return 1;
+}
+
+int launch_stage2_blocked(const S2Args& a, long long n_prefix_total, const int* prefix_probe,
+                          cudaStream_t st) {
+  if (n_prefix_total <= 0) return 0;
+  k_s2_blocked<<<(unsigned)((n_prefix_total + 255) / 256), 256, 0, st>>>(a, n_prefix_total,
+                                                                         prefix_probe);
+  return 1;
+}
+
+// ------------------------------------------------------------- finalisation
+
+__device__ void write_config(const FinArgs& a, int probe, const uint16_t* cb_task,
+                             jsv_plan_out& o) {
+  const DGraph& g = *a.g;
+  const int T = a.T;
+  double lat[MAXT], cap[MAXT], acc[MAXT], fan[MAXE];
+  int sl[MAXT];
+  uint32_t present = 0;
+  for (int u = 0; u < T; ++u) {
+    const int c = cb_task[u];
+    const int job = probe * T + u;
+    const int outd = g.succ_off[u + 1] - g.succ_off[u];
+    o.n_items[u] = 0;
+    if (c == NONE16) {
+      lat[u] = 0.0; cap[u] = 0.0; acc[u] = 1.0; sl[u] = 0;
+      for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = 0.0;
+      continue;
+    }
+    const long long q = (long long)job * a.W + c;
+    lat[u] = a.p_lat[q]; cap[u] = a.p_cap[q]; acc[u] = a.p_acc[q]; sl[u] = a.p_sl[q];
+    for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = a.p_fan[q * a.maxout + j];
+    present |= 1u << u;
+    const long long cand = (long long)probe * a.C_probe + a.task_base[u] + a.pool_cand[q];
+    const int n = a.nitems[cand];
+    o.n_items[u] = n;
+    const int kb = g.key_off[u];
+    for (int k = 0; k < n; ++k) {
+      const uint32_t w = a.items[cand * a.maxi + k];
+      o.items[u][k] = w;
+      o.hput[u][k] = (double)(w & 0xFFFFu) * a.tb.key_thr[kb + (w >> 16)];
+    }
+  }
+  EvalOut ev;
+  evaluate<true>(g, *a.rq, a.probes[probe], lat, cap, acc, sl, fan, present, ev, o.lat_margin,
+                 o.thr_margin, &o.res_margin, &o.acc_margin);
+  for (int u = 0; u < T; ++u) {
+    o.latency[u] = lat[u];
+    o.capacity[u] = cap[u];
+    o.accuracy[u] = acc[u];
+    o.slices[u] = sl[u];
+    o.demand[u] = ev.dem[u];
+  }
+  for (int e = 0; e < g.E; ++e) o.fanout[e] = ev.fan[e];
+  for (int p = 0; p < g.P; ++p) {
+    double prod = 1.0;
+    for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) prod *= acc[g.path_task[k]];
+    o.path_acc[p] = prod;
+  }
+  o.total_slices = ev.total_sl;
+  o.a_obj = ev.a_obj;
+  o.objective = ev.objective;
+  o.uncovered_mask = ev.uncovered;
+  o.has_config = 1;
+  o.feasible = ev.feasible ? 1 : 0;
+  o.binding = ev.first_fail;
+}
+
+__device__ int binding_from_kills(const int* k) {
+  int best = 0;
+  for (int n = 1; n < 5; ++n)
+    if (k[n] > k[best]) best = n;
+  return k[best] ? best : JSV_BIND_THROUGHPUT;
+}
+
+__global__ void k_finalize(FinArgs a) {
+  const int probe = blockIdx.x * blockDim.x + threadIdx.x;
+  if (probe >= a.n_probes) return;
+  const DGraph& g = *a.g;
+  const int T = a.T;
+  jsv_plan_out& o = a.out[probe];
+  o.has_config = 0;
+  o.feasible = 0;
+  o.binding = JSV_BIND_THROUGHPUT;
+  o.objective = 0.0;
+  o.a_obj = 0.0;
+  o.dead = a.dead[probe];
+  for (int t = 0; t < T; ++t) {
+    o.pool_size[t] = a.pool_n[probe * T + t];
+    o.truncated[t] = a.pool_trunc[probe * T + t];
+    o.pool_present[t] = 1;
+  }
+  const BestRec& B = a.best[probe];
+  o.nodes = 0;
+  o.leaves = (long long)B.leaves;
+  if (a.uninformed) {
+    uint16_t cb[MAXT];
+    for (int t = 0; t < T; ++t) cb[t] = NONE16;
+    for (int i = 0; i < T; ++i) {
+      const int t = g.topo[i];
+      const int pk = a.pick[probe * T + t];
+      if (pk == -2) continue;  // demand_star == 0: no instances
+      if (pk < 0) {
+        for (int k = i + 1; k < T; ++k) o.pool_present[g.topo[k]] = 0;
+        o.binding = binding_from_kills(a.uni_kills + (probe * T + t) * 5);
+        return;
+      }
+      cb[t] = (uint16_t)pk;
+    }
+    write_config(a, probe, cb, o);
+    if (o.feasible) o.binding = JSV_BIND_NONE;
+    return;
+  }
+  if (o.dead) {
+    o.binding = JSV_BIND_RESOURCES;
+    return;
+  }
+  if (B.has) {
+    uint16_t cb[MAXT];
+    for (int u = 0; u < T; ++u) cb[u] = B.choice[g.pos_of[u]];
+    write_config(a, probe, cb, o);
+    o.binding = JSV_BIND_NONE;
+    return;
+  }
+  if (B.deepest >= 0) {
+    o.binding = binding_from_kills(B.kills[B.deepest]);
+  } else if (B.has_leaf) {
+    uint16_t cb[MAXT];
+    for (int u = 0; u < T; ++u) cb[u] = B.leaf_choice[g.pos_of[u]];
+    jsv_plan_out tmp;
+    write_config(a, probe, cb, tmp);
+    o.binding = tmp.binding < 0 ? JSV_BIND_THROUGHPUT : tmp.binding;
+  } else {
+    o.binding = JSV_BIND_THROUGHPUT;
+  }
+  o.has_config = 0;
+  o.feasible = 0;
+}
+
+int launch_finalize(const FinArgs& a, cudaStream_t st) {
+  k_finalize<<<(a.n_probes + 63) / 64, 64, 0, st>>>(a);
+  return 1;
+}
+
+// ------------------------------------------------------- plan_uninformed picks
+
+// One block per (probe, task): exact per-task filters + argmax of
+// (alpha*w_t*acc - beta*s, -s), ties on items (planner.py:1064-1100).
+__global__ void __launch_bounds__(256) k_uni_pick(S2Args a, FinArgs f, int* pick, int* kills) {
+  __shared__ int sk[5];
+  __shared__ double s_score[256];
+  __shared__ int s_sl[256];
+  __shared__ int s_idx[256];
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const DProbe& pr = a.probes[probe];
+  const DReq& rq = *a.rq;
+  if (threadIdx.x < 5) sk[threadIdx.x] = 0;
+  if (pr.star[t] == 0.0) {
+    if (threadIdx.x == 0) {
+      pick[job] = -2;
+      for (int k = 0; k < 5; ++k) kills[job * 5 + k] = 0;
+    }
+    return;
+  }
+  __syncthreads();
+  const double need = pr.star[t] * (1.0 + rq.slack);
+  const int P = a.pool_n[job];
+  const double wa = pr.alpha * pr.weight[t];
+  double bscore = 0.0;
+  int bsl = 0, bidx = -1;
+  const long long cbase = (long long)probe * f.C_probe + f.task_base[t];
+  for (int k = threadIdx.x; k < P; k += blockDim.x) {
+    const long long q = (long long)job * a.W + k;
+    int why = -1;
+    if (a.p_cap[q] < need) why = JSV_BIND_THROUGHPUT;
+    else if (2.0 * a.p_lat[q] > pr.lat_budget[t]) why = JSV_BIND_LATENCY;
+    else if ((double)a.p_sl[q] > pr.slice_budget[t]) why = JSV_BIND_RESOURCES;
+    else if (a.p_acc[q] < pr.floor_[t]) why = JSV_BIND_ACCURACY;
+    if (why >= 0) {
+      atomicAdd(&sk[why], 1);
+      continue;
+    }
+    const double score = wa * a.p_acc[q] - pr.beta * (double)a.p_sl[q];
+    bool better;
+    if (bidx < 0) better = true;
+    else if (score != bscore) better = score > bscore;
+    else if (a.p_sl[q] != bsl) better = a.p_sl[q] < bsl;
+    else {
+      const long long c1 = cbase + f.pool_cand[q], c2 = cbase + f.pool_cand[(long long)job * a.W + bidx];
+      const int n1 = f.nitems[c1], n2 = f.nitems[c2];
+      int r = 0;
+      for (int i = 0; i < (n1 < n2 ? n1 : n2) && r == 0; ++i) {
+        uint32_t x = f.items[c1 * f.maxi + i], y = f.items[c2 * f.maxi + i];
+        if (x != y) r = x < y ? -1 : 1;
+      }
+      if (r == 0) r = n1 < n2 ? -1 : (n1 > n2 ? 1 : 0);
+      better = r < 0;
+    }
+    if (better) { bscore = score; bsl = a.p_sl[q]; bidx = k; }
+  }
+  s_score[threadIdx.x] = bscore;
+  s_sl[threadIdx.x] = bsl;
+  s_idx[threadIdx.x] = bidx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int bi = -1;
+    double bs = 0.0;
+    int bl = 0;
+    for (int x = 0; x < blockDim.x; ++x) {
+      const int k = s_idx[x];
+      if (k < 0) continue;
+      bool better;
+      if (bi < 0) better = true;
+      else if (s_score[x] != bs) better = s_score[x] > bs;
+      else if (s_sl[x] != bl) better = s_sl[x] < bl;
+      else {
+        const long long c1 = cbase + f.pool_cand[(long long)job * a.W + k];
+        const long long c2 = cbase + f.pool_cand[(long long)job * a.W + bi];
+        const int n1 = f.nitems[c1], n2 = f.nitems[c2];
+        int r = 0;
+        for (int i = 0; i < (n1 < n2 ? n1 : n2) && r == 0; ++i) {
+          uint32_t xx = f.items[c1 * f.maxi + i], yy = f.items[c2 * f.maxi + i];
+          if (xx != yy) r = xx < yy ? -1 : 1;
+        }
+        if (r == 0) r = n1 < n2 ? -1 : (n1 > n2 ? 1 : 0);
+        better = r < 0;
+      }
+      if (better) { bi = k; bs = s_score[x]; bl = s_sl[x]; }
+    }
+    pick[job] = bi;
+    for (int k = 0; k < 5; ++k) kills[job * 5 + k] = sk[k];
+  }
+}
+
+int launch_uninformed(const S2Args& a, const FinArgs& f, int* pick, int* kills, cudaStream_t st) {
+  k_uni_pick<<<a.n_probes * a.T, 256, 0, st>>>(a, f, pick, kills);
+  return 1;
+}
+
+// ---------------------------------------------------------- derive / validate
+
+__global__ void k_derive(DeriveArgs a) {
+  const DGraph& g = *a.g;
+  const int T = g.T;
+  jsv_plan_out& o = *a.out;
+  double lat[MAXT], cap[MAXT], acc[MAXT], fan[MAXE];
+  int sl[MAXT];
+  uint32_t present = 0;
+  for (int u = 0; u < T; ++u) {
+    const int n = a.n_items[u];
+    Stat s;
+    bundle_stats(g, a.tb, u, a.items + u * MAXI, n, s);
+    lat[u] = s.lat; cap[u] = s.cap; acc[u] = s.acc; sl[u] = s.sl;
+    const int outd = g.succ_off[u + 1] - g.succ_off[u];
+    for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = s.fan[j];
+    o.n_items[u] = n;
+    const int kb = g.key_off[u];
+    for (int k = 0; k < n; ++k) {
+      const uint32_t w = a.items[u * MAXI + k];
+      o.items[u][k] = w;
+      o.hput[u][k] = (double)(w & 0xFFFFu) * a.tb.key_thr[kb + (w >> 16)];
+    }
+    if (n) present |= 1u << u;
+  }
+  EvalOut ev;
+  evaluate<true>(g, *a.rq, *a.probe, lat, cap, acc, sl, fan, present, ev, o.lat_margin,
+                 o.thr_margin, &o.res_margin, &o.acc_margin);
+  for (int u = 0; u < T; ++u) {
+    o.latency[u] = lat[u];
+    o.capacity[u] = cap[u];
+    o.accuracy[u] = acc[u];
+    o.slices[u] = sl[u];
+    o.demand[u] = ev.dem[u];
+  }
+  for (int e = 0; e < g.E; ++e) o.fanout[e] = ev.fan[e];
+  for (int p = 0; p < g.P; ++p) {
+    double prod = 1.0;
+    for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) prod *= acc[g.path_task[k]];
+    o.path_acc[p] = prod;
+  }
+  o.total_slices = ev.total_sl;
+  o.a_obj = ev.a_obj;
+  o.objective = ev.objective;
+  o.uncovered_mask = ev.uncovered;
+  o.has_config = 1;
+  o.feasible = ev.feasible ? 1 : 0;
+  o.binding = ev.first_fail;
+}
+
+int launch_derive(const DeriveArgs& a, cudaStream_t st) {
+  k_derive<<<1, 1, 0, st>>>(a);
+  return 1;
+}
+
+// validate_configuration on caller-supplied fields (planner.py:329-361)
+__global__ void k_validate(ValidateArgs a) {
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const DProbe& pr = *a.probe;
+  jsv_plan_out& o = *a.out;
+  bool ok = true;
+  for (int p = 0; p < g.P; ++p) {
+    PySum ps;
+    for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) ps.add(2.0 * a.lat[g.path_task[k]]);
+    o.lat_margin[p] = pr.slo_eff - ps.result();
+    ok = ok && o.lat_margin[p] >= 0;
+  }
+  for (int t = 0; t < g.T; ++t) {
+    o.thr_margin[t] = a.cap[t] - a.dem[t] * (1.0 + rq.slack);
+    ok = ok && o.thr_margin[t] >= 0;
+  }
+  o.res_margin = (double)(rq.S - a.total_sl);
+  o.acc_margin = a.a_obj - pr.acc_slo;
+  o.uncovered_mask = a.uncovered;
+  o.feasible = ok && o.res_margin >= 0 && o.acc_margin >= 0 && a.uncovered == 0;
+}
+
+int launch_validate(const ValidateArgs& a, cudaStream_t st) {
+  k_validate<<<1, 1, 0, st>>>(a);
+  return 1;
+}

@@ -1,0 +1,412 @@
+"""Drop-in replacement for ``sliceserve.planner`` backed by the sm_100a library.
+
+Same public names, signatures and result types as the reference module
+(reference pkg/src/sliceserve/planner.py:36-54).  Every candidate is
+enumerated, evaluated, filtered and reduced on the GPU by libjsv.so:
+
+    plan()            -> jsv_plan_batch        (planner.py:915-957 / 973-1110)
+    plan_uninformed() -> jsv_plan_batch, T off (planner.py:973-1110)
+    max_demand()      -> jsv_max_demand_batch  (planner.py:1125-1175)
+    derive_configuration()   -> jsv_derive     (planner.py:243-315)
+    validate_configuration() -> jsv_validate   (planner.py:329-361)
+
+Host Python only validates inputs, lowers them to flat arrays once per
+(graph, profile), and rebuilds the frozen result dataclasses.  If the CUDA
+library or a GPU is missing, calls raise ``NativeError``; there is no CPU
+fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+from collections import OrderedDict
+from typing import Mapping, Sequence
+
+import numpy as np
+
+from . import _lower as LW
+from . import _native as N
+from .errors import ConfigError
+from .plan_types import (
+    ALL_SPACES,
+    Configuration,
+    ConstraintVerdict,
+    MaxDemandResult,
+    OracleCaps,
+    PlannerOptions,
+    PlanRequest,
+    PlanResult,
+    SearchSpace,
+    SolverStats,
+    plan_result_to_dict,
+)
+
+__all__ = [
+    "SearchSpace",
+    "ALL_SPACES",
+    "PlanRequest",
+    "PlannerOptions",
+    "Configuration",
+    "derive_configuration",
+    "ConstraintVerdict",
+    "validate_configuration",
+    "SolverStats",
+    "PlanResult",
+    "plan",
+    "plan_uninformed",
+    "plan_batch",
+    "MaxDemandResult",
+    "max_demand",
+    "max_demand_grid",
+    "OracleCaps",
+    "plan_result_to_dict",
+    "last_stats",
+]
+
+# ------------------------------------------------------------ problem cache
+
+_CACHE: "OrderedDict[tuple, tuple]" = OrderedDict()
+_CACHE_MAX = 32
+
+
+def _problem(app, profile, device=None) -> LW.Lowered:
+    ctx = N.context(device)
+    key = (id(app.graph), id(profile), ctx.value)
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0] is app.graph and hit[1] is profile:
+        _CACHE.move_to_end(key)
+        return hit[2]
+    lw = LW.attach(LW.lower(app, profile), ctx)
+    _CACHE[key] = (app.graph, profile, lw)  # strong refs keep ids unique while cached
+    while len(_CACHE) > _CACHE_MAX:
+        _CACHE.popitem(last=False)
+    return lw
+
+
+def last_stats(device=None) -> dict:
+    s = N.last_stats(N.context(device))
+    return {k: getattr(s, k) for k, _ in s._fields_}
+
+
+# ------------------------------------------------------------ result decode
+
+def _binding(code: int) -> str | None:
+    return None if code < 0 else N.BINDING_NAMES[code]
+
+
+def _config_from(out: N.PlanOut, app, lw: LW.Lowered, demand: float) -> Configuration:
+    g = app.graph
+    m = []
+    hput = {}
+    for ti, t in enumerate(lw.ids):
+        for k in range(out.n_items[ti]):
+            w = out.items[ti][k]
+            vid, seg, batch = lw.keys[ti][w >> 16]
+            m.append(((t, vid, seg, batch), int(w & 0xFFFF)))
+    for t in g.topological_order:
+        ti = lw.index[t]
+        for k in range(out.n_items[ti]):
+            w = out.items[ti][k]
+            vid, seg, batch = lw.keys[ti][w >> 16]
+            hput[(t, vid, seg, batch)] = out.hput[ti][k]
+    idx = lw.index
+    fan = {}
+    for t in g.task_ids:
+        for d in g.successors[t]:
+            fan[(t, d)] = out.fanout[lw.edge_index[(t, d)]]
+    return Configuration(
+        m=tuple(m),
+        entry_demand_rps=float(demand),
+        latency_ms={t: out.latency[idx[t]] for t in g.task_ids},
+        capacity_rps={t: out.capacity[idx[t]] for t in g.task_ids},
+        demand_rps={t: out.demand[idx[t]] for t in g.topological_order},
+        slices={t: int(out.slices[idx[t]]) for t in g.task_ids},
+        accuracy={t: out.accuracy[idx[t]] for t in g.task_ids},
+        fanout=fan,
+        hput=hput,
+        path_accuracy={p: out.path_acc[i] for i, p in enumerate(lw.paths)},
+        total_slices=int(out.total_slices),
+        a_obj=out.a_obj,
+        a_max=lw.a_max,
+        objective=out.objective,
+        structurally_infeasible=tuple(
+            t for t in g.topological_order if (out.uncovered_mask >> idx[t]) & 1
+        ),
+    )
+
+
+def _verdicts_from(out: N.PlanOut, app, lw: LW.Lowered) -> tuple[ConstraintVerdict, ...]:
+    g = app.graph
+    vs = []
+    for i, p in enumerate(lw.paths):
+        mg = out.lat_margin[i]
+        vs.append(ConstraintVerdict("latency", "->".join(p), mg >= 0, mg))
+    for t in g.topological_order:
+        mg = out.thr_margin[lw.index[t]]
+        vs.append(ConstraintVerdict("throughput", t, mg >= 0, mg))
+    mg = out.res_margin
+    vs.append(ConstraintVerdict("resources", "", mg >= 0, mg))
+    mg = out.acc_margin
+    vs.append(ConstraintVerdict("accuracy", "", mg >= 0, mg))
+    bad = tuple(t for t in g.topological_order if (out.uncovered_mask >> lw.index[t]) & 1)
+    vs.append(ConstraintVerdict("coverage", ",".join(bad), not bad,
+                                0.0 if not bad else -float(len(bad))))
+    return tuple(vs)
+
+
+def _result_from(out: N.PlanOut, app, lw: LW.Lowered, request, wall_ms: float) -> PlanResult:
+    g = app.graph
+    sizes = {}
+    cut = []
+    for t in g.topological_order:
+        ti = lw.index[t]
+        if out.pool_present[ti]:
+            sizes[t] = int(out.pool_size[ti])
+            if out.truncated[ti]:
+                cut.append(t)
+    stats = SolverStats(int(out.nodes), wall_ms, sizes, tuple(cut))
+    if not out.has_config:
+        return PlanResult(False, None, None, lw.a_max, _binding(out.binding), (), stats)
+    cfg = _config_from(out, app, lw, request.demand_rps)
+    vs = _verdicts_from(out, app, lw)
+    if out.feasible:
+        return PlanResult(True, cfg, cfg.objective, lw.a_max, None, vs, stats)
+    return PlanResult(False, cfg, None, lw.a_max, _binding(out.binding), vs, stats)
+
+
+# ------------------------------------------------------------------ solves
+
+def _prepare(app, profile, request: PlanRequest, options: PlannerOptions, device=None):
+    lw = _problem(app, profile, device)
+    statics = None
+    if request.space.task_graph_informed:
+        LW.check_usable(app, profile, lw, request)
+    else:
+        statics = LW.uninformed_statics(app, profile, lw, request)
+    return lw, statics
+
+
+def plan_batch(
+    app,
+    profile,
+    requests: Sequence[PlanRequest],
+    options: PlannerOptions | None = None,
+    apps: Sequence | None = None,
+    device: int | None = None,
+) -> list[PlanResult]:
+    """Many plan() calls in one GPU batch.
+
+    All requests must share slice budget, space, slack and overrides; demand
+    (and, through ``apps``, the SLO/objective scalars) may differ per probe.
+    Results equal ``[plan(a, profile, r, options) for a, r in ...]``.
+    """
+    options = options or PlannerOptions()
+    if not requests:
+        return []
+    apps = list(apps) if apps is not None else [app] * len(requests)
+    r0 = requests[0]
+    for r in requests[1:]:
+        if (r.slice_budget, r.space, r.slack, dict(r.factor_overrides or {})) != (
+                r0.slice_budget, r0.space, r0.slack, dict(r0.factor_overrides or {})):
+            raise ConfigError("plan_batch requests must share budget, space, slack and overrides")
+    t0 = time.perf_counter()
+    lw, _ = _prepare(app, profile, r0, options, device)
+    probes = (N.Probe * len(requests))()
+    for i, (a, r) in enumerate(zip(apps, requests)):
+        if a.graph is not app.graph:
+            raise ConfigError("plan_batch apps must share one task graph")
+        st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
+        probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
+    req, keep = LW.request_struct(lw, r0, options)
+    outs = (N.PlanOut * len(requests))()
+    N.check(N.load_library().jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests),
+                                            probes, outs))
+    wall = (time.perf_counter() - t0) * 1000.0
+    return [_result_from(outs[i], apps[i], lw, requests[i], wall) for i in range(len(requests))]
+
+
+def plan(
+    app,
+    profile,
+    request: PlanRequest,
+    options: PlannerOptions | None = None,
+) -> PlanResult:
+    """Best instance-count assignment in the requested search space (planner.py:915-957)."""
+    return plan_batch(app, profile, [request], options)[0]
+
+
+def plan_uninformed(
+    app,
+    profile,
+    request: PlanRequest,
+    options: PlannerOptions | None = None,
+) -> PlanResult:
+    """Statically budgeted baseline (planner.py:973-1110)."""
+    if request.space.task_graph_informed:
+        raise ConfigError("plan_uninformed requires a space with task_graph_informed=False")
+    return plan_batch(app, profile, [request], options)[0]
+
+
+def max_demand_grid(
+    apps: Sequence,
+    profile,
+    slice_budget: int,
+    space: SearchSpace,
+    slack: float = 0.05,
+    options: PlannerOptions | None = None,
+    rel_tol: float = 1e-3,
+    device: int | None = None,
+) -> list[MaxDemandResult]:
+    """max_demand() for several SLO variants of one app graph, solved together.
+
+    Each point replays the reference doubling + bisection exactly
+    (planner.py:1152-1175); the GPU evaluates many speculative probes per launch.
+    """
+    if slice_budget <= 0:
+        raise ConfigError(f"slice budget must be positive, got {slice_budget}")
+    options = options or PlannerOptions()
+    apps = list(apps)
+    if not apps:
+        return []
+    t0 = time.perf_counter()
+    base_req = PlanRequest(1e-6, slice_budget, space, slack)
+    lw, _ = _prepare(apps[0], profile, base_req, options, device)
+    points = (N.Probe * len(apps))()
+    for i, a in enumerate(apps):
+        if a.graph is not apps[0].graph:
+            raise ConfigError("max_demand_grid apps must share one task graph")
+        st = None if space.task_graph_informed else LW.uninformed_statics(a, profile, lw, base_req)
+        points[i] = LW.probe_struct(a, lw, 0.0, st)
+    req, keep = LW.request_struct(lw, base_req, options)
+    outs = (N.DemandOut * len(apps))()
+    plans = (N.PlanOut * len(apps))()
+    N.check(N.load_library().jsv_max_demand_batch(lw.ctx, lw.handle, C.byref(req), len(apps),
+                                                  points, float(rel_tol), outs, plans))
+    wall = (time.perf_counter() - t0) * 1000.0
+    res = []
+    for i, a in enumerate(apps):
+        o = outs[i]
+        dem = 0.0 if o.status == 1 else o.demand
+        plan_dem = 1e-6 if o.status == 1 else o.demand
+        pr = _result_from(plans[i], a, lw, PlanRequest(plan_dem, slice_budget, space, slack), wall)
+        res.append(MaxDemandResult(dem, pr, int(o.probes)))
+    return res
+
+
+def max_demand(
+    app,
+    profile,
+    slice_budget: int,
+    space: SearchSpace,
+    slack: float = 0.05,
+    options: PlannerOptions | None = None,
+    rel_tol: float = 1e-3,
+) -> MaxDemandResult:
+    """Largest serviceable demand for a space, by doubling then bisection (1125-1175)."""
+    return max_demand_grid([app], profile, slice_budget, space, slack, options, rel_tol)[0]
+
+
+# -------------------------------------------------------- derive / validate
+
+def _scalar_request(app, profile, request=None):
+    lw = _problem(app, profile)
+    request = request or PlanRequest(0.0, 0)
+    req, keep = LW.request_struct(lw, request, PlannerOptions())
+    return lw, req, keep
+
+
+def derive_configuration(
+    m: Mapping,
+    app,
+    profile,
+    demand_rps: float,
+    factor_overrides: Mapping[tuple[str, str], float] | None = None,
+) -> Configuration:
+    """Every quantity implied by an instance-count map, computed on the GPU (243-315)."""
+    lw = _problem(app, profile)
+    n_items, items, _ = LW.encode_assignment(app, profile, lw, m)
+    request = PlanRequest(0.0, 0, SearchSpace(True, True, True), 0.0, factor_overrides)
+    req, keep = LW.request_struct(lw, request, PlannerOptions())
+    probe = LW.probe_struct(app, lw, float(demand_rps))
+    out = N.PlanOut()
+    N.check(N.load_library().jsv_derive(
+        lw.ctx, lw.handle, C.byref(req), C.byref(probe),
+        n_items.ctypes.data_as(C.POINTER(C.c_int32)),
+        items.ctypes.data_as(C.POINTER(C.c_uint32)), C.byref(out)))
+    return _config_from(out, app, lw, demand_rps)
+
+
+def validate_configuration(config: Configuration, app, profile, request: PlanRequest):
+    """Constraint verdicts with margins, computed on the GPU (329-361)."""
+    lw = _problem(app, profile)
+    req, keep = LW.request_struct(lw, request, PlannerOptions())
+    probe = LW.probe_struct(app, lw, request.demand_rps)
+    T = len(lw.ids)
+    lat = np.zeros(T)
+    cap = np.zeros(T)
+    dem = np.zeros(T)
+    for t, ti in lw.index.items():
+        lat[ti] = config.latency_ms[t]
+        cap[ti] = config.capacity_rps[t]
+        dem[ti] = config.demand_rps[t]
+    mask = 0
+    for t in config.structurally_infeasible:
+        mask |= 1 << lw.index[t]
+    out = N.PlanOut()
+    fp = C.POINTER(C.c_double)
+    N.check(N.load_library().jsv_validate(
+        lw.ctx, lw.handle, C.byref(req), C.byref(probe), lat.ctypes.data_as(fp),
+        cap.ctypes.data_as(fp), dem.ctypes.data_as(fp), int(config.total_slices),
+        float(config.a_obj), mask, C.byref(out)))
+    g = app.graph
+    vs = []
+    for i, p in enumerate(lw.paths):
+        mg = out.lat_margin[i]
+        vs.append(ConstraintVerdict("latency", "->".join(p), mg >= 0, mg))
+    for t in g.topological_order:
+        mg = out.thr_margin[lw.index[t]]
+        vs.append(ConstraintVerdict("throughput", t, mg >= 0, mg))
+    vs.append(ConstraintVerdict("resources", "", out.res_margin >= 0, out.res_margin))
+    vs.append(ConstraintVerdict("accuracy", "", out.acc_margin >= 0, out.acc_margin))
+    bad = config.structurally_infeasible
+    vs.append(ConstraintVerdict("coverage", ",".join(bad), not bad,
+                                0.0 if not bad else -float(len(bad))))
+    return tuple(vs)
+
+
+def pool_dump(app, profile, request: PlanRequest, options: PlannerOptions | None = None,
+              device=None) -> dict:
+    """Stage-1 pools computed on the GPU, in the reference's frontier order (test helper)."""
+    options = options or PlannerOptions()
+    lw, _ = _prepare(app, profile, request, options, device)
+    req, keep = LW.request_struct(lw, request, options)
+    probe = LW.probe_struct(app, lw, request.demand_rps)
+    lib = N.load_library()
+    g = app.graph
+    out = {}
+    cap = max(1, options.pareto_width)
+    for t in g.topological_order:
+        ti = lw.index[t]
+        outd = len(g.successors[t])
+        n = C.c_int32()
+        trunc = C.c_int32()
+        nit = np.zeros(cap, dtype=np.int32)
+        its = np.zeros((cap, N.MAX_ITEMS), dtype=np.uint32)
+        st = np.zeros((cap, 4 + outd), dtype=np.float64)
+        N.check(lib.jsv_pool_dump(lw.ctx, lw.handle, C.byref(req), C.byref(probe), ti, cap,
+                                  C.byref(n), nit.ctypes.data_as(C.POINTER(C.c_int32)),
+                                  its.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                  st.ctypes.data_as(C.POINTER(C.c_double)), C.byref(trunc)))
+        rows = []
+        for k in range(n.value):
+            items = []
+            for i in range(nit[k]):
+                w = int(its[k, i])
+                vid, seg, batch = lw.keys[ti][w >> 16]
+                items.append([vid, seg.mig, seg.mps, batch, w & 0xFFFF])
+            rows.append({"items": items, "slices": int(st[k, 0]), "capacity": float(st[k, 1]),
+                         "accuracy": float(st[k, 2]), "latency": float(st[k, 3]),
+                         "fanout": [float(x) for x in st[k, 4:4 + outd]]})
+        out[t] = rows
+    return out
