@@ -57,7 +57,7 @@ enum BufId {
   B_PCAP, B_PACC, B_PLAT, B_PFAN, B_RANKP, B_RANKM, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
   B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
-  B_COUNT
+  B_BOFF, B_PART, B_INC, B_COUNT
 };
 
 struct jsv_context {
@@ -124,6 +124,8 @@ extern "C" int jsv_context_create(int device, jsv_context** out) {
   CK(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10)
     return fail(JSV_ERR_NODEV, std::string("libjsv is built for sm_100a, device is ") + prop.name);
+  // the leaf evaluator keeps per-task arrays on the thread stack; make room explicitly
+  CK(cudaDeviceSetLimit(cudaLimitStackSize, 8192));
   auto* c = new jsv_context();
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
@@ -488,6 +490,7 @@ static int get_s1plan(jsv_problem& p, const jsv_request& rq, std::shared_ptr<S1P
 
 struct BatchState {
   int n = 0;
+  int feasible_only = 0;
   std::shared_ptr<S1Plan> pl;
   S1Args s1{};
   std::vector<int> pool_n;
@@ -671,6 +674,16 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   s2_base(p, bs, a);
   a.diag = diag ? 1 : 0;
   a.want_config = want_config ? 1 : 0;
+  const bool fonly = bs.feasible_only != 0;
+  a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
+  a.ipt = 16;
+  CK(B[B_INC].ensure(sizeof(unsigned long long) * n));
+  CK(cudaMemsetAsync(B[B_INC].p, 0, sizeof(unsigned long long) * n, st));
+  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
+  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
+  a.inc = B[B_INC].as<unsigned long long>();
+  a.active = B[B_ACTIVE].as<int>();
+  a.dbg = getenv("JSV_DEBUG") ? 1 : 0;
   std::vector<long long> fcount(n, 0);
   for (int i = 0; i < n; ++i) fcount[i] = (active[i] && !bs.dead[i]) ? 1 : 0;
   std::vector<long long> foff(n), woff(n + 1), nxt_off(n), nxt_cap(n);
@@ -730,8 +743,37 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
     a.nxt_off = B[B_NXTOFF].as<long long>();
     a.nxt_cap = B[B_NXTCAP].as<long long>();
     a.total_work = total;
-    c.stats.kernel_launches += launch_stage2_level(a, st);
+    if (last) {
+      std::vector<long long> boff(n + 1);
+      long long nb = 0;
+      const long long per_block = 256LL * a.ipt;
+      for (int i = 0; i < n; ++i) {
+        boff[i] = nb;
+        nb += (woff[i + 1] - woff[i] + per_block - 1) / per_block;
+      }
+      boff[n] = nb;
+      CK(B[B_BOFF].ensure(sizeof(long long) * (n + 1)));
+      CK(cudaMemcpyAsync(B[B_BOFF].p, boff.data(), sizeof(long long) * (n + 1),
+                         cudaMemcpyHostToDevice, st));
+      CK(B[B_PART].ensure(sizeof(LeafPart) * std::max<long long>(1, nb)));
+      a.boff = B[B_BOFF].as<long long>();
+      a.part = B[B_PART].as<LeafPart>();
+      c.stats.kernel_launches += launch_stage2_leaf(a, nb, st);
+    } else {
+      c.stats.kernel_launches += launch_stage2_level(a, st);
+    }
     CK(cudaGetLastError());
+    if (getenv("JSV_DEBUG")) {
+      std::vector<int> pp(std::max<long long>(1, F), 0);
+      for (int i = 0; i < n; ++i)
+        for (long long k = 0; k < fcount[i]; ++k) pp[foff[i] + k] = i;
+      CK(B[B_PPROBE].ensure(sizeof(int) * pp.size()));
+      CK(cudaMemcpy(B[B_PPROBE].p, pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice));
+      launch_stage2_check(a, F, L, B[B_PPROBE].as<int>(), st);
+      CK(cudaStreamSynchronize(st));
+      fprintf(stderr, "[jsv] level %d F=%lld total_work=%lld diag=%d mode=%d\n", L, F, total,
+              (int)diag, a.mode);
+    }
     if (diag && F > 0) {
       std::vector<int> pp(F);
       for (int i = 0; i < n; ++i)
@@ -847,6 +889,7 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   if (rq.pareto_width < 1 || rq.pareto_width > 32766) return fail(JSV_ERR_ARG, "pareto_width");
   if (rq.n_mix < 0 || rq.n_mix > JSV_MAX_MIX) return fail(JSV_ERR_ARG, "too many mix fractions");
   BatchState bs;
+  bs.feasible_only = rq.feasible_only;
   bs.probes.resize(n);
   for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], bs.probes[i]);
   CK(cudaEventRecord(c.ev[0], st));
@@ -870,6 +913,10 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     CK(cudaStreamSynchronize(st));
     std::vector<int> redo(n, 0);
     bool any = false;
+    if (getenv("JSV_DEBUG"))
+      for (int i = 0; i < n; ++i)
+        fprintf(stderr, "[jsv] probe %d has %d leaves %llu obj %.17g\n", i, best[i].has,
+                best[i].leaves, best[i].obj);
     for (int i = 0; i < n; ++i) {
       if (!best[i].has && !bs.dead[i] && want_config) {
         redo[i] = 1;

@@ -6,6 +6,7 @@
 // division (the nvcc default -prec-div=true) is used everywhere.
 #pragma once
 #include <cstdint>
+#include <cstdio>
 #include <cuda_runtime.h>
 #include "../../include/jsv.h"
 

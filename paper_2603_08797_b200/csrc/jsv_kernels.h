@@ -88,7 +88,33 @@ struct S2Args {
   const long long* nxt_cap;     // [n_probes]
   long long total_work;
   int* err;
+  // leaf level: blocks own (probe, chunk); per-block partial best, then a per-probe reduce
+  int mode;                 // LEAF_FULL / LEAF_FIRST / LEAF_ANY
+  const long long* boff;    // [n_probes+1] leaf-block offsets
+  int ipt;                  // work items per thread in the leaf kernel
+  struct LeafPart* part;    // [total leaf blocks]
+  unsigned long long* inc;  // [n_probes] incumbent objective (order-preserving bits)
+  int dbg;
 };
+
+#define LEAF_FULL 0
+#define LEAF_FIRST 1
+#define LEAF_ANY 2
+
+struct LeafPart {
+  int has;        // feasible candidate
+  int sl;
+  double obj;
+  long long code; // (prefix << 16) | choice-at-last-level (0xFFFF = empty)
+  int has_leaf;   // reached leaf (diagnostics)
+  int pad_;
+  long long leaf; // max reached leaf code
+  unsigned long long leaves;
+};
+
+int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st);
+int launch_stage2_check(const S2Args& a, long long n, int depth, const int* pp, cudaStream_t st);
+int launch_stage2_reduce(const S2Args& a, cudaStream_t st);
 
 int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
                        cudaStream_t st);

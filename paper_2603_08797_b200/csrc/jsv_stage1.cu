@@ -515,16 +515,22 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     ++launches;
   }
   long long tot = (long long)a.n_probes * a.C_probe;
-  k_stats<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
-  ++launches;
-  dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
-  DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a);
-  ++launches;
+  if (tot > 0) {
+    k_stats<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
+    ++launches;
+  }
+  if (L.tiles_pp > 0) {
+    dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
+    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a);
+    ++launches;
+  }
   k_compact<<<a.n_probes * a.T, 1024, 0, st>>>(a);
   ++launches;
-  dim3 gb((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_b);
-  DISPATCH_D(a.D, k_pairs_b, gb, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_b);
-  ++launches;
+  if (L.tiles_pp > 0) {
+    dim3 gb((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_b);
+    DISPATCH_D(a.D, k_pairs_b, gb, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_b);
+    ++launches;
+  }
   k_truncate<<<a.n_probes * a.T, 1024, 0, st>>>(a);
   ++launches;
   dim3 gm((unsigned)(a.n_probes * a.T), (unsigned)((2 * (a.W + 1) + 255) / 256));

@@ -94,302 +94,8 @@ __device__ inline void load_leaf(const S2Args& a, int probe, const uint16_t* ch_
   }
 }
 
-__device__ inline void with_lock(int* lock, bool& done) { done = atomicCAS(lock, 0, 1) == 0; }
+#include "jsv_search.cuh"
 
-__device__ void leaf_visit(const S2Args& a, int probe, const uint16_t* ch_topo) {
-  const DGraph& g = *a.g;
-  const DReq& rq = *a.rq;
-  const DProbe& pr = a.probes[probe];
-  BestRec* B = a.best + probe;
-  double lat[MAXT], cap[MAXT], acc[MAXT], fan[MAXE];
-  int sl[MAXT];
-  uint32_t present;
-  load_leaf(a, probe, ch_topo, lat, cap, acc, sl, fan, present);
-  EvalOut ev;
-  evaluate<false>(g, rq, pr, lat, cap, acc, sl, fan, present, ev, nullptr, nullptr, nullptr,
-                  nullptr);
-  atomicAdd(&B->leaves, 1ull);
-  if (a.diag) {
-    // last reached leaf in DFS order = lexicographically largest choice vector
-    unsigned long long lk[4];
-    leaf_key(a.T, ch_topo, lk);
-    volatile BestRec* VB = B;
-    if (!(VB->has_leaf && lk[0] < VB->leafkey[0])) {
-      bool done = false;
-      while (!done) {
-        with_lock(&B->lock, done);
-        if (done) {
-          __threadfence();
-          if (!B->has_leaf || cmp_words(lk, B->leafkey, 4) > 0) {
-            for (int k = 0; k < 4; ++k) B->leafkey[k] = lk[k];
-            for (int k = 0; k < a.T; ++k) B->leaf_choice[k] = ch_topo[k];
-            B->has_leaf = 1;
-          }
-          __threadfence();
-          atomicExch(&B->lock, 0);
-        }
-      }
-    }
-  }
-  if (!ev.feasible) return;
-  if (rq.feasible_only) {
-    if (!a.want_config) {
-      if (!B->found) {
-        bool done = false;
-        while (!done) {
-          with_lock(&B->lock, done);
-          if (done) {
-            __threadfence();
-            if (!B->has) {
-              for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
-              B->obj = ev.objective;
-              B->sl = ev.total_sl;
-              B->has = 1;
-              B->found = 1;
-            }
-            __threadfence();
-            atomicExch(&B->lock, 0);
-          }
-        }
-      }
-      return;
-    }
-    // first feasible leaf in DFS order = lexicographically smallest choice vector
-    unsigned long long lk[4];
-    leaf_key(a.T, ch_topo, lk);
-    volatile BestRec* VB = B;
-    if (VB->has && lk[0] > VB->tie[0]) return;
-    bool done = false;
-    while (!done) {
-      with_lock(&B->lock, done);
-      if (done) {
-        __threadfence();
-        if (!B->has || cmp_words(lk, B->tie, 4) < 0) {
-          for (int k = 0; k < 4; ++k) B->tie[k] = lk[k];
-          for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
-          B->obj = ev.objective;
-          B->sl = ev.total_sl;
-          B->has = 1;
-          B->found = 1;
-        }
-        __threadfence();
-        atomicExch(&B->lock, 0);
-      }
-    }
-    return;
-  }
-  {
-    volatile BestRec* VB = B;
-    if (VB->has) {
-      double bo = VB->obj;
-      int bs = VB->sl;
-      if (ev.objective < bo || (ev.objective == bo && ev.total_sl > bs)) return;
-    }
-  }
-  uint16_t cb[MAXT];
-  for (int u = 0; u < a.T; ++u) cb[u] = ch_topo[g.pos_of[u]];
-  unsigned long long tk[4];
-  tie_key(a, probe, cb, tk);
-  bool done = false;
-  while (!done) {
-    with_lock(&B->lock, done);
-    if (done) {
-      __threadfence();
-      bool better;
-      if (!B->has) better = true;
-      else if (ev.objective != B->obj) better = ev.objective > B->obj;
-      else if (ev.total_sl != B->sl) better = ev.total_sl < B->sl;
-      else better = cmp_words(tk, B->tie, 4) < 0;
-      if (better) {
-        B->obj = ev.objective;
-        B->sl = ev.total_sl;
-        for (int k = 0; k < 4; ++k) B->tie[k] = tk[k];
-        for (int k = 0; k < a.T; ++k) B->choice[k] = ch_topo[k];
-        B->has = 1;
-        B->found = 1;
-      }
-      __threadfence();
-      atomicExch(&B->lock, 0);
-    }
-  }
-}
-
-__global__ void __launch_bounds__(256) k_s2_level(S2Args a) {
-  const DGraph& g = *a.g;
-  const DReq& rq = *a.rq;
-  const int T = a.T, L = a.level;
-  const int t = g.topo[L];
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < a.total_work;
-       w += stride) {
-    int lo = 0, hi = a.n_probes - 1;
-    while (lo < hi) {
-      int mid = (lo + hi + 1) >> 1;
-      if (a.woff[mid] <= w) lo = mid;
-      else hi = mid - 1;
-    }
-    const int probe = lo;
-    BestRec* B = a.best + probe;
-    if (!a.diag && rq.feasible_only && !a.want_config && ((volatile BestRec*)B)->found) continue;
-    const long long lw = w - a.woff[probe];
-    const int width = a.width[probe];
-    const long long p = lw / width;
-    const int b = (int)(lw % width);
-    const long long pidx = a.foff[probe] + p;
-    uint16_t ch[MAXT];
-    for (int k = 0; k < L; ++k) ch[k] = a.cur[pidx * T + k];
-    const DProbe& pr = a.probes[probe];
-    const int jb = probe * T;
-    // demand reaching each task so far (_demand_at, planner.py:821-833)
-    double r[MAXT];
-    int used = 0;
-    for (int k = 0; k <= L; ++k) {
-      const int u = g.topo[k];
-      double ru;
-      if (u == g.entry) {
-        ru = pr.demand;
-      } else {
-        ru = 0.0;
-        for (int qq = g.pred_off[u]; qq < g.pred_off[u + 1]; ++qq) {
-          const int e = g.pred_edge[qq];
-          const int s = g.edge_src[e];
-          const int cs = ch[g.pos_of[s]];
-          if (cs == NONE16 || r[s] == 0.0) continue;
-          const double fan = rq.has_ov[e]
-                                 ? rq.ov[e]
-                                 : a.p_fan[((long long)(jb + s) * a.W + cs) * a.maxout +
-                                           (e - g.succ_off[s])];
-          ru += r[s] * fan;
-        }
-      }
-      r[u] = ru;
-      if (k < L && ch[k] != NONE16) used += a.p_sl[(long long)(jb + u) * a.W + ch[k]];
-    }
-    const double rt = r[t];
-    if (rt == 0.0) {
-      // nothing flows here: the empty assignment is the only child (planner.py:868-875)
-      if (b != 0) continue;
-      ch[L] = NONE16;
-      if (a.last) {
-        leaf_visit(a, probe, ch);
-      } else {
-        unsigned long long pos = atomicAdd(&a.nxt_cnt[probe], 1ull);
-        if ((long long)pos >= a.nxt_cap[probe]) { atomicExch(a.err, 3); continue; }
-        uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
-        for (int k = 0; k <= L; ++k) dst[k] = ch[k];
-      }
-      continue;
-    }
-    if (a.diag && b == 0) atomicOr(&a.cur_flag[pidx], 1);
-    const int P = a.pool_n[jb + t];
-    if (b >= P) continue;
-    const long long q = (long long)(jb + t) * a.W + b;
-    const int* fut = a.future + probe * (T + 1);
-    const double need = rt * (1.0 + rq.slack);
-    const double eps = rq.eps;
-    int why = -1;
-    double ub = 0.0;
-    const int bsl = a.p_sl[q];
-    if (a.p_cap[q] + eps < need) {
-      why = JSV_BIND_THROUGHPUT;
-    } else if ((double)(used + bsl + fut[L + 1]) > (double)rq.S + eps) {
-      why = JSV_BIND_RESOURCES;
-    } else {
-      // partial-path latency with lower bounds for open tasks (_latency_ok, 805-819)
-      const double lat2 = 2.0 * a.p_lat[q];
-      bool ok = true;
-      for (int pp = 0; pp < g.P && ok; ++pp) {
-        if (!((g.path_mask[pp] >> t) & 1u)) continue;
-        double tot = 0.0;
-        for (int k = g.path_off[pp]; k < g.path_off[pp + 1]; ++k) {
-          const int u = g.path_task[k];
-          if (u == t) {
-            tot += lat2;
-          } else if (g.pos_of[u] < L) {
-            const int c = ch[g.pos_of[u]];
-            tot += (c == NONE16) ? 0.0 : 2.0 * a.p_lat[(long long)(jb + u) * a.W + c];
-          } else {
-            tot += a.min_lat2[jb + u];
-          }
-        }
-        if (tot > pr.slo_eff + eps) ok = false;
-      }
-      if (!ok) {
-        why = JSV_BIND_LATENCY;
-      } else {
-        double acc[MAXT];
-        for (int u = 0; u < T; ++u) {
-          const int pu = g.pos_of[u];
-          if (pu < L) {
-            const int c = ch[pu];
-            acc[u] = (c == NONE16) ? 1.0 : a.p_acc[(long long)(jb + u) * a.W + c];
-          } else if (u == t) {
-            acc[u] = a.p_acc[q];
-          } else {
-            acc[u] = a.acc_ub[jb + u];
-          }
-        }
-        ub = weighted_paths(g, acc) / g.a_max;
-        if (ub < pr.acc_slo - eps) why = JSV_BIND_ACCURACY;
-      }
-    }
-    if (why >= 0) {
-      if (a.diag) atomicAdd(&B->kills[L][why], 1);
-      continue;
-    }
-    if (a.diag) atomicOr(&a.cur_flag[pidx], 2);
-    if (!rq.feasible_only) {
-      volatile BestRec* VB = B;
-      if (VB->has) {
-        const double obj_ub = pr.alpha * ub - pr.beta * (double)(used + bsl + fut[L + 1]);
-        if (obj_ub < VB->obj - eps) continue;  // bound prune (counts as a survivor)
-      }
-    }
-    ch[L] = (uint16_t)b;
-    if (a.last) {
-      leaf_visit(a, probe, ch);
-    } else {
-      unsigned long long pos = atomicAdd(&a.nxt_cnt[probe], 1ull);
-      if ((long long)pos >= a.nxt_cap[probe]) { atomicExch(a.err, 3); continue; }
-      uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
-      for (int k = 0; k <= L; ++k) dst[k] = ch[k];
-    }
-  }
-}
-
-// deepest blocked level: a prefix with r > 0 whose children all died (planner.py:910-911)
-__global__ void k_s2_blocked(S2Args a, long long n_prefix, const int* prefix_probe) {
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n_prefix) return;
-  const int f = a.cur_flag[i];
-  if ((f & 1) && !(f & 2)) atomicMax(&a.best[prefix_probe[i]].deepest, a.level);
-}
-
-int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
-                       cudaStream_t st) {
-  // S2Args.min_lat2 etc. point at Stage-1 per-pool values on entry
-  k_s2_prep<<<(a.n_probes + 127) / 128, 128, 0, st>>>(a, min_lat2, min_sl, acc_ub, future,
-                                                       a.min_lat2, a.min_sl, a.acc_ub);
-  return 1;
-}
-
-int launch_stage2_level(const S2Args& a, cudaStream_t st) {
-  if (a.total_work <= 0) return 0;
-  long long blocks = (a.total_work + 255) / 256;
-  if (blocks > 148 * 16) blocks = 148 * 16;
-  k_s2_level<<<(unsigned)blocks, 256, 0, st>>>(a);
-  return 1;
-}
-
-int launch_stage2_blocked(const S2Args& a, long long n_prefix_total, const int* prefix_probe,
-                          cudaStream_t st) {
-  if (n_prefix_total <= 0) return 0;
-  k_s2_blocked<<<(unsigned)((n_prefix_total + 255) / 256), 256, 0, st>>>(a, n_prefix_total,
-                                                                         prefix_probe);
-  return 1;
-}
-
-// ------------------------------------------------------------- finalisation
 
 __device__ void write_config(const FinArgs& a, int probe, const uint16_t* cb_task,
                              jsv_plan_out& o) {
