@@ -173,6 +173,10 @@ typedef struct {
   int64_t leaves;                       /* Stage-2 candidates evaluated */
   int64_t nodes;
   int32_t kernel_launches;
+  int32_t dims;                         /* skyline row width D (padded) */
+  int64_t pair_tests_a;                 /* sum over jobs of n^2 (Stage-1 skyline pairs) */
+  int64_t pair_tests_b;                 /* sum over jobs of F^2 (frontier ranking pairs) */
+  int64_t leaf_work;                    /* (prefix, bundle) items at the last level */
 } jsv_stats;
 
 const char* jsv_last_error(void);
@@ -217,6 +221,15 @@ int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const jsv_request* 
                   int32_t* n_items, uint32_t* items, double* stats, int32_t* truncated);
 
 int jsv_last_stats(jsv_context* ctx, jsv_stats* out);
+
+/* Per-kernel CUDA-event timing on the library stream (bench roofline).
+ * jsv_profile(on) resets the accumulators; jsv_kernel_times fills ms[k] /
+ * count[k] for kernel ids 0..n-1 (see JSV_KERNEL_NAMES) and returns the id count. */
+int jsv_profile(jsv_context* ctx, int on);
+int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
+#define JSV_KERNEL_NAMES \
+  "generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank", "s2_prep", \
+  "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed"
 
 #ifdef __cplusplus
 }

@@ -82,7 +82,8 @@ class DemandOut(C.Structure):
 class Stats(C.Structure):
     _fields_ = [("ms_stage1", C.c_float), ("ms_stage2", C.c_float), ("ms_total", C.c_float),
                 ("candidates_generated", C.c_int64), ("leaves", C.c_int64), ("nodes", C.c_int64),
-                ("kernel_launches", C.c_int32)]
+                ("kernel_launches", C.c_int32), ("dims", C.c_int32), ("pair_tests_a", C.c_int64),
+                ("pair_tests_b", C.c_int64), ("leaf_work", C.c_int64)]
 
 
 EXPORTS = {
@@ -106,7 +107,25 @@ EXPORTS = {
     "jsv_pool_dump": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.POINTER(Probe),
                                 C.c_int32, C.c_int32, _I32P, _I32P, _U32P, _F64P, _I32P]),
     "jsv_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "jsv_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "jsv_kernel_times": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double),
+                                   C.POINTER(C.c_int64)]),
 }
+
+KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",
+                "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed")
+
+
+def profile(ctx, on: bool) -> None:
+    check(load_library().jsv_profile(ctx, 1 if on else 0))
+
+
+def kernel_times(ctx) -> dict:
+    n = len(KERNEL_NAMES)
+    ms = (C.c_double * n)()
+    cnt = (C.c_int64 * n)()
+    load_library().jsv_kernel_times(ctx, n, ms, cnt)
+    return {KERNEL_NAMES[i]: (ms[i], cnt[i]) for i in range(n)}
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libjsv.so")
 _lib = None

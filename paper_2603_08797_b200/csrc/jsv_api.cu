@@ -66,7 +66,54 @@ struct jsv_context {
   cudaEvent_t ev[4] = {};
   DevBuf buf[B_COUNT];
   jsv_stats stats{};
+  Prof prof;
+  double kms[K_COUNT_] = {};
+  long long kcnt[K_COUNT_] = {};
 };
+
+thread_local Prof* g_prof = nullptr;
+
+// fold the per-kernel event pairs recorded since the last collection (stream is idle)
+static void collect_prof(jsv_context& c) {
+  Prof& P = c.prof;
+  if (!P.on) return;
+  for (size_t i = 0; i + 1 < P.used; i += 2) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, P.ev[i], P.ev[i + 1]) == cudaSuccess) {
+      c.kms[P.ids[i / 2]] += ms;
+      c.kcnt[P.ids[i / 2]] += 1;
+    }
+  }
+  P.used = 0;
+}
+
+struct ProfScope {
+  explicit ProfScope(jsv_context* c) {
+    c->prof.st = c->st;
+    g_prof = c->prof.on ? &c->prof : nullptr;
+  }
+  ~ProfScope() { g_prof = nullptr; }
+};
+
+extern "C" int jsv_profile(jsv_context* ctx, int on) {
+  if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  ctx->prof.on = on != 0;
+  ctx->prof.st = ctx->st;
+  for (int k = 0; k < K_COUNT_; ++k) {
+    ctx->kms[k] = 0.0;
+    ctx->kcnt[k] = 0;
+  }
+  return JSV_OK;
+}
+
+extern "C" int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count) {
+  if (!ctx || !ms || !count) return fail(JSV_ERR_ARG, "null argument");
+  for (int k = 0; k < n && k < K_COUNT_; ++k) {
+    ms[k] = ctx->kms[k];
+    count[k] = ctx->kcnt[k];
+  }
+  return K_COUNT_;
+}
 
 struct S1Plan {
   std::vector<GenDesc> desc;
@@ -708,6 +755,7 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
     }
     woff[n] = total;
     if (total == 0) break;
+    if (last && !diag) c.stats.leaf_work += total;
     long long NO = 0;
     for (int i = 0; i < n; ++i) {
       nxt_off[i] = NO;
@@ -934,6 +982,7 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   if (rc) return rc;
   CK(cudaEventRecord(c.ev[3], st));
   CK(cudaEventSynchronize(c.ev[3]));
+  collect_prof(c);
   float ms1 = 0, ms2 = 0, mst = 0;
   cudaEventElapsedTime(&ms1, c.ev[0], c.ev[1]);
   cudaEventElapsedTime(&ms2, c.ev[1], c.ev[2]);
@@ -943,9 +992,15 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   c.stats.ms_total += mst;
   long long gen = 0;
   {
-    std::vector<int> cnt((size_t)n * p.T);
+    std::vector<int> cnt((size_t)n * p.T), fc((size_t)n * p.T);
     CK(cudaMemcpy(cnt.data(), bs.s1.cnt, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost));
-    for (int v : cnt) gen += v;
+    CK(cudaMemcpy(fc.data(), bs.s1.fcnt, sizeof(int) * fc.size(), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < cnt.size(); ++i) {
+      gen += cnt[i];
+      c.stats.pair_tests_a += (long long)cnt[i] * cnt[i];
+      c.stats.pair_tests_b += (long long)fc[i] * fc[i];
+    }
+    c.stats.dims = bs.s1.D;
   }
   c.stats.candidates_generated += gen;
   return JSV_OK;
@@ -957,6 +1012,7 @@ extern "C" int jsv_plan_batch(jsv_context* ctx, const jsv_problem* prob, const j
   if (n == 0) return JSV_OK;
   CK(cudaSetDevice(ctx->device));
   memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ProfScope ps(ctx);
   return plan_batch_internal(*const_cast<jsv_problem*>(prob), *req, n, probes, out, true);
 }
 
@@ -983,6 +1039,7 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
   if (n == 0) return JSV_OK;
   CK(cudaSetDevice(ctx->device));
   memset(&ctx->stats, 0, sizeof(ctx->stats));
+  ProfScope pscope(ctx);
   jsv_problem& p = *const_cast<jsv_problem*>(prob);
   jsv_request preq = *req;
   preq.feasible_only = 1;

@@ -1,6 +1,49 @@
 // jsv_kernels.h -- kernel argument blocks and launchers shared by the host runtime.
 #pragma once
+#include <vector>
 #include "jsv_internal.cuh"
+
+// Per-kernel CUDA-event timing on the launching stream (bench.py roofline).
+enum KernelId {
+  K_GENERATE, K_STATS, K_PAIRS_A, K_COMPACT, K_PAIRS_B, K_TRUNCATE, K_MRANK, K_S2_PREP,
+  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_COUNT_
+};
+
+struct Prof {
+  bool on = false;
+  cudaStream_t st = nullptr;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> ids;
+  size_t used = 0;
+  void begin(int id) {
+    if (!on) return;
+    if (used + 2 > ev.size()) {
+      for (int i = 0; i < 64; ++i) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ev.push_back(e);
+      }
+    }
+    ids.resize(ev.size() / 2 + 1);
+    ids[used / 2] = id;
+    cudaEventRecord(ev[used], st);
+  }
+  void end() {
+    if (!on) return;
+    cudaEventRecord(ev[used + 1], st);
+    used += 2;
+  }
+};
+
+extern thread_local Prof* g_prof;
+#define PROF_BEGIN(id) \
+  do {                 \
+    if (g_prof) g_prof->begin(id); \
+  } while (0)
+#define PROF_END()     \
+  do {                 \
+    if (g_prof) g_prof->end(); \
+  } while (0)
 
 struct S1Args {
   const DGraph* g;

@@ -421,8 +421,10 @@ __global__ void k_s2_blocked(S2Args a, long long n_prefix, const int* prefix_pro
 int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
                        cudaStream_t st) {
   // on entry S2Args.min_lat2 / min_sl / acc_ub point at the Stage-1 per-pool values
+  PROF_BEGIN(K_S2_PREP);
   k_s2_prep<<<(a.n_probes + 127) / 128, 128, 0, st>>>(a, min_lat2, min_sl, acc_ub, future,
                                                        a.min_lat2, a.min_sl, a.acc_ub);
+  PROF_END();
   return 1;
 }
 
@@ -430,14 +432,20 @@ int launch_stage2_level(const S2Args& a, cudaStream_t st) {
   if (a.total_work <= 0) return 0;
   long long blocks = (a.total_work + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
+  PROF_BEGIN(K_S2_LEVEL);
   k_s2_level<<<(unsigned)blocks, 256, 0, st>>>(a);
+  PROF_END();
   return 1;
 }
 
 int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st) {
   if (n_blocks <= 0) return 0;
+  PROF_BEGIN(K_S2_LEAF);
   k_s2_leaf<<<(unsigned)n_blocks, 256, 0, st>>>(a);
+  PROF_END();
+  PROF_BEGIN(K_S2_REDUCE);
   k_s2_reduce<<<a.n_probes, 256, 0, st>>>(a);
+  PROF_END();
   return 2;
 }
 

@@ -511,30 +511,44 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   int launches = 0;
   long long gen = (long long)a.n_probes * a.U;
   if (gen > 0) {
+    PROF_BEGIN(K_GENERATE);
     k_generate<<<(unsigned)((gen + 255) / 256), 256, 0, st>>>(a);
+    PROF_END();
     ++launches;
   }
   long long tot = (long long)a.n_probes * a.C_probe;
   if (tot > 0) {
+    PROF_BEGIN(K_STATS);
     k_stats<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(a);
+    PROF_END();
     ++launches;
   }
   if (L.tiles_pp > 0) {
     dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
+    PROF_BEGIN(K_PAIRS_A);
     DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a);
+    PROF_END();
     ++launches;
   }
+  PROF_BEGIN(K_COMPACT);
   k_compact<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+  PROF_END();
   ++launches;
   if (L.tiles_pp > 0) {
     dim3 gb((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_b);
+    PROF_BEGIN(K_PAIRS_B);
     DISPATCH_D(a.D, k_pairs_b, gb, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_b);
+    PROF_END();
     ++launches;
   }
+  PROF_BEGIN(K_TRUNCATE);
   k_truncate<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+  PROF_END();
   ++launches;
   dim3 gm((unsigned)(a.n_probes * a.T), (unsigned)((2 * (a.W + 1) + 255) / 256));
+  PROF_BEGIN(K_MRANK);
   k_mrank<<<gm, 256, 0, st>>>(a);
+  PROF_END();
   ++launches;
   return launches;
 }

@@ -225,7 +225,9 @@ __global__ void k_finalize(FinArgs a) {
 }
 
 int launch_finalize(const FinArgs& a, cudaStream_t st) {
+  PROF_BEGIN(K_FINALIZE);
   k_finalize<<<(a.n_probes + 63) / 64, 64, 0, st>>>(a);
+  PROF_END();
   return 1;
 }
 
@@ -321,7 +323,9 @@ __global__ void __launch_bounds__(256) k_uni_pick(S2Args a, FinArgs f, int* pick
 }
 
 int launch_uninformed(const S2Args& a, const FinArgs& f, int* pick, int* kills, cudaStream_t st) {
+  PROF_BEGIN(K_UNINFORMED);
   k_uni_pick<<<a.n_probes * a.T, 256, 0, st>>>(a, f, pick, kills);
+  PROF_END();
   return 1;
 }
 
