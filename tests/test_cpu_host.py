@@ -1,0 +1,220 @@
+"""CPU-only tests: C-ABI surface, host lowering, numerics helpers, multi-process plumbing."""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import random
+import re
+import subprocess
+import tempfile
+
+import pytest
+
+from golden_io import case_inputs, load
+from oracle import planner_oracle as O
+from paper_2603_08797_b200 import _lower as LW
+from paper_2603_08797_b200 import _native as N
+from paper_2603_08797_b200.model import app_from_dict
+from paper_2603_08797_b200.profiles import profile_from_rows
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "jsv.h")
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(N.LIB_PATH):
+        from paper_2603_08797_b200 import _build
+        _build.build()
+    return N.load_library()
+
+
+def header_functions() -> list[str]:
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"^\s*(?:int|void|const char\*)\s+(jsv_\w+)\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol(lib):
+    names = header_functions()
+    assert len(names) >= 12
+    for n in names:
+        assert hasattr(lib, n), n
+        assert n in N.EXPORTS, f"{n} not bound in _native.EXPORTS"
+
+
+def test_no_cpu_fallback_without_gpu(lib):
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    h = C.c_void_p()
+    assert lib.jsv_context_create(0, C.byref(h)) == 4  # JSV_ERR_NODEV
+    assert b"no CPU fallback" in lib.jsv_last_error()
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.errors import NativeError
+
+    app, table, req, opt = case_inputs(load("plans_bundled.json")[0])
+    with pytest.raises(NativeError):
+        P.plan(app, table, req, opt)
+
+
+def test_product_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2603_08797_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                text = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(from|import)\s+oracle", text, re.M), f
+
+
+C_LAYOUT = r"""
+#include <stdio.h>
+#include <stddef.h>
+#include "jsv.h"
+#define P(T) printf(#T " %zu\n", sizeof(T));
+#define O(T, f) printf(#T "." #f " %zu\n", offsetof(T, f));
+int main(void) {
+  P(jsv_problem_desc) P(jsv_request) P(jsv_probe) P(jsv_plan_out) P(jsv_demand_out) P(jsv_stats)
+  O(jsv_request, mix) O(jsv_request, feasible_only) O(jsv_probe, uni_min_cost)
+  O(jsv_plan_out, items) O(jsv_plan_out, hput) O(jsv_plan_out, lat_margin)
+  O(jsv_plan_out, acc_margin) O(jsv_problem_desc, a_max) O(jsv_stats, leaf_work)
+  return 0;
+}
+"""
+
+
+def test_ctypes_layout_matches_the_c_header():
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "l.c")
+        exe = os.path.join(d, "l")
+        open(src, "w").write(C_LAYOUT)
+        subprocess.run(["gcc", "-I", os.path.join(ROOT, "include"), src, "-o", exe], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    got = dict(line.rsplit(" ", 1) for line in out.strip().splitlines())
+    py = {"jsv_problem_desc": N.ProblemDesc, "jsv_request": N.Request, "jsv_probe": N.Probe,
+          "jsv_plan_out": N.PlanOut, "jsv_demand_out": N.DemandOut, "jsv_stats": N.Stats}
+    for name, cls in py.items():
+        assert int(got[name]) == C.sizeof(cls), name
+    for key, val in got.items():
+        if "." in key:
+            s, f = key.split(".")
+            assert int(val) == getattr(py[s], f).offset, key
+
+
+def pysum_restated(xs):
+    """The device PySum (jsv_internal.cuh): CPython 3.12 sum() of floats from int 0."""
+    if not xs:
+        return 0
+    f, c = 0.0 + xs[0], 0.0
+    for x in xs[1:]:
+        t = f + x
+        if abs(f) >= abs(x):
+            c += (f - t) + x
+        else:
+            c += (x - t) + f
+        f = t
+    if c and c == c and abs(c) != float("inf"):
+        f += c
+    return f
+
+
+def test_device_pysum_algorithm_matches_cpython_sum():
+    rng = random.Random(7)
+    differs = 0
+    for _ in range(20000):
+        xs = [2.0 * rng.uniform(1.0, 900.0) for _ in range(rng.randint(1, 6))]
+        assert pysum_restated(xs) == sum(xs)
+        naive = 0.0
+        for x in xs:
+            naive += x
+        differs += naive != sum(xs)
+    assert differs > 100  # the compensated sum genuinely differs from naive summation
+
+
+@pytest.mark.parametrize("name", ["social-media", "traffic-analysis", "ar-assistant"])
+def test_lowering_ranks_and_subspaces_follow_python_order(name):
+    doc = load("apps.json")[name]
+    app = app_from_dict(doc["app"])
+    table = profile_from_rows(doc["profile"])
+    lw = LW.lower(app, table)
+    assert lw.ids == sorted(app.graph.task_ids)
+    for ti, t in enumerate(lw.ids):
+        task = app.graph.task(t)
+        keys = lw.keys[ti]
+        assert keys == sorted(keys, key=lambda k: (k[0], k[1].mig, k[1].mps, k[2]))
+        for a in (0, 1):
+            for s in (0, 1):
+                rows = O.tuples_of(task, table, O.variants_in(task, bool(a)), O.segments_in(bool(s)))
+                got = [keys[i] for i in lw.sub_tuples[ti][2 * a + s]]
+                assert got == [(r[0], r[1], r[2]) for r in rows]
+
+
+def test_uninformed_statics_match_the_oracle():
+    for doc in load("plans_bundled.json"):
+        app, table, req, opt = case_inputs(doc)
+        if req.space.task_graph_informed:
+            continue
+        lw = LW.lower(app, table)
+        st = LW.uninformed_statics(app, table, lw, req)
+        lat_b, _, _, weight, floor = O.uninformed_budgets(app, table, req)
+        assert st["lat_budget"] == lat_b
+        assert st["weight"] == weight
+        assert st["floor"] == floor
+
+
+# ------------------------------------------------------------ multi-process
+
+def _gloo_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2603_08797_b200 import shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = random.Random(1234 + rank)
+    recs = [(1, round(rng.uniform(0.3, 0.5), 2), rng.randint(5, 9),
+             tuple(rng.randrange(1 << 64) for _ in range(4))) for _ in range(5)]
+    if rank == 1:
+        recs.append((0, 9.0, 0, (0, 0, 0, 0)))  # an infeasible shard never wins
+    local = recs[shard.combine_best(recs)]
+    gathered = shard.all_gather_best(local)
+    win = gathered[shard.combine_best(gathered)]
+    items = list(range(11))
+    mapped = shard.sharded_map(items, lambda xs: [x * x for x in xs])
+    q.put((rank, win, gathered, mapped))
+    dist.destroy_process_group()
+
+
+def test_gloo_two_rank_best_record_combine_and_sharded_map():
+    import torch.multiprocessing as mp
+
+    from paper_2603_08797_b200 import shard
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.Random().randrange(2000)
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    outs = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    outs.sort()
+    (_, w0, g0, m0), (_, w1, g1, m1) = outs
+    assert w0 == w1 and g0 == g1
+    assert g0[shard.combine_best(g0)] == w0
+    assert m0 == m1 == [x * x for x in range(11)]
+    # round trip of the wire format keeps every bit
+    for rec in g0:
+        assert shard.unpack_record(shard.pack_record(rec)) == rec
+
+
+def test_block_range_partitions_exactly():
+    from paper_2603_08797_b200.shard import block_range
+
+    for n in range(0, 40):
+        for w in range(1, 9):
+            spans = [block_range(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
