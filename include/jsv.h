@@ -229,7 +229,7 @@ int jsv_profile(jsv_context* ctx, int on);
 int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
 #define JSV_KERNEL_NAMES \
   "generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank", "s2_prep", \
-  "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed"
+  "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket", "s2_prefix"
 
 #ifdef __cplusplus
 }

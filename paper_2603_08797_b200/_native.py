@@ -113,7 +113,8 @@ EXPORTS = {
 }
 
 KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",
-                "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed")
+                "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket",
+                "s2_prefix")
 
 
 def profile(ctx, on: bool) -> None:

@@ -14,6 +14,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "jsv_internal.cuh"
 #include "jsv_kernels.h"
 
@@ -57,7 +59,8 @@ enum BufId {
   B_PCAP, B_PACC, B_PLAT, B_PFAN, B_RANKP, B_RANKM, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
   B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
-  B_BOFF, B_PART, B_INC, B_COUNT
+  B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
+  B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_COUNT
 };
 
 struct jsv_context {
@@ -590,6 +593,8 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_FCR].ensure(sizeof(int) * C1));
   CK(B[B_SORTED].ensure(sizeof(int) * C1));
   CK(B[B_SCR].ensure(sizeof(int) * C1));
+  CK(B[B_ORDER].ensure(sizeof(int) * C1));
+  CK(B[B_BSTART].ensure(sizeof(int) * jobs * (rq.budget + 2)));
   CK(B[B_CNT].ensure(sizeof(int) * jobs));
   CK(B[B_FCNT].ensure(sizeof(int) * jobs));
   CK(B[B_POOLC].ensure(sizeof(int) * jobs * W));
@@ -653,6 +658,9 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.pool_min_sl = B[B_S1SL].as<int>();
   a.pool_acc_ub = B[B_S1ACC].as<double>();
   a.err = B[B_ERR].as<int>();
+  a.S = rq.budget;
+  a.order = B[B_ORDER].as<int>();
+  a.bstart = B[B_BSTART].as<int>();
   S1Launch L{};
   L.tile_task = B[B_TILE_TASK].as<int>();
   L.tile_start = B[B_TILE_START].as<int>();
@@ -702,6 +710,12 @@ static void s2_base(jsv_problem& p, BatchState& bs, S2Args& a) {
   a.p_fan = bs.s1.p_fan;
   a.rank_p = bs.s1.rank_p;
   a.rank_m = bs.s1.rank_m;
+  a.items = bs.s1.items;
+  a.nitems = bs.s1.nitems;
+  a.pool_cand = bs.s1.pool_cand;
+  a.C_probe = bs.s1.C_probe;
+  for (int t = 0; t <= p.T; ++t) a.task_base[t] = bs.s1.task_base[t];
+  a.maxi = bs.s1.maxi;
   a.min_lat2 = B[B_S2LAT2].as<double>();
   a.min_sl = B[B_S2SL].as<int>();
   a.acc_ub = B[B_S2ACC].as<double>();
@@ -716,7 +730,7 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   jsv_context& c = *p.ctx;
   cudaStream_t st = c.st;
   auto& B = c.buf;
-  const int n = bs.n, T = p.T;
+  const int n = bs.n, T = p.T, P = p.P;
   S2Args a;
   s2_base(p, bs, a);
   a.diag = diag ? 1 : 0;
@@ -724,126 +738,145 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   const bool fonly = bs.feasible_only != 0;
   a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
   a.ipt = 16;
+  a.dbg = getenv("JSV_DEBUG") ? 1 : 0;
   CK(B[B_INC].ensure(sizeof(unsigned long long) * n));
   CK(cudaMemsetAsync(B[B_INC].p, 0, sizeof(unsigned long long) * n, st));
   CK(B[B_ACTIVE].ensure(sizeof(int) * n));
   CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
   a.inc = B[B_INC].as<unsigned long long>();
   a.active = B[B_ACTIVE].as<int>();
-  a.dbg = getenv("JSV_DEBUG") ? 1 : 0;
-  std::vector<long long> fcount(n, 0);
-  for (int i = 0; i < n; ++i) fcount[i] = (active[i] && !bs.dead[i]) ? 1 : 0;
-  std::vector<long long> foff(n), woff(n + 1), nxt_off(n), nxt_cap(n);
-  std::vector<int> width(n);
   // level-0 frontier: one empty prefix per active probe
-  long long F = 0;
-  for (int i = 0; i < n; ++i) { foff[i] = F; F += fcount[i]; }
-  CK(B[B_FR0].ensure(sizeof(uint16_t) * std::max<long long>(1, F) * T));
-  CK(cudaMemsetAsync(B[B_FR0].p, 0xFF, sizeof(uint16_t) * std::max<long long>(1, F) * T, st));
+  std::vector<long long> foff(n), fcap(n, 1), pstart(n), nxt_off(n), nxt_cap(n), boff(n + 1);
+  std::vector<unsigned long long> cnt0(n), ptot(n), fcnt(n);
+  for (int i = 0; i < n; ++i) {
+    foff[i] = i;
+    cnt0[i] = (active[i] && !bs.dead[i]) ? 1 : 0;
+  }
+  long long n_slots = n;
+  CK(B[B_FR0].ensure(sizeof(uint16_t) * n * T));
+  CK(cudaMemsetAsync(B[B_FR0].p, 0xFF, sizeof(uint16_t) * n * T, st));
+  CK(B[B_CNT2].ensure(sizeof(unsigned long long) * n));
+  CK(cudaMemcpyAsync(B[B_CNT2].p, cnt0.data(), sizeof(unsigned long long) * n,
+                     cudaMemcpyHostToDevice, st));
   DevBuf* cur = &B[B_FR0];
   DevBuf* nxt = &B[B_FR1];
+  DevBuf* ccnt = &B[B_CNT2];     // live counts of the current frontier
+  DevBuf* ncnt = &B[B_NXTCNT];   // counts of the next frontier
   long long nodes = 0;
   for (int L = 0; L < T; ++L) {
     const bool last = (L == T - 1);
-    const int t = p.topo[L];
-    long long total = 0;
-    for (int i = 0; i < n; ++i) {
-      width[i] = std::max(1, bs.pool_n[(size_t)i * T + t]);
-      woff[i] = total;
-      total += fcount[i] * width[i];
-      nodes += fcount[i];
-    }
-    woff[n] = total;
-    if (total == 0) break;
-    if (last && !diag) c.stats.leaf_work += total;
-    long long NO = 0;
-    for (int i = 0; i < n; ++i) {
-      nxt_off[i] = NO;
-      nxt_cap[i] = last ? 0 : fcount[i] * width[i];
-      NO += nxt_cap[i];
-    }
-    CK(B[B_WOFF].ensure(sizeof(long long) * (n + 1)));
+    const size_t S1 = (size_t)std::max<long long>(1, n_slots);
     CK(B[B_FOFF].ensure(sizeof(long long) * n));
-    CK(B[B_WIDTH].ensure(sizeof(int) * n));
-    CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
-    CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
-    CK(B[B_NXTCNT].ensure(sizeof(unsigned long long) * n));
-    CK(cudaMemcpyAsync(B[B_WOFF].p, woff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
+    CK(B[B_FCAP].ensure(sizeof(long long) * n));
     CK(cudaMemcpyAsync(B[B_FOFF].p, foff.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(B[B_WIDTH].p, width.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(B[B_NXTOFF].p, nxt_off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(B[B_NXTCAP].p, nxt_cap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(B[B_NXTCNT].p, 0, sizeof(unsigned long long) * n, st));
-    if (!last) CK(nxt->ensure(sizeof(uint16_t) * std::max<long long>(1, NO) * T));
+    CK(cudaMemcpyAsync(B[B_FCAP].p, fcap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    CK(B[B_PWIDTH].ensure(sizeof(long long) * (S1 + 1)));
+    CK(B[B_PFLAG].ensure(sizeof(int) * S1));
+    CK(B[B_PPROBE].ensure(sizeof(int) * S1));
+    CK(B[B_PR].ensure(sizeof(double) * S1));
+    CK(B[B_PUSED].ensure(sizeof(int) * S1));
+    CK(B[B_PLATS].ensure(sizeof(double) * S1 * P));
+    CK(B[B_PACCS].ensure(sizeof(double) * S1 * P));
+    CK(B[B_PTOT].ensure(sizeof(unsigned long long) * n));
+    CK(B[B_PFX].ensure(sizeof(long long) * (S1 + 1)));
+    CK(cudaMemsetAsync(B[B_PTOT].p, 0, sizeof(unsigned long long) * n, st));
     if (diag) {
-      CK(B[B_FLAGS].ensure(sizeof(int) * std::max<long long>(1, F)));
-      CK(cudaMemsetAsync(B[B_FLAGS].p, 0, sizeof(int) * std::max<long long>(1, F), st));
+      CK(B[B_FLAGS].ensure(sizeof(int) * S1));
+      CK(cudaMemsetAsync(B[B_FLAGS].p, 0, sizeof(int) * S1, st));
     }
     a.level = L;
     a.last = last ? 1 : 0;
-    a.woff = B[B_WOFF].as<long long>();
+    a.n_slots = n_slots;
     a.foff = B[B_FOFF].as<long long>();
-    a.width = B[B_WIDTH].as<int>();
+    a.fcap = B[B_FCAP].as<long long>();
+    a.fcnt = ccnt->as<unsigned long long>();
     a.cur = cur->as<uint16_t>();
     a.cur_flag = B[B_FLAGS].as<int>();
-    a.nxt = last ? nullptr : nxt->as<uint16_t>();
-    a.nxt_cnt = B[B_NXTCNT].as<unsigned long long>();
-    a.nxt_off = B[B_NXTOFF].as<long long>();
-    a.nxt_cap = B[B_NXTCAP].as<long long>();
-    a.total_work = total;
-    if (last) {
-      std::vector<long long> boff(n + 1);
-      long long nb = 0;
-      const long long per_block = 256LL * a.ipt;
-      for (int i = 0; i < n; ++i) {
-        boff[i] = nb;
-        nb += (woff[i + 1] - woff[i] + per_block - 1) / per_block;
-      }
-      boff[n] = nb;
-      CK(B[B_BOFF].ensure(sizeof(long long) * (n + 1)));
-      CK(cudaMemcpyAsync(B[B_BOFF].p, boff.data(), sizeof(long long) * (n + 1),
-                         cudaMemcpyHostToDevice, st));
-      CK(B[B_PART].ensure(sizeof(LeafPart) * std::max<long long>(1, nb)));
-      a.boff = B[B_BOFF].as<long long>();
-      a.part = B[B_PART].as<LeafPart>();
-      c.stats.kernel_launches += launch_stage2_leaf(a, nb, st);
-    } else {
-      c.stats.kernel_launches += launch_stage2_level(a, st);
-    }
+    a.pr_width = B[B_PWIDTH].as<long long>();
+    a.pr_flag = B[B_PFLAG].as<int>();
+    a.pr_probe = B[B_PPROBE].as<int>();
+    a.pr_r = B[B_PR].as<double>();
+    a.pr_used = B[B_PUSED].as<int>();
+    a.pr_lat = B[B_PLATS].as<double>();
+    a.pr_acc = B[B_PACCS].as<double>();
+    a.ptot = B[B_PTOT].as<unsigned long long>();
+    a.pfx = B[B_PFX].as<long long>();
+    c.stats.kernel_launches += launch_stage2_prefix(a, st);
     CK(cudaGetLastError());
-    if (getenv("JSV_DEBUG")) {
-      std::vector<int> pp(std::max<long long>(1, F), 0);
-      for (int i = 0; i < n; ++i)
-        for (long long k = 0; k < fcount[i]; ++k) pp[foff[i] + k] = i;
-      CK(B[B_PPROBE].ensure(sizeof(int) * pp.size()));
-      CK(cudaMemcpy(B[B_PPROBE].p, pp.data(), sizeof(int) * pp.size(), cudaMemcpyHostToDevice));
-      launch_stage2_check(a, F, L, B[B_PPROBE].as<int>(), st);
-      CK(cudaStreamSynchronize(st));
-      fprintf(stderr, "[jsv] level %d F=%lld total_work=%lld diag=%d mode=%d\n", L, F, total,
-              (int)diag, a.mode);
+    // exclusive scan of the per-slot widths (width 0 beyond the live prefixes)
+    {
+      size_t tmp = 0;
+      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, a.pr_width, a.pfx, n_slots + 1, st));
+      CK(B[B_SCAN].ensure(tmp));
+      CK(cub::DeviceScan::ExclusiveSum(B[B_SCAN].p, tmp, a.pr_width, a.pfx, n_slots + 1, st));
     }
-    if (diag && F > 0) {
-      std::vector<int> pp(F);
-      for (int i = 0; i < n; ++i)
-        for (long long k = 0; k < fcount[i]; ++k) pp[foff[i] + k] = i;
-      CK(B[B_PPROBE].ensure(sizeof(int) * F));
-      CK(cudaMemcpyAsync(B[B_PPROBE].p, pp.data(), sizeof(int) * F, cudaMemcpyHostToDevice, st));
-      c.stats.kernel_launches += launch_stage2_blocked(a, F, B[B_PPROBE].as<int>(), st);
-      CK(cudaStreamSynchronize(st));  // pp is host-local
-    }
-    if (last) break;
-    std::vector<unsigned long long> cnt(n);
-    CK(cudaMemcpyAsync(cnt.data(), B[B_NXTCNT].p, sizeof(unsigned long long) * n,
-                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(ptot.data(), a.ptot, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
+                       st));
+    CK(cudaMemcpyAsync(fcnt.data(), a.fcnt, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
+                       st));
     CK(cudaStreamSynchronize(st));
-    // compact the next frontier in place: regions are [nxt_off, nxt_off + cnt)
-    F = 0;
+    long long total = 0;
     for (int i = 0; i < n; ++i) {
-      fcount[i] = (long long)cnt[i];
+      pstart[i] = total;
+      total += (long long)ptot[i];
+      nodes += (long long)fcnt[i];
+    }
+    if (last && !diag) c.stats.leaf_work += total;
+    if (total > 0) {
+      CK(B[B_PSTART].ensure(sizeof(long long) * n));
+      CK(cudaMemcpyAsync(B[B_PSTART].p, pstart.data(), sizeof(long long) * n,
+                         cudaMemcpyHostToDevice, st));
+      a.pstart = B[B_PSTART].as<long long>();
+      if (last) {
+        long long nb = 0;
+        const long long per_block = 256LL * a.ipt;
+        for (int i = 0; i < n; ++i) {
+          boff[i] = nb;
+          nb += ((long long)ptot[i] + per_block - 1) / per_block;
+        }
+        boff[n] = nb;
+        CK(B[B_BOFF].ensure(sizeof(long long) * (n + 1)));
+        CK(cudaMemcpyAsync(B[B_BOFF].p, boff.data(), sizeof(long long) * (n + 1),
+                           cudaMemcpyHostToDevice, st));
+        CK(B[B_PART].ensure(sizeof(LeafPart) * std::max<long long>(1, nb)));
+        a.boff = B[B_BOFF].as<long long>();
+        a.part = B[B_PART].as<LeafPart>();
+        c.stats.kernel_launches += launch_stage2_leaf(a, nb, st);
+      } else {
+        long long NO = 0;
+        for (int i = 0; i < n; ++i) {
+          nxt_off[i] = NO;
+          nxt_cap[i] = (long long)ptot[i];
+          NO += nxt_cap[i];
+        }
+        CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
+        CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
+        CK(ncnt->ensure(sizeof(unsigned long long) * n));
+        CK(cudaMemcpyAsync(B[B_NXTOFF].p, nxt_off.data(), sizeof(long long) * n,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(B[B_NXTCAP].p, nxt_cap.data(), sizeof(long long) * n,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemsetAsync(ncnt->p, 0, sizeof(unsigned long long) * n, st));
+        CK(nxt->ensure(sizeof(uint16_t) * std::max<long long>(1, NO) * T));
+        a.nxt = nxt->as<uint16_t>();
+        a.nxt_cnt = ncnt->as<unsigned long long>();
+        a.nxt_off = B[B_NXTOFF].as<long long>();
+        a.nxt_cap = B[B_NXTCAP].as<long long>();
+        c.stats.kernel_launches += launch_stage2_level(a, total, st);
+      }
+      CK(cudaGetLastError());
+    }
+    if (diag) c.stats.kernel_launches += launch_stage2_blocked(a, st);
+    if (last || total == 0) break;
+    // next frontier: slots [nxt_off, nxt_off + nxt_cap) per probe, live counts on the device
+    n_slots = 0;
+    for (int i = 0; i < n; ++i) {
       foff[i] = nxt_off[i];
-      F = std::max(F, nxt_off[i] + fcount[i]);
+      fcap[i] = nxt_cap[i];
+      n_slots = std::max(n_slots, nxt_off[i] + nxt_cap[i]);
     }
     std::swap(cur, nxt);
+    std::swap(ccnt, ncnt);
   }
   int err = 0;
   CK(cudaMemcpyAsync(&err, B[B_ERR].p, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -1146,9 +1179,7 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
       PointState& s = ps[i];
       if (s.phase == 1) {
         const size_t cnt = tree[i].size();
-        size_t k = 0;
-        bool stopped = false;
-        for (; k < cnt; ++k) {
+        for (size_t k = 0; k < cnt; ++k) {
           s.probes++;
           if (f[cursor + k]) {
             s.lo = s.hi;
@@ -1156,16 +1187,13 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
             if (s.hi > std::ldexp(1.0, 60)) {
               s.status = 2;
               s.phase = 3;
-              stopped = true;
               break;
             }
           } else {
             s.phase = 2;
-            stopped = true;
             break;
           }
         }
-        (void)stopped;
         cursor += cnt;
       } else if (s.phase == 2) {
         // walk the heap-ordered subtree

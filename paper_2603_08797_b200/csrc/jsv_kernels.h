@@ -6,7 +6,7 @@
 // Per-kernel CUDA-event timing on the launching stream (bench.py roofline).
 enum KernelId {
   K_GENERATE, K_STATS, K_PAIRS_A, K_COMPACT, K_PAIRS_B, K_TRUNCATE, K_MRANK, K_S2_PREP,
-  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_COUNT_
+  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_COUNT_
 };
 
 struct Prof {
@@ -83,6 +83,9 @@ struct S1Args {
   int* pool_min_sl;
   double* pool_acc_ub;
   int* err;
+  int S;          // slice budget
+  int* order;     // [Ctot] per-job candidate order by slices
+  int* bstart;    // [jobs * (S+2)] slice bucket starts
 };
 
 struct S1Launch {
@@ -112,6 +115,13 @@ struct S2Args {
   const double* p_fan;
   const uint16_t* rank_p;
   const uint16_t* rank_m;
+  // candidate items, for the m tie-break (planner.py:852)
+  const uint32_t* items;
+  const int* nitems;
+  const int* pool_cand;
+  long long C_probe;
+  long long task_base[MAXT + 1];
+  int maxi;
   const double* min_lat2;  // [jobs] (0 for could_zero tasks, set by stage2 prep)
   const int* min_sl;
   const double* acc_ub;
@@ -120,16 +130,27 @@ struct S2Args {
   int* active;             // [n_probes] 1 = search this probe
   // level expansion
   int level, last, diag, want_config;
-  const long long* woff;   // [n_probes+1] work offsets
-  const long long* foff;   // [n_probes] frontier base of the current level
-  const int* width;        // [n_probes] options per prefix
-  const uint16_t* cur;     // current frontier choices [*, T] (topo positions)
-  int* cur_flag;           // [*] bit0 = r > 0, bit1 = some child survived
+  long long n_slots;            // frontier slots of this level (all probes, with gaps)
+  const long long* foff;        // [n_probes] first slot of each probe
+  const long long* fcap;        // [n_probes] slot capacity of each probe
+  const unsigned long long* fcnt;  // [n_probes] live prefixes of each probe (device)
+  const uint16_t* cur;          // frontier choices [slot, T] (topo positions)
+  int* cur_flag;                // [slot] bit0 = r > 0, bit1 = some child survived (diag)
+  // per-slot prefix state (k_s2_prefix)
+  long long* pr_width;           // 64-bit so the work scan cannot overflow (> 2^31 items)
+  int* pr_flag;
+  int* pr_probe;
+  double* pr_r;
+  int* pr_used;
+  double* pr_lat;               // [slot * P] partial path latency before t
+  double* pr_acc;               // [slot * P] partial path accuracy product
+  unsigned long long* ptot;     // [n_probes] work items of each probe
+  long long* pfx;               // [n_slots + 1] exclusive scan of pr_width
+  const long long* pstart;      // [n_probes] first work item of each probe
   uint16_t* nxt;
   unsigned long long* nxt_cnt;  // [n_probes]
   const long long* nxt_off;     // [n_probes]
   const long long* nxt_cap;     // [n_probes]
-  long long total_work;
   int* err;
   // leaf level: blocks own (probe, chunk); per-block partial best, then a per-probe reduce
   int mode;                 // LEAF_FULL / LEAF_FIRST / LEAF_ANY
@@ -156,14 +177,13 @@ struct LeafPart {
 };
 
 int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st);
-int launch_stage2_check(const S2Args& a, long long n, int depth, const int* pp, cudaStream_t st);
 int launch_stage2_reduce(const S2Args& a, cudaStream_t st);
 
 int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
                        cudaStream_t st);
-int launch_stage2_level(const S2Args& a, cudaStream_t st);
-int launch_stage2_blocked(const S2Args& a, long long n_prefix_total, const int* prefix_probe,
-                          cudaStream_t st);
+int launch_stage2_prefix(const S2Args& a, cudaStream_t st);
+int launch_stage2_level(const S2Args& a, long long total, cudaStream_t st);
+int launch_stage2_blocked(const S2Args& a, cudaStream_t st);
 
 struct FinArgs {
   const DGraph* g;

@@ -1,12 +1,21 @@
-// jsv_search.cuh -- level-synchronous branch-and-bound expansion and the
-// lock-free leaf reduction (included by jsv_stage2.cu).
+// jsv_search.cuh -- level-synchronous branch-and-bound over the Stage-1 pools
+// (included by jsv_stage2.cu).
 //
-// A work item (prefix, b) applies the reference _visit filters
-// (planner.py:876-903) in order.  Intermediate levels append surviving
-// children to the next frontier; the last level derives + validates each
-// reached leaf (planner.py:835-855) and reduces it per thread, per block
-// (shared memory) and finally per probe (k_s2_reduce) -- no locks, so
-// thousands of concurrent feasible leaves never serialise.
+// Per level L (task t = topo[L]):
+//   k_s2_prefix  one thread per frontier slot: demand reaching t (_demand_at,
+//                planner.py:821-833), slices used, the partial path latency and
+//                accuracy products of the chosen prefix, and the number of pool
+//                bundles that can pass the resource filter (the pool is sorted by
+//                slices, so they form a prefix: "budget trimming").  In the
+//                diagnostic re-run nothing is trimmed so kill counts are exact.
+//   (scan)       exclusive scan of the per-slot widths -> work offsets.
+//   k_s2_level   intermediate level: one work item = (slot, bundle); applies the
+//                _visit filters (planner.py:876-903) in the reference order and
+//                appends survivors to the next frontier.
+//   k_s2_leaf    last level: same filters, then derive + validate of every
+//                reached leaf (planner.py:835-855) and a per-thread, per-block
+//                (shared memory) and per-probe (k_s2_reduce) lexicographic
+//                reduction -- lock free.
 
 #define ST_SKIP (-2)
 #define ST_PASS (-1)
@@ -22,27 +31,50 @@ __device__ __forceinline__ double bits_obj(unsigned long long b) {
   return __longlong_as_double((long long)b);
 }
 
-// Per-thread scratch of expand_item.  Declared once at kernel scope by the
-// callers: with the arrays local to the inlined callee, nvcc 12.9's stack
-// slot colouring overlapped the callee's acc[] with the caller's ch[].
-struct ExpScratch {
-  double r[MAXT];
-  double acc[MAXT];
-  uint16_t ch[MAXT];
-};
+__device__ __forceinline__ int find_probe(const long long* off, int n, long long x) {
+  int lo = 0, hi = n - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (off[mid] <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
-// Apply the node filters to child b of prefix pidx; fills xs.ch[0..L].
-__device__ __forceinline__ int expand_item(const S2Args& a, int probe, long long pidx, int b,
-                                           ExpScratch& xs, bool& rpos, bool check_bound) {
+// largest slot s in [lo, hi) with pfx[s] <= w
+__device__ __forceinline__ long long find_slot(const long long* pfx, long long lo, long long hi,
+                                               long long w) {
+  --hi;
+  while (lo < hi) {
+    const long long mid = (lo + hi + 1) >> 1;
+    if (pfx[mid] <= w) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+// ------------------------------------------------------------ prefix state
+
+__global__ void __launch_bounds__(256) k_s2_prefix(S2Args a) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= a.n_slots) return;
   const DGraph& g = *a.g;
   const DReq& rq = *a.rq;
-  const int T = a.T, L = a.level;
+  const int T = a.T, L = a.level, P = g.P;
   const int t = g.topo[L];
-  uint16_t* ch = xs.ch;
-  for (int k = 0; k < L; ++k) ch[k] = a.cur[pidx * T + k];
+  const int probe = find_probe(a.foff, a.n_probes, s);
+  const long long local = s - a.foff[probe];
+  if (local >= a.fcap[probe] || local >= (long long)a.fcnt[probe]) {
+    a.pr_width[s] = 0;
+    a.pr_flag[s] = 0;
+    return;
+  }
+  a.pr_probe[s] = probe;
+  uint16_t ch[MAXT];
+  for (int k = 0; k < L; ++k) ch[k] = a.cur[s * T + k];
   const DProbe& pr = a.probes[probe];
   const int jb = probe * T;
-  double* r = xs.r;
+  double r[MAXT];
   int used = 0;
   for (int k = 0; k <= L; ++k) {
     const int u = g.topo[k];
@@ -50,78 +82,133 @@ __device__ __forceinline__ int expand_item(const S2Args& a, int probe, long long
     if (u == g.entry) {
       ru = pr.demand;
     } else {
-      // _demand_at (planner.py:821-833)
       ru = 0.0;
       for (int qq = g.pred_off[u]; qq < g.pred_off[u + 1]; ++qq) {
         const int e = g.pred_edge[qq];
-        const int s = g.edge_src[e];
-        const int cs = ch[g.pos_of[s]];
-        if (cs == NONE16 || r[s] == 0.0) continue;
+        const int src = g.edge_src[e];
+        const int cs = ch[g.pos_of[src]];
+        if (cs == NONE16 || r[src] == 0.0) continue;  // empty bundles carry no demand
         const double fan = rq.has_ov[e] ? rq.ov[e]
-                                        : a.p_fan[((long long)(jb + s) * a.W + cs) * a.maxout +
-                                                  (e - g.succ_off[s])];
-        ru += r[s] * fan;
+                                        : a.p_fan[((long long)(jb + src) * a.W + cs) * a.maxout +
+                                                  (e - g.succ_off[src])];
+        ru += r[src] * fan;
       }
     }
     r[u] = ru;
     if (k < L && ch[k] != NONE16) used += a.p_sl[(long long)(jb + u) * a.W + ch[k]];
   }
   const double rt = r[t];
+  a.pr_r[s] = rt;
+  a.pr_used[s] = used;
+  int width, flag;
   if (rt == 0.0) {
-    rpos = false;
-    if (b != 0) return ST_SKIP;
-    ch[L] = NONE16;
-    return ST_PASS;
+    width = 1;  // the empty assignment is the only child (planner.py:868-875)
+    flag = 0;
+  } else {
+    flag = 1;
+    const int Pt = a.pool_n[jb + t];
+    if (a.diag) {
+      width = Pt;
+    } else {
+      // bundles passing `used + s + future > S + eps` form a prefix of the slices-sorted pool
+      const int* psl = a.p_sl + (long long)(jb + t) * a.W;
+      const int fut = a.future[probe * (T + 1) + L + 1];
+      const double lim = (double)rq.S + rq.eps;
+      int lo = 0, hi = Pt;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((double)(used + psl[mid] + fut) > lim) hi = mid;
+        else lo = mid + 1;
+      }
+      width = lo;
+    }
   }
-  rpos = true;
-  const int P = a.pool_n[jb + t];
-  if (b >= P) return ST_SKIP;
+  a.pr_width[s] = width;
+  a.pr_flag[s] = flag;
+  if (a.diag && flag) atomicOr(&a.cur_flag[s], 1);
+  if (flag) {
+    // partial path sums / products of the chosen prefix (path order, planner.py:805-819,
+    // model.py:267-282); tasks after t on a path are descendants, hence still open
+    for (int pp = 0; pp < P; ++pp) {
+      const bool through = (g.path_mask[pp] >> t) & 1u;
+      double lat = 0.0, prod = 1.0;
+      for (int k = g.path_off[pp]; k < g.path_off[pp + 1]; ++k) {
+        const int u = g.path_task[k];
+        if (through && u == t) break;
+        const int pu = g.pos_of[u];
+        if (pu < L) {
+          const int c = ch[pu];
+          if (c != NONE16) {
+            const long long q = (long long)(jb + u) * a.W + c;
+            lat += 2.0 * a.p_lat[q];
+            prod *= a.p_acc[q];
+          } else {
+            lat += 0.0;
+            prod *= 1.0;
+          }
+        } else {
+          prod *= a.acc_ub[jb + u];
+        }
+      }
+      a.pr_lat[s * P + pp] = lat;
+      a.pr_acc[s * P + pp] = prod;
+    }
+  }
+  atomicAdd(&a.ptot[probe], (unsigned long long)width);
+}
+
+// Filters of one (slot, bundle) item.  Returns ST_PASS (child survives; ub set),
+// a JSV_BIND_* kill reason, ST_BOUND (objective bound prune) or ST_SKIP.
+__device__ __forceinline__ int filter_item(const S2Args& a, int probe, long long s, int b,
+                                           bool check_bound, double& ub_out) {
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const int T = a.T, L = a.level, P = g.P;
+  const int t = g.topo[L];
+  if (!(a.pr_flag[s] & 1)) return b == 0 ? ST_PASS : ST_SKIP;
+  const int jb = probe * T;
+  const DProbe& pr = a.probes[probe];
   const long long q = (long long)(jb + t) * a.W + b;
-  const int* fut = a.future + probe * (T + 1);
-  const double need = rt * (1.0 + rq.slack);
   const double eps = rq.eps;
+  const int used = a.pr_used[s];
+  const int fut = a.future[probe * (T + 1) + L + 1];
   const int bsl = a.p_sl[q];
-  if (a.p_cap[q] + eps < need) return JSV_BIND_THROUGHPUT;
-  if ((double)(used + bsl + fut[L + 1]) > (double)rq.S + eps) return JSV_BIND_RESOURCES;
-  // partial-path latency (_latency_ok, planner.py:805-819)
+  if (a.p_cap[q] + eps < a.pr_r[s] * (1.0 + rq.slack)) return JSV_BIND_THROUGHPUT;
+  if ((double)(used + bsl + fut) > (double)rq.S + eps) return JSV_BIND_RESOURCES;
   const double lat2 = 2.0 * a.p_lat[q];
-  for (int pp = 0; pp < g.P; ++pp) {
+  const double accb = a.p_acc[q];
+  for (int pp = 0; pp < P; ++pp) {
     if (!((g.path_mask[pp] >> t) & 1u)) continue;
-    double tot = 0.0;
+    double x = a.pr_lat[s * P + pp] + lat2;
+    bool after = false;
     for (int k = g.path_off[pp]; k < g.path_off[pp + 1]; ++k) {
       const int u = g.path_task[k];
-      if (u == t) {
-        tot += lat2;
-      } else if (g.pos_of[u] < L) {
-        const int c = ch[g.pos_of[u]];
-        tot += (c == NONE16) ? 0.0 : 2.0 * a.p_lat[(long long)(jb + u) * a.W + c];
-      } else {
-        tot += a.min_lat2[jb + u];
+      if (after) x += a.min_lat2[jb + u];
+      if (u == t) after = true;
+    }
+    if (x > pr.slo_eff + eps) return JSV_BIND_LATENCY;
+  }
+  double total = 0.0;
+  for (int pp = 0; pp < P; ++pp) {
+    double A = a.pr_acc[s * P + pp];
+    if ((g.path_mask[pp] >> t) & 1u) {
+      A *= accb;
+      bool after = false;
+      for (int k = g.path_off[pp]; k < g.path_off[pp + 1]; ++k) {
+        const int u = g.path_task[k];
+        if (after) A *= a.acc_ub[jb + u];
+        if (u == t) after = true;
       }
     }
-    if (tot > pr.slo_eff + eps) return JSV_BIND_LATENCY;
+    total += g.path_frac[pp] * A;
   }
-  // accuracy upper bound (planner.py:889-894)
-  double* acc = xs.acc;
-  for (int u = 0; u < T; ++u) {
-    const int pu = g.pos_of[u];
-    if (pu < L) {
-      const int c = ch[pu];
-      acc[u] = (c == NONE16) ? 1.0 : a.p_acc[(long long)(jb + u) * a.W + c];
-    } else if (u == t) {
-      acc[u] = a.p_acc[q];
-    } else {
-      acc[u] = a.acc_ub[jb + u];
-    }
-  }
-  const double ub = weighted_paths(g, acc) / g.a_max;
+  const double ub = total / g.a_max;
   if (ub < pr.acc_slo - eps) return JSV_BIND_ACCURACY;
-  ch[L] = (uint16_t)b;
+  ub_out = ub;
   if (check_bound) {
-    // objective bound against the incumbent (planner.py:895-902)
     const unsigned long long ib = ((volatile unsigned long long*)a.inc)[probe];
     if (ib) {
-      const double obj_ub = pr.alpha * ub - pr.beta * (double)(used + bsl + fut[L + 1]);
+      const double obj_ub = pr.alpha * ub - pr.beta * (double)(used + bsl + fut);
       if (obj_ub < bits_obj(ib) - eps) return ST_BOUND;
     }
   }
@@ -130,29 +217,19 @@ __device__ __forceinline__ int expand_item(const S2Args& a, int probe, long long
 
 __global__ void __launch_bounds__(256) k_s2_level(S2Args a) {
   const int T = a.T, L = a.level;
+  const long long total = a.pfx[a.n_slots];
   const long long stride = (long long)gridDim.x * blockDim.x;
-  ExpScratch xs;
-  const uint16_t* ch = xs.ch;
-  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < a.total_work;
-       w += stride) {
-    int lo = 0, hi = a.n_probes - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (a.woff[mid] <= w) lo = mid;
-      else hi = mid - 1;
-    }
-    const int probe = lo;
-    const long long lw = w - a.woff[probe];
-    const int width = a.width[probe];
-    const long long pidx = a.foff[probe] + lw / width;
-    const int b = (int)(lw % width);
-    bool rpos = false;
-    const int st = expand_item(a, probe, pidx, b, xs, rpos, false);
+  for (long long w = blockIdx.x * (long long)blockDim.x + threadIdx.x; w < total; w += stride) {
+    const long long s = find_slot(a.pfx, 0, a.n_slots, w);
+    const int probe = a.pr_probe[s];
+    const int b = (int)(w - a.pfx[s]);
+    double ub = 0.0;
+    const int st = filter_item(a, probe, s, b, false, ub);
     if (st == ST_SKIP) continue;
+    const bool rpos = a.pr_flag[s] & 1;
     if (a.diag && rpos) {
-      if (b == 0) atomicOr(&a.cur_flag[pidx], 1);
       if (st >= 0 && st < 5) atomicAdd(&a.best[probe].kills[L][st], 1);
-      else atomicOr(&a.cur_flag[pidx], 2);
+      else atomicOr(&a.cur_flag[s], 2);
     }
     if (st != ST_PASS) continue;
     const unsigned long long pos = atomicAdd(&a.nxt_cnt[probe], 1ull);
@@ -161,7 +238,8 @@ __global__ void __launch_bounds__(256) k_s2_level(S2Args a) {
       continue;
     }
     uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
-    for (int k = 0; k <= L; ++k) dst[k] = ch[k];
+    for (int k = 0; k < L; ++k) dst[k] = a.cur[s * T + k];
+    dst[L] = rpos ? (uint16_t)b : (uint16_t)NONE16;
   }
 }
 
@@ -176,8 +254,8 @@ struct Cand {
 };
 
 __device__ __forceinline__ void code_choices(const S2Args& a, long long code, uint16_t* ch) {
-  const long long pidx = code >> 16;
-  for (int k = 0; k < a.level; ++k) ch[k] = a.cur[pidx * a.T + k];
+  const long long s = code >> 16;
+  for (int k = 0; k < a.level; ++k) ch[k] = a.cur[s * a.T + k];
   ch[a.level] = (uint16_t)(code & 0xFFFF);
 }
 
@@ -192,19 +270,52 @@ __device__ inline int cmp_leaf(const S2Args& a, long long c1, long long c2) {
   return 0;
 }
 
+// Cursor over the canonical m of one leaf: ((task, variant, segment, batch), count)
+// tuples in task-id order (planner.py:262), each encoded as task << 32 | key << 16 | count.
+struct MCursor {
+  const S2Args* a;
+  int probe;
+  const uint16_t* ch;  // choices by topo position
+  int u, k, n;
+  long long base;
+  __device__ void open_task() {
+    while (u < a->T) {
+      const int c = ch[a->g->pos_of[u]];
+      if (c != NONE16) {
+        const long long q = (long long)(probe * a->T + u) * a->W + c;
+        base = (long long)probe * a->C_probe + a->task_base[u] + a->pool_cand[q];
+        n = a->nitems[base];
+        if (n > 0) return;
+      }
+      ++u;
+    }
+  }
+  __device__ bool next(unsigned long long& e) {
+    if (u >= a->T) return false;
+    e = ((unsigned long long)u << 32) | a->items[base * a->maxi + k];
+    if (++k >= n) {
+      ++u;
+      k = 0;
+      open_task();
+    }
+    return true;
+  }
+};
+
+// m(leaf c1) vs m(leaf c2) as Python tuple comparison (planner.py:852)
 __device__ inline int cmp_tie(const S2Args& a, int probe, long long c1, long long c2) {
-  const DGraph& g = *a.g;
-  uint16_t x[MAXT], y[MAXT], cx[MAXT], cy[MAXT];
+  uint16_t x[MAXT], y[MAXT];
   code_choices(a, c1, x);
   code_choices(a, c2, y);
-  for (int u = 0; u < a.T; ++u) {
-    cx[u] = x[g.pos_of[u]];
-    cy[u] = y[g.pos_of[u]];
+  MCursor cx{&a, probe, x, 0, 0, 0, 0}, cy{&a, probe, y, 0, 0, 0, 0};
+  cx.open_task();
+  cy.open_task();
+  while (true) {
+    unsigned long long ex = 0, ey = 0;
+    const bool hx = cx.next(ex), hy = cy.next(ey);
+    if (!hx || !hy) return hx == hy ? 0 : (hx ? 1 : -1);  // a strict prefix is smaller
+    if (ex != ey) return ex < ey ? -1 : 1;
   }
-  unsigned long long kx[4], ky[4];
-  tie_key(a, probe, cx, kx);
-  tie_key(a, probe, cy, ky);
-  return cmp_words(kx, ky, 4);
 }
 
 // is A a better feasible candidate than B?
@@ -230,16 +341,6 @@ __device__ inline void merge(const S2Args& a, int probe, Cand& X, const Cand& Y)
   }
 }
 
-__device__ __forceinline__ int probe_of_block(const S2Args& a, long long blk) {
-  int lo = 0, hi = a.n_probes - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (a.boff[mid] <= blk) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
   __shared__ int sk[5];
   __shared__ Cand sc[256];
@@ -248,37 +349,39 @@ __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
   if (threadIdx.x == 0) s_leaves = 0;
   __syncthreads();
   const long long blk = blockIdx.x;
-  const int probe = probe_of_block(a, blk);
+  const int probe = find_probe(a.boff, a.n_probes, blk);
   const long long chunk = blk - a.boff[probe];
-  const long long work = a.woff[probe + 1] - a.woff[probe];
-  const int width = a.width[probe];
-  const long long per_block = (long long)blockDim.x * a.ipt;
-  const long long w0 = chunk * per_block;
+  const long long w_begin = a.pstart[probe];
+  const long long w_end = w_begin + (long long)a.ptot[probe];
+  const long long s_lo = a.foff[probe], s_hi = a.foff[probe] + a.fcap[probe];
+  const long long w0 = w_begin + chunk * (long long)blockDim.x * a.ipt;
   const DGraph& g = *a.g;
   const DReq& rq = *a.rq;
   const DProbe& pr = a.probes[probe];
   const bool check_bound = (a.mode == LEAF_FULL);
+  const int L = a.level;
   Cand best;
   best.has = 0; best.sl = 0; best.obj = 0.0; best.code = 0; best.has_leaf = 0; best.leaf = 0;
   unsigned long long leaves = 0;
-  volatile int* found = a.active;  // reused as the per-probe "found" flags
-  ExpScratch xs;
+  volatile int* found = a.active;  // per-probe "found" flags of feasible-only probes
+  uint16_t ch[MAXT];
   for (int k = 0; k < a.ipt; ++k) {
-    const long long lw = w0 + (long long)k * blockDim.x + threadIdx.x;
-    if (lw >= work) break;
+    const long long w = w0 + (long long)k * blockDim.x + threadIdx.x;
+    if (w >= w_end) break;
     if (a.mode == LEAF_ANY && found[probe]) break;
-    const long long pidx = a.foff[probe] + lw / width;
-    const int b = (int)(lw % width);
-    bool rpos = false;
-    const int st = expand_item(a, probe, pidx, b, xs, rpos, check_bound);
-    const uint16_t* ch = xs.ch;
+    const long long s = find_slot(a.pfx, s_lo, s_hi, w);
+    const int b = (int)(w - a.pfx[s]);
+    double ub = 0.0;
+    const int st = filter_item(a, probe, s, b, check_bound, ub);
     if (st == ST_SKIP) continue;
+    const bool rpos = a.pr_flag[s] & 1;
     if (a.diag && rpos) {
-      if (b == 0) atomicOr(&a.cur_flag[pidx], 1);
       if (st >= 0 && st < 5) atomicAdd(&sk[st], 1);
-      else atomicOr(&a.cur_flag[pidx], 2);
+      else atomicOr(&a.cur_flag[s], 2);
     }
     if (st != ST_PASS) continue;
+    for (int q = 0; q < L; ++q) ch[q] = a.cur[s * a.T + q];
+    ch[L] = rpos ? (uint16_t)b : (uint16_t)NONE16;
     // leaf: derive_configuration + validate_configuration from scratch
     double lat[MAXT], cap[MAXT], acc[MAXT], fan[MAXE];
     int sl[MAXT];
@@ -288,7 +391,7 @@ __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
     evaluate<false>(g, rq, pr, lat, cap, acc, sl, fan, present, ev, nullptr, nullptr, nullptr,
                     nullptr);
     ++leaves;
-    const long long code = (pidx << 16) | (long long)ch[a.level];
+    const long long code = (s << 16) | (long long)ch[L];
     if (a.diag && (!best.has_leaf || cmp_leaf(a, code, best.leaf) > 0)) {
       best.has_leaf = 1;
       best.leaf = code;
@@ -315,10 +418,10 @@ __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
   sc[threadIdx.x] = best;
   atomicAdd(&s_leaves, leaves);
   __syncthreads();
-  for (int s = 128; s > 0; s >>= 1) {
-    if (threadIdx.x < s) {
+  for (int st = 128; st > 0; st >>= 1) {
+    if (threadIdx.x < st) {
       Cand x = sc[threadIdx.x];
-      merge(a, probe, x, sc[threadIdx.x + s]);
+      merge(a, probe, x, sc[threadIdx.x + st]);
       sc[threadIdx.x] = x;
     }
     __syncthreads();
@@ -334,7 +437,7 @@ __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
     P.leaves = s_leaves;
   }
   if (a.diag && threadIdx.x < 5 && sk[threadIdx.x])
-    atomicAdd(&a.best[probe].kills[a.level][threadIdx.x], sk[threadIdx.x]);
+    atomicAdd(&a.best[probe].kills[L][threadIdx.x], sk[threadIdx.x]);
 }
 
 // per-probe fold of the leaf-block partials into BestRec
@@ -390,32 +493,12 @@ __global__ void __launch_bounds__(256) k_s2_reduce(S2Args a) {
   }
 }
 
-// debug: every frontier entry must hold valid pool indices
-__global__ void k_s2_check(S2Args a, long long n_prefix, int depth, const int* prefix_probe) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n_prefix) return;
-  const int probe = prefix_probe[i];
-  for (int k = 0; k < depth; ++k) {
-    const int c = a.cur[i * a.T + k];
-    const int t = a.g->topo[k];
-    if (c != NONE16 && c >= a.pool_n[probe * a.T + t])
-      printf("bad frontier entry %lld pos %d value %d (pool %d)\n", i, k, c,
-             a.pool_n[probe * a.T + t]);
-  }
-}
-
-int launch_stage2_check(const S2Args& a, long long n, int depth, const int* pp, cudaStream_t st) {
-  if (n <= 0) return 0;
-  k_s2_check<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, n, depth, pp);
-  return 1;
-}
-
 // deepest blocked level: a prefix with r > 0 whose children all died (planner.py:910-911)
-__global__ void k_s2_blocked(S2Args a, long long n_prefix, const int* prefix_probe) {
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (i >= n_prefix) return;
-  const int f = a.cur_flag[i];
-  if ((f & 1) && !(f & 2)) atomicMax(&a.best[prefix_probe[i]].deepest, a.level);
+__global__ void k_s2_blocked(S2Args a) {
+  const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (s >= a.n_slots) return;
+  const int f = a.cur_flag[s];
+  if ((f & 1) && !(f & 2)) atomicMax(&a.best[a.pr_probe[s]].deepest, a.level);
 }
 
 int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
@@ -428,9 +511,17 @@ int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* a
   return 1;
 }
 
-int launch_stage2_level(const S2Args& a, cudaStream_t st) {
-  if (a.total_work <= 0) return 0;
-  long long blocks = (a.total_work + 255) / 256;
+int launch_stage2_prefix(const S2Args& a, cudaStream_t st) {
+  if (a.n_slots <= 0) return 0;
+  PROF_BEGIN(K_S2_PREFIX);
+  k_s2_prefix<<<(unsigned)((a.n_slots + 255) / 256), 256, 0, st>>>(a);
+  PROF_END();
+  return 1;
+}
+
+int launch_stage2_level(const S2Args& a, long long total, cudaStream_t st) {
+  if (total <= 0) return 0;
+  long long blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   PROF_BEGIN(K_S2_LEVEL);
   k_s2_level<<<(unsigned)blocks, 256, 0, st>>>(a);
@@ -449,10 +540,8 @@ int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st) {
   return 2;
 }
 
-int launch_stage2_blocked(const S2Args& a, long long n_prefix_total, const int* prefix_probe,
-                          cudaStream_t st) {
-  if (n_prefix_total <= 0) return 0;
-  k_s2_blocked<<<(unsigned)((n_prefix_total + 255) / 256), 256, 0, st>>>(a, n_prefix_total,
-                                                                         prefix_probe);
+int launch_stage2_blocked(const S2Args& a, cudaStream_t st) {
+  if (a.n_slots <= 0) return 0;
+  k_s2_blocked<<<(unsigned)((a.n_slots + 255) / 256), 256, 0, st>>>(a);
   return 1;
 }

@@ -192,6 +192,47 @@ __global__ void k_stats(S1Args a) {
   a.flag[c] = 0u;
 }
 
+// Counting sort of a job's candidates by slice count: order[] and bucket starts
+// bstart[s] = #candidates with fewer than s slices (s = 0 .. S+1).
+#define BUCKET_SMEM_MAX 12288
+__global__ void __launch_bounds__(1024) k_bucket(S1Args a) {
+  extern __shared__ int hist[];
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int n = a.cnt[job];
+  const int NB = a.S + 2;
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  int* bst = a.bstart + (long long)job * NB;
+  if (NB > BUCKET_SMEM_MAX) {
+    // huge budgets: identity order, every candidate scanned
+    for (int s = threadIdx.x; s < NB; s += blockDim.x) bst[s] = (s == 0) ? 0 : n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) a.order[base + i] = i;
+    return;
+  }
+  for (int s = threadIdx.x; s < NB; s += blockDim.x) hist[s] = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    atomicAdd(&hist[(int)a.arr[base + i] + 1], 1);  // arr[0] = slices
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int acc = 0;
+    for (int s = 0; s < NB; ++s) {
+      acc += hist[s];
+      hist[s] = acc;
+      bst[s] = acc;
+    }
+  }
+  __syncthreads();
+  // hist[s] is now the start of bucket s; scatter (order inside a bucket is irrelevant)
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int s = (int)a.arr[base + i];
+    const int pos = atomicAdd(&hist[s], 1);
+    a.order[base + pos] = i;
+  }
+  (void)tot;
+}
+
 // items(c1) < items(c2) lexicographically over ((key, count), ...) tuples
 __device__ __forceinline__ int cmp_items(const S1Args& a, long long c1, long long c2) {
   const int n1 = a.nitems[c1], n2 = a.nitems[c2];
@@ -209,32 +250,47 @@ template <int D>
 __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
                                                  const int* tile_start, int tiles_pp, int jchunk) {
   __shared__ double sh[D * TJ];
+  __shared__ int shj[TJ];
+  __shared__ int s_end;
   const int probe = blockIdx.x / tiles_pp;
   const int tl = blockIdx.x % tiles_pp;
   const int t = tile_task[tl];
   const int i0 = tile_start[tl];
-  const int n = a.cnt[probe * a.T + t];
+  const int job = probe * a.T + t;
+  const int n = a.cnt[job];
   if (i0 >= n) return;
   const int j0 = blockIdx.y * jchunk;
   if (j0 >= n) return;
-  const int j1 = min(n, j0 + jchunk);
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long base = job_base(a, probe, t);
-  const int i = i0 + threadIdx.x;
-  const bool act = i < n;
+  const int* order = a.order + base;
+  const int* bst = a.bstart + (long long)job * (a.S + 2);
+  // i runs over the slices-sorted order so a block's candidates have similar slices
+  const bool act = i0 + (int)threadIdx.x < n;
+  const int i = act ? order[i0 + threadIdx.x] : 0;
   double xi[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) xi[d] = act ? a.arr[d * tot + base + i] : 0.0;
+  // only candidates with no more slices can dominate: scan order[0 .. end_i)
+  const int end_i = act ? bst[(int)xi[0] + 1] : 0;
+  if (threadIdx.x == 0) s_end = 0;
+  __syncthreads();
+  if (act) atomicMax(&s_end, end_i);
+  __syncthreads();
+  const int j1 = min(min(n, j0 + jchunk), s_end);
   unsigned fl = 0;
   for (int jt = j0; jt < j1; jt += TJ) {
     const int nj = min(TJ, j1 - jt);
+    for (int x = threadIdx.x; x < TJ; x += blockDim.x) shj[x] = x < nj ? order[jt + x] : 0;
+    __syncthreads();
     for (int x = threadIdx.x; x < D * TJ; x += blockDim.x) {
       int d = x / TJ, jj = x % TJ;
-      sh[x] = jj < nj ? a.arr[d * tot + base + jt + jj] : 0.0;
+      sh[x] = jj < nj ? a.arr[d * tot + base + shj[jj]] : 0.0;
     }
     __syncthreads();
     if (act && !fl) {
-      for (int jj = 0; jj < nj; ++jj) {
+      const int lim = min(nj, end_i - jt);
+      for (int jj = 0; jj < lim; ++jj) {
         bool le = true, eq = true;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
@@ -247,7 +303,7 @@ __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
             fl |= 1u;
             break;
           }
-          const int j = jt + jj;
+          const int j = shj[jj];
           if (j != i) {
             int c = cmp_items(a, base + j, base + i);
             if (c < 0 || (c == 0 && j < i)) {
@@ -523,6 +579,14 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     PROF_END();
     ++launches;
   }
+  {
+    const int NB = a.S + 2;
+    const size_t smem = NB <= BUCKET_SMEM_MAX ? sizeof(int) * NB : 0;
+    PROF_BEGIN(K_BUCKET);
+    k_bucket<<<a.n_probes * a.T, 1024, smem, st>>>(a);
+    PROF_END();
+    ++launches;
+  }
   if (L.tiles_pp > 0) {
     dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
     PROF_BEGIN(K_PAIRS_A);
@@ -545,10 +609,6 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   k_truncate<<<a.n_probes * a.T, 1024, 0, st>>>(a);
   PROF_END();
   ++launches;
-  dim3 gm((unsigned)(a.n_probes * a.T), (unsigned)((2 * (a.W + 1) + 255) / 256));
-  PROF_BEGIN(K_MRANK);
-  k_mrank<<<gm, 256, 0, st>>>(a);
-  PROF_END();
-  ++launches;
+  // (m ties are resolved directly on the item lists in Stage 2; no rank pass needed)
   return launches;
 }
