@@ -177,6 +177,9 @@ typedef struct {
   int64_t pair_tests_a;                 /* sum over jobs of n^2 (Stage-1 skyline pairs) */
   int64_t pair_tests_b;                 /* sum over jobs of F^2 (frontier ranking pairs) */
   int64_t leaf_work;                    /* (prefix, bundle) items at the last level */
+  int64_t exh_candidates;               /* mixed-radix candidates swept by the exhaustive kernel */
+  int32_t exh_probes;                   /* probes solved by the exhaustive kernel */
+  int32_t exh_pad_;
 } jsv_stats;
 
 const char* jsv_last_error(void);
@@ -222,6 +225,32 @@ int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const jsv_request* 
 
 int jsv_last_stats(jsv_context* ctx, jsv_stats* out);
 
+/*
+ * Stage-2 strategy of a context (no reference counterpart: the reference has
+ * one CPU branch-and-bound, planner.py:731-912; every strategy returns its
+ * exact result).
+ *   JSV_STRATEGY_SEARCH      level-synchronous branch-and-bound (reference filters)
+ *   JSV_STRATEGY_EXHAUSTIVE  mixed-radix sweep of the whole Stage-1 cross-product
+ *                            (every candidate derived + validated) for probes whose
+ *                            cross-product is <= max_candidates; search otherwise
+ *   JSV_STRATEGY_AUTO        exhaustive when the cross-product is <= max_candidates
+ *                            (default 2^22), search otherwise
+ */
+#define JSV_STRATEGY_SEARCH 0
+#define JSV_STRATEGY_EXHAUSTIVE 1
+#define JSV_STRATEGY_AUTO 2
+int jsv_set_strategy(jsv_context* ctx, int strategy, int64_t max_candidates);
+
+/*
+ * Shard the exhaustive sweep of every probe across `world` GPUs: this context
+ * evaluates prefix range [Q*rank/world, Q*(rank+1)/world) of each probe's
+ * candidate space and returns its local argmax (jsv_plan_out of the local best,
+ * or the replicated infeasibility diagnosis).  Ranks combine the outputs with
+ * one all-gather (paper_2603_08797_b200/shard.py).  Search-strategy probes are
+ * replicated on every rank.
+ */
+int jsv_set_shard(jsv_context* ctx, int rank, int world);
+
 /* Per-kernel CUDA-event timing on the library stream (bench roofline).
  * jsv_profile(on) resets the accumulators; jsv_kernel_times fills ms[k] /
  * count[k] for kernel ids 0..n-1 (see JSV_KERNEL_NAMES) and returns the id count. */
@@ -229,7 +258,8 @@ int jsv_profile(jsv_context* ctx, int on);
 int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
 #define JSV_KERNEL_NAMES \
   "generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank", "s2_prep", \
-  "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket", "s2_prefix"
+  "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket", "s2_prefix", "s2_exh", \
+  "s2_xreduce", "s2_xsort"
 
 #ifdef __cplusplus
 }

@@ -83,7 +83,8 @@ class Stats(C.Structure):
     _fields_ = [("ms_stage1", C.c_float), ("ms_stage2", C.c_float), ("ms_total", C.c_float),
                 ("candidates_generated", C.c_int64), ("leaves", C.c_int64), ("nodes", C.c_int64),
                 ("kernel_launches", C.c_int32), ("dims", C.c_int32), ("pair_tests_a", C.c_int64),
-                ("pair_tests_b", C.c_int64), ("leaf_work", C.c_int64)]
+                ("pair_tests_b", C.c_int64), ("leaf_work", C.c_int64),
+                ("exh_candidates", C.c_int64), ("exh_probes", C.c_int32), ("exh_pad_", C.c_int32)]
 
 
 EXPORTS = {
@@ -108,13 +109,30 @@ EXPORTS = {
                                 C.c_int32, C.c_int32, _I32P, _I32P, _U32P, _F64P, _I32P]),
     "jsv_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
     "jsv_profile": (C.c_int, [C.c_void_p, C.c_int]),
+    "jsv_set_strategy": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
+    "jsv_set_shard": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "jsv_kernel_times": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double),
                                    C.POINTER(C.c_int64)]),
 }
 
 KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",
                 "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket",
-                "s2_prefix")
+                "s2_prefix", "s2_exh", "s2_xreduce", "s2_xsort")
+
+STRATEGY_SEARCH, STRATEGY_EXHAUSTIVE, STRATEGY_AUTO = 0, 1, 2
+STRATEGIES = {"search": STRATEGY_SEARCH, "exhaustive": STRATEGY_EXHAUSTIVE, "auto": STRATEGY_AUTO}
+
+
+def set_strategy(ctx, strategy: str, max_candidates: int = 1 << 22) -> None:
+    """Stage-2 strategy of a context (include/jsv.h jsv_set_strategy)."""
+    if strategy not in STRATEGIES:
+        raise ValueError(f"unknown strategy {strategy!r}; expected one of {sorted(STRATEGIES)}")
+    check(load_library().jsv_set_strategy(ctx, STRATEGIES[strategy], int(max_candidates)))
+
+
+def set_shard(ctx, rank: int, world: int) -> None:
+    """Evaluate only shard `rank` of `world` of every exhaustive sweep (jsv_set_shard)."""
+    check(load_library().jsv_set_shard(ctx, int(rank), int(world)))
 
 
 def profile(ctx, on: bool) -> None:

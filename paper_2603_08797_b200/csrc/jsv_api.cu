@@ -60,7 +60,8 @@ enum BufId {
   B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
-  B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_COUNT
+  B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
+  B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_COUNT
 };
 
 struct jsv_context {
@@ -72,6 +73,9 @@ struct jsv_context {
   Prof prof;
   double kms[K_COUNT_] = {};
   long long kcnt[K_COUNT_] = {};
+  int strategy = JSV_STRATEGY_SEARCH;
+  long long exh_limit = 1LL << 22;
+  int shard_rank = 0, shard_world = 1;
 };
 
 thread_local Prof* g_prof = nullptr;
@@ -140,6 +144,11 @@ struct jsv_problem {
   std::vector<double> key_lat, key_thr;
   std::vector<int> sub_off, sub_key, grp_off, grp_rep;
   double a_max = 0.0;
+  // every profile latency is +0 or positive and finite, and no path sum can
+  // overflow: the exhaustive kernel's Neumaier step may then use max/min for the
+  // |f| >= |x| ordering and skip the non-finite-compensation test (exact)
+  // (capacities finite too: fl(a - b) >= 0 <=> a >= b for the verdicts)
+  bool lat_fast = false;
   DGraph hg{};
   DevBuf dgraph, d_var_acc, d_var_fac_off, d_var_fac, d_key_var, d_key_cost, d_key_lat, d_key_thr,
       d_sub_off, d_sub_key, d_grp_off, d_grp_rep;
@@ -230,6 +239,19 @@ extern "C" int jsv_problem_create(jsv_context* ctx, const jsv_problem_desc* d, j
   p.key_cost.assign(d->key_cost, d->key_cost + K);
   p.key_lat.assign(d->key_lat, d->key_lat + K);
   p.key_thr.assign(d->key_thr, d->key_thr + K);
+  {
+    double mx = 0.0;
+    bool ok = true;
+    for (double v : p.key_lat) {
+      if (!(v >= 0.0) || std::signbit(v) || !std::isfinite(v)) ok = false;
+      else mx = std::max(mx, v);
+    }
+    for (double v : p.key_thr) ok = ok && std::isfinite(v) && v < 1e290;
+    // accuracy threshold monotonicity: accuracies and path fractions >= +0
+    for (double v : p.var_acc) ok = ok && v >= 0.0 && !std::signbit(v) && std::isfinite(v);
+    for (double v : p.path_frac) ok = ok && v >= 0.0 && !std::signbit(v) && std::isfinite(v);
+    p.lat_fast = ok && mx * 2.0 * (double)(T + 1) < 1e300;
+  }
   p.sub_off.assign(d->sub_off, d->sub_off + 4 * T + 1);
   p.sub_key.assign(d->sub_key, d->sub_key + p.sub_off[4 * T]);
   p.grp_off.assign(d->grp_off, d->grp_off + 4 * T + 1);
@@ -360,6 +382,45 @@ static double host_pysum(const double* x, int n) {
   return f;
 }
 
+// order-preserving keys of doubles (NaN excluded)
+static inline unsigned long long h_key(double x) {
+  unsigned long long b;
+  memcpy(&b, &x, 8);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+static inline double h_unkey(unsigned long long k) {
+  unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFull) : ~k;
+  double x;
+  memcpy(&x, &b, 8);
+  return x;
+}
+static inline bool h_acc_pass(double w, double a_max, double s) {
+  const double a = w / a_max;  // a_obj (model.py:293)
+  return a - s >= 0;           // accuracy verdict (planner.py:350-351)
+}
+
+// Smallest double W with h_acc_pass(W); ok = 0 when no exact threshold exists.
+static void acc_threshold(double a_max, double s, double& thr, int& ok) {
+  ok = 0;
+  thr = 0.0;
+  if (!(a_max > 0) || !std::isfinite(a_max) || !std::isfinite(s)) return;
+  const double ninf = -INFINITY, pinf = INFINITY;
+  if (h_acc_pass(ninf, a_max, s)) {
+    thr = ninf;
+    ok = 1;
+    return;
+  }
+  if (!h_acc_pass(pinf, a_max, s)) return;
+  unsigned long long lo = h_key(ninf), hi = h_key(pinf);  // lo fails, hi passes
+  while (hi - lo > 1) {
+    const unsigned long long mid = lo + (hi - lo) / 2;
+    if (h_acc_pass(h_unkey(mid), a_max, s)) hi = mid;
+    else lo = mid;
+  }
+  thr = h_unkey(hi);
+  ok = 1;
+}
+
 static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_probe& in,
                        DProbe& o) {
   memset(&o, 0, sizeof(o));
@@ -368,6 +429,7 @@ static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_pr
   o.acc_slo = in.acc_slo;
   o.alpha = in.alpha;
   o.beta = in.beta;
+  acc_threshold(p.a_max, in.acc_slo, o.acc_thr, o.acc_thr_ok);
   double fac[MAXE], r[MAXT];
   for (int a = 0; a < 2; ++a) {
     host_factors(p, rq, a == 1, true, fac);
@@ -962,6 +1024,129 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
   return JSV_OK;
 }
 
+// Exhaustive Stage 2 (jsv_exhaustive.cuh) for the probes whose Stage-1
+// cross-product is at most the context limit; clears active[i] for them.
+static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
+                          std::vector<int>& active) {
+  jsv_context& c = *p.ctx;
+  if (c.strategy == JSV_STRATEGY_SEARCH) return JSV_OK;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  const int n = bs.n, T = p.T;
+  const int W = bs.s1.W;
+  const size_t smem_cap = 200 * 1024;
+  std::vector<XProbe> xp(n);
+  std::vector<long long> boff(n + 1, 0);
+  long long nb = 0, cand = 0;
+  int max_pn_last = 1, nx = 0;
+  for (int i = 0; i < n; ++i) {
+    boff[i] = nb;
+    if (!active[i] || bs.dead[i]) continue;
+    XProbe& x = xp[i];
+    memset(&x, 0, sizeof(x));
+    unsigned __int128 N = 1;
+    bool over = false;
+    for (int k = 0; k < T; ++k) {
+      const int t = p.topo[k];
+      x.pn[k] = bs.pool_n[(size_t)i * T + t];
+      x.radix[k] = x.pn[k] + (int)((bs.probes[i].could_zero >> t) & 1u);
+      if (!over) N *= (unsigned)x.radix[k];
+      if (N > (unsigned __int128)c.exh_limit) over = true;  // keep filling pn/radix
+    }
+    if (over || N == 0) continue;
+    if (x_smem_bytes(x.pn[T - 1], p.P, p.lat_fast) > smem_cap) continue;
+    x.R = x.radix[T - 1];
+    const long long Q = (long long)(N / (unsigned)x.R);
+    x.q0 = (long long)((__int128)Q * c.shard_rank / c.shard_world);
+    const long long q1 = (long long)((__int128)Q * (c.shard_rank + 1) / c.shard_world);
+    x.nq = q1 - x.q0;
+    int glog = 0;
+    while ((1 << glog) < x.R && glog < 5) ++glog;
+    x.glog = glog;
+    // ~32k candidates per block so the TMA staging of the sink pool is amortised
+    // ~1M candidates per block amortise the sink-pool staging and the block prologue
+    x.rounds = (int)std::max<long long>(1, (1LL << 20) / ((long long)(XBLOCK / 32) * x_slots(p.P) * x.R));
+    cand += x.nq * x.R;
+    max_pn_last = std::max(max_pn_last, x.pn[T - 1]);
+    active[i] = 0;
+    ++nx;
+  }
+  if (nx == 0) return JSV_OK;
+  // keep >= 4 blocks per SM when the batch is small
+  for (int it = 0; it < 16; ++it) {
+    nb = 0;
+    bool can = false;
+    for (int i = 0; i < n; ++i) {
+      boff[i] = nb;
+      if (xp[i].rounds == 0) continue;
+      const long long per_block = (long long)(XBLOCK / 32) * x_slots(p.P) * xp[i].rounds;
+      nb += (xp[i].nq + per_block - 1) / per_block;
+      can = can || xp[i].rounds > 1;
+    }
+    boff[n] = nb;
+    if (nb >= 148 * 4 || !can) break;
+    for (int i = 0; i < n; ++i)
+      if (xp[i].rounds > 1) xp[i].rounds = (xp[i].rounds + 1) / 2;
+  }
+  c.stats.exh_candidates += cand;
+  c.stats.exh_probes += nx;
+  CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
+  CK(B[B_XBOFF].ensure(sizeof(long long) * (n + 1)));
+  CK(B[B_XPART].ensure(sizeof(XPart) * std::max<long long>(1, nb)));
+  CK(cudaMemcpyAsync(B[B_XPROBE].p, xp.data(), sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_XBOFF].p, boff.data(), sizeof(long long) * (n + 1),
+                     cudaMemcpyHostToDevice, st));
+  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
+  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
+  XArgs a;
+  memset(&a, 0, sizeof(a));
+  s2_base(p, bs, a.s);
+  a.s.active = B[B_ACTIVE].as<int>();
+  const bool fonly = bs.feasible_only != 0;
+  a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
+  a.xp = B[B_XPROBE].as<XProbe>();
+  a.boff = B[B_XBOFF].as<long long>();
+  a.part = B[B_XPART].as<XPart>();
+  a.tma = (W % 4 == 0) ? 1 : 0;
+  a.fast = p.lat_fast ? 1 : 0;
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(bs.probes[i].slo_eff) || !std::isfinite(bs.probes[i].demand)) a.fast = 0;
+  {
+    const int tl = p.topo[T - 1];
+    double mx = 0.0;
+    for (int k = p.key_off[tl]; k < p.key_off[tl + 1]; ++k) mx = std::max(mx, p.key_lat[k]);
+    a.lat2_max = 2.0 * mx;
+  }
+  a.max_pn_last = max_pn_last;
+  // register records need whole-warp prefix groups (every sink pool >= 32) and <= 512 bundles
+  a.rpl = 0;
+  if (p.P <= 4 && max_pn_last <= 512 && bs.s1.S < 0x7FFF) {
+    bool all32 = true;
+    for (int i = 0; i < n; ++i)
+      if (xp[i].rounds > 0 && xp[i].glog < 5) all32 = false;
+    if (all32) a.rpl = ((max_pn_last + 127) / 128) * 4;
+  }
+  if (getenv("JSV_NO_RPL")) a.rpl = 0;
+  if (a.fast) {
+    CK(B[B_XSACC].ensure(sizeof(double) * (size_t)n * W));
+    CK(B[B_XSCAP].ensure(sizeof(double) * (size_t)n * W));
+    CK(B[B_XSLAT].ensure(sizeof(double) * (size_t)n * W));
+    CK(B[B_XRANK].ensure(sizeof(uint4) * (size_t)n * W));
+    CK(B[B_XPACK].ensure(sizeof(uint2) * (size_t)n * W));
+    a.xpack = B[B_XPACK].as<uint2>();
+    a.sacc = B[B_XSACC].as<double>();
+    a.scap = B[B_XSCAP].as<double>();
+    a.slat2 = B[B_XSLAT].as<double>();
+    a.xrank = B[B_XRANK].as<uint4>();
+  }
+  if (getenv("JSV_NO_FAST")) a.fast = 0;
+  if (getenv("JSV_NO_TMA")) a.tma = 0;
+  c.stats.kernel_launches +=
+      launch_stage2_exhaustive(a, nb, p.P, x_smem_bytes(max_pn_last, p.P, a.fast != 0), st);
+  CK(cudaGetLastError());
+  return JSV_OK;
+}
+
 // plan() for a batch of probes sharing one request
 static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, const jsv_probe* in,
                                jsv_plan_out* out, bool want_config) {
@@ -983,9 +1168,15 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     rc = stage2_prep(p, bs);
     if (rc) return rc;
     std::vector<int> active(n, 1);
-    long long nn = 0;
-    rc = run_stage2(p, bs, false, want_config, active, &nn);
+    rc = run_exhaustive(p, bs, want_config, active);
     if (rc) return rc;
+    long long nn = 0;
+    bool any_search = false;
+    for (int i = 0; i < n; ++i) any_search = any_search || (active[i] && !bs.dead[i]);
+    if (any_search) {
+      rc = run_stage2(p, bs, false, want_config, active, &nn);
+      if (rc) return rc;
+    }
     c.stats.nodes += nn;
     // infeasible full plans: diagnostic re-run for the binding constraint
     std::vector<BestRec> best(n);
@@ -1047,6 +1238,24 @@ extern "C" int jsv_plan_batch(jsv_context* ctx, const jsv_problem* prob, const j
   memset(&ctx->stats, 0, sizeof(ctx->stats));
   ProfScope ps(ctx);
   return plan_batch_internal(*const_cast<jsv_problem*>(prob), *req, n, probes, out, true);
+}
+
+extern "C" int jsv_set_strategy(jsv_context* ctx, int strategy, int64_t max_candidates) {
+  if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  if (strategy < JSV_STRATEGY_SEARCH || strategy > JSV_STRATEGY_AUTO)
+    return fail(JSV_ERR_ARG, "unknown strategy");
+  if (max_candidates < 1) return fail(JSV_ERR_ARG, "max_candidates must be positive");
+  ctx->strategy = strategy;
+  ctx->exh_limit = max_candidates;
+  return JSV_OK;
+}
+
+extern "C" int jsv_set_shard(jsv_context* ctx, int rank, int world) {
+  if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(JSV_ERR_ARG, "bad shard rank/world");
+  ctx->shard_rank = rank;
+  ctx->shard_world = world;
+  return JSV_OK;
 }
 
 extern "C" int jsv_last_stats(jsv_context* ctx, jsv_stats* out) {

@@ -78,6 +78,13 @@ struct DProbe {
   int best_slices[MAXT], min_cost[MAXT];
   double star[MAXT];         // demand_star (planner.py:1014-1015)
   double slice_budget[MAXT]; // planner.py:1017-1037
+  // accuracy verdict as a threshold on the path-weighted sum W: the reference
+  // tests fl(fl(W / a_max) - acc_slo) >= 0 (model.py:293, planner.py:350-351);
+  // fl(W / a_max) is monotone in W, so the verdict holds iff W >= acc_thr
+  // (host binary search over the doubles with the same IEEE division)
+  double acc_thr;
+  int acc_thr_ok;            // 0: a_max/acc_slo not finite-positive, divide per candidate
+  int pad_;
 };
 
 // Stage-1 generation descriptor: one per (task, enabled sub-space).

@@ -6,7 +6,7 @@
 // Per-kernel CUDA-event timing on the launching stream (bench.py roofline).
 enum KernelId {
   K_GENERATE, K_STATS, K_PAIRS_A, K_COMPACT, K_PAIRS_B, K_TRUNCATE, K_MRANK, K_S2_PREP,
-  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_COUNT_
+  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_S2_EXH, K_S2_XREDUCE, K_S2_XSORT, K_COUNT_
 };
 
 struct Prof {
@@ -175,6 +175,55 @@ struct LeafPart {
   long long leaf; // max reached leaf code
   unsigned long long leaves;
 };
+
+// exhaustive Stage 2 (jsv_exhaustive.cuh)
+#define XBLOCK 256
+
+struct XPart {
+  int has, sl;
+  double obj;
+  long long idx;
+  unsigned long long leaves;
+};
+
+// per-probe decomposition (host-computed after Stage 1)
+struct XProbe {
+  int radix[MAXT];      // digit radix by topo position (pool_n + could_zero)
+  int pn[MAXT];         // pool size by topo position ("no instances" digit value)
+  long long q0, nq;     // prefix range of this shard
+  int glog;             // lanes per prefix group = 1 << glog
+  int R;                // radix of the last position
+  int rounds;           // prefix rounds per block (amortises the sink-pool staging)
+                        // (a round = 8 warps x x_slots(P) prefixes)
+  int pad_;
+};
+
+struct XArgs {
+  S2Args s;
+  const XProbe* xp;
+  const long long* boff;  // [n_probes + 1] blocks of each probe
+  XPart* part;            // [blocks]
+  int mode;               // LEAF_FULL / LEAF_FIRST / LEAF_ANY
+  int tma;                // stage the sink pool with cp.async.bulk (alignment holds)
+  int fast;               // jsv_problem::lat_fast (non-negative bounded latencies)
+  double lat2_max;        // 2 x the largest profile latency of the sink task
+  // rank space (fast != 0), per probe [n_probes * W]: records and sorted columns
+  uint4* xrank;           // {rank(capacity), rank(accuracy), rank(2 L), slices} per bundle
+  uint2* xpack;           // the same as two SWAR words of 15-bit fields (rpl > 0)
+  double* scap;           // sink-pool capacities sorted ascending
+  double* sacc;           // sink-pool accuracies sorted ascending
+  double* slat2;          // sink-pool 2 L sorted ascending
+  int max_pn_last;        // largest sink pool of the batch
+  int rpl;                // rank space: sink records per lane kept in registers (0 = loop)
+};
+
+// prefix-state slots per warp of the exhaustive kernel for a graph with P paths
+__host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <= 16 ? 8 : 2); }
+// sink-pool records padded to a whole number of 4 x 32-lane sweeps
+__host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) & ~127; }
+size_t x_smem_bytes(int max_pn_last, int P, bool rank);
+int launch_stage2_exhaustive(const XArgs& a, long long n_blocks, int P, size_t smem,
+                             cudaStream_t st);
 
 int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st);
 int launch_stage2_reduce(const S2Args& a, cudaStream_t st);

@@ -62,6 +62,7 @@ __all__ = [
     "OracleCaps",
     "plan_result_to_dict",
     "last_stats",
+    "set_strategy",
 ]
 
 # ------------------------------------------------------------ problem cache
@@ -82,6 +83,18 @@ def _problem(app, profile, device=None) -> LW.Lowered:
     while len(_CACHE) > _CACHE_MAX:
         _CACHE.popitem(last=False)
     return lw
+
+
+def set_strategy(strategy: str, max_candidates: int = 1 << 22, device=None) -> None:
+    """Choose the Stage-2 strategy of this process's planner context.
+
+    "search" (level-synchronous branch-and-bound with the reference's filters),
+    "exhaustive" (every allocation of the Stage-1 cross-product derived and
+    validated, for solves with at most `max_candidates` allocations) or "auto".
+    All strategies return the reference's exact result; this is a performance
+    knob with no reference counterpart.
+    """
+    N.set_strategy(N.context(device), strategy, max_candidates)
 
 
 def last_stats(device=None) -> dict:

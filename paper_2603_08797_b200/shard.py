@@ -92,3 +92,59 @@ def sharded_map(items: Sequence, solve: Callable[[Sequence], list], group=None) 
     for start, res in parts:
         out[start:start + len(res)] = res
     return out
+
+
+# ------------------------------------------------- one solve split across GPUs
+
+def _result_better(a, b) -> bool:
+    """Reference tie-break between feasible plans (planner.py:850-854):
+    objective desc, total slices asc, then the canonical m tuple asc."""
+    if a.objective != b.objective:
+        return a.objective > b.objective
+    if a.config.total_slices != b.config.total_slices:
+        return a.config.total_slices < b.config.total_slices
+    return a.config.m < b.config.m
+
+
+def pick_sharded(results: Sequence):
+    """Combine the per-shard PlanResults of one solve.
+
+    Each shard evaluated a disjoint block of the mixed-radix candidate space
+    (jsv_set_shard) and returned its local argmax; the global argmax is the
+    best feasible local result.  When no shard is feasible every rank ran the
+    same replicated infeasibility diagnosis, so any result (rank 0's) is the
+    answer.
+    """
+    win = None
+    for r in results:
+        if r.feasible and (win is None or _result_better(r, win)):
+            win = r
+    return win if win is not None else results[0]
+
+
+def plan_sharded(app, profile, request, options=None, group=None, device=None):
+    """plan() with the exhaustive Stage-2 sweep split across the ranks of ``group``.
+
+    Stage 1 is replicated (deterministic, microseconds); each rank sweeps prefix
+    block [Q*r/W, Q*(r+1)/W) of the candidate space and the local results are
+    exchanged with one all-gather, then reduced with the reference tie-break on
+    every rank -- the answer does not depend on the rank count.
+    """
+    import torch.distributed as dist
+
+    from . import _native as N
+    from . import planner
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    ctx = N.context(device)
+    N.set_shard(ctx, rank, world)
+    try:
+        local = planner.plan_batch(app, profile, [request], options, device=device)[0]
+    finally:
+        N.set_shard(ctx, 0, 1)
+    if world == 1:
+        return local
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    return pick_sharded(parts)

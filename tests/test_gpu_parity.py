@@ -4,6 +4,11 @@ Bit-exact: chosen allocations (m), feasibility, binding constraint, pool
 sizes / truncation, max-serviceable demand and probe counts; every float in
 the serialised result is compared with == (the north-star tolerance of 1e-9
 relative is not needed because the kernels reproduce CPython's float order).
+
+Every case runs under both Stage-2 strategies: the level-synchronous
+branch-and-bound ("search") and the mixed-radix sweep of the whole Stage-1
+cross-product ("exhaustive", for solves of at most 2^32 allocations; larger
+ones fall back to the search inside the library).
 """
 
 from __future__ import annotations
@@ -14,12 +19,16 @@ from golden_io import all_plan_cases, case_inputs, load, profile_of, result_dict
 
 pytestmark = pytest.mark.gpu
 
+EXH_LIMIT = 1 << 32
 
-@pytest.fixture(scope="module")
-def P():
+
+@pytest.fixture(scope="module", params=["search", "exhaustive"])
+def P(request):
     from paper_2603_08797_b200 import planner
 
-    return planner
+    planner.set_strategy(request.param, EXH_LIMIT)
+    yield planner
+    planner.set_strategy("search")
 
 
 def _ids(d):
