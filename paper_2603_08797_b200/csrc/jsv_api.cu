@@ -73,8 +73,8 @@ struct jsv_context {
   Prof prof;
   double kms[K_COUNT_] = {};
   long long kcnt[K_COUNT_] = {};
-  int strategy = JSV_STRATEGY_SEARCH;
-  long long exh_limit = 1LL << 22;
+  int strategy = JSV_STRATEGY_AUTO;
+  long long exh_limit = 1LL << 31;
   int shard_rank = 0, shard_world = 1;
 };
 

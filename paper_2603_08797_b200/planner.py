@@ -85,7 +85,7 @@ def _problem(app, profile, device=None) -> LW.Lowered:
     return lw
 
 
-def set_strategy(strategy: str, max_candidates: int = 1 << 22, device=None) -> None:
+def set_strategy(strategy: str, max_candidates: int = 1 << 31, device=None) -> None:
     """Choose the Stage-2 strategy of this process's planner context.
 
     "search" (level-synchronous branch-and-bound with the reference's filters),

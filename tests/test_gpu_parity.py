@@ -28,7 +28,7 @@ def P(request):
 
     planner.set_strategy(request.param, EXH_LIMIT)
     yield planner
-    planner.set_strategy("search")
+    planner.set_strategy("auto")
 
 
 def _ids(d):

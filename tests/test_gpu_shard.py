@@ -25,7 +25,7 @@ def env():
     planner.set_strategy("exhaustive", 1 << 32)
     yield planner, shard, N
     N.set_shard(N.context(), 0, 1)
-    planner.set_strategy("search")
+    planner.set_strategy("auto")
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
