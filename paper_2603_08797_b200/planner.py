@@ -227,7 +227,7 @@ def plan_batch(
     lw, _ = _prepare(app, profile, r0, options, device)
     probes = (N.Probe * len(requests))()
     for i, (a, r) in enumerate(zip(apps, requests)):
-        if a.graph is not app.graph:
+        if a.graph is not app.graph and a.graph != app.graph:
             raise ConfigError("plan_batch apps must share one task graph")
         st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
         probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
@@ -287,7 +287,7 @@ def max_demand_grid(
     lw, _ = _prepare(apps[0], profile, base_req, options, device)
     points = (N.Probe * len(apps))()
     for i, a in enumerate(apps):
-        if a.graph is not apps[0].graph:
+        if a.graph is not apps[0].graph and a.graph != apps[0].graph:
             raise ConfigError("max_demand_grid apps must share one task graph")
         st = None if space.task_graph_informed else LW.uninformed_statics(a, profile, lw, base_req)
         points[i] = LW.probe_struct(a, lw, 0.0, st)

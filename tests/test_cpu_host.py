@@ -218,3 +218,29 @@ def test_block_range_partitions_exactly():
             spans = [block_range(n, w, r) for r in range(w)]
             assert spans[0][0] == 0 and spans[-1][1] == n
             assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_workloads_star_matches_golden_generator():
+    """configs[3]'s in-repo generator reproduces the star cases pinned to the reference."""
+    from golden_io import load, profile_of
+
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.model import app_from_dict
+    from paper_2603_08797_b200.profiles import profile_to_rows
+
+    for doc in load("plans_star.json"):
+        n = int(doc["name"].split("_")[1])
+        app, table = workloads.star(n)
+        assert app == app_from_dict(doc["app"])
+        assert profile_to_rows(table) == profile_to_rows(profile_of(doc))
+
+
+def test_workloads_c3_grid_matches_golden_slos():
+    from golden_io import load
+
+    from paper_2603_08797_b200 import workloads
+
+    grid = workloads.c3_grid()
+    docs = load("max_demand_c3.json")
+    assert [(a.latency_slo_ms, a.accuracy_slo) for a in grid] == \
+        [(d["app"]["slo"]["latency_ms"], d["app"]["slo"]["accuracy_frac"]) for d in docs]
