@@ -259,7 +259,8 @@ int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
 #define JSV_KERNEL_NAMES \
   "generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank", "s2_prep", \
   "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket", "s2_prefix", "s2_exh", \
-  "s2_xreduce", "s2_xsort"
+  "s2_xreduce", "s2_xsort", \
+  "fo_prep", "fo_enum", "fo_eval"
 
 #ifdef __cplusplus
 }

@@ -117,7 +117,8 @@ EXPORTS = {
 
 KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",
                 "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket",
-                "s2_prefix", "s2_exh", "s2_xreduce", "s2_xsort")
+                "s2_prefix", "s2_exh", "s2_xreduce", "s2_xsort", "fo_prep", "fo_enum",
+                "fo_eval")
 
 STRATEGY_SEARCH, STRATEGY_EXHAUSTIVE, STRATEGY_AUTO = 0, 1, 2
 STRATEGIES = {"search": STRATEGY_SEARCH, "exhaustive": STRATEGY_EXHAUSTIVE, "auto": STRATEGY_AUTO}

@@ -61,7 +61,8 @@ enum BufId {
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
-  B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_COUNT
+  B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_COUNT
 };
 
 struct jsv_context {
@@ -1147,6 +1148,121 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   return JSV_OK;
 }
 
+// Fan-out graphs (one entry, every other task a leaf fed only by it) whose
+// cross-product is too large to sweep: knapsack-DP bounded enumeration of the
+// near-optimal class vectors + exact evaluation (jsv_fanout.cuh).  Full plans
+// only; clears active[i] for the probes it solved.
+static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active) {
+  jsv_context& c = *p.ctx;
+  if (c.strategy == JSV_STRATEGY_SEARCH || bs.feasible_only || !p.lat_fast) return JSV_OK;
+  if (getenv("JSV_NO_FANOUT")) return JSV_OK;
+  const int n = bs.n, T = p.T;
+  if (T < 3 || p.P != T - 1) return JSV_OK;
+  FoArgs a;
+  memset(&a, 0, sizeof(a));
+  a.entry = p.topo[0];
+  a.k = T - 1;
+  if (p.succ_off[a.entry + 1] - p.succ_off[a.entry] != T - 1) return JSV_OK;
+  for (int j = 0; j < a.k; ++j) {
+    if (p.path_off[j + 1] - p.path_off[j] != 2 || p.path_task[p.path_off[j]] != a.entry)
+      return JSV_OK;
+    const int l = p.path_task[p.path_off[j] + 1];
+    if (p.succ_off[l + 1] != p.succ_off[l] || p.pred_off[l + 1] - p.pred_off[l] != 1) return JSV_OK;
+    a.leaf[j] = l;
+    a.edge[j] = p.pred_edge[p.pred_off[l]];
+  }
+  const int W = bs.s1.W;
+  if (W > 1024) return JSV_OK;
+  std::vector<int> act(n, 0);
+  int P0max = 0, nact = 0;
+  for (int i = 0; i < n; ++i) {
+    const DProbe& pr = bs.probes[i];
+    if (!active[i] || bs.dead[i] || !(pr.alpha > 0) || !(pr.beta >= 0) ||
+        !std::isfinite(pr.alpha) || !std::isfinite(pr.beta))
+      continue;
+    act[i] = 1;
+    ++nact;
+    P0max = std::max(P0max, bs.pool_n[(size_t)i * T + a.entry]);
+  }
+  if (nact == 0 || P0max == 0) return JSV_OK;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  a.P0max = P0max;
+  a.SB = bs.s1.S;
+  const size_t nb0 = (size_t)n * P0max;
+  CK(B[B_FOACT].ensure(sizeof(int) * n));
+  CK(B[B_FOCLS].ensure(sizeof(FoCls) * nb0 * a.k * W));
+  CK(B[B_FONCLS].ensure(sizeof(int) * nb0 * a.k));
+  CK(B[B_FOF].ensure(sizeof(double) * nb0 * (a.k + 1) * (size_t)(a.SB + 1)));
+  CK(B[B_FOB0].ensure(sizeof(double) * nb0));
+  CK(B[B_FOTAU].ensure(sizeof(double) * n));
+  const long long cap = 1LL << 22;
+  CK(B[B_FOCAND].ensure(sizeof(FoCand) * (size_t)cap));
+  CK(B[B_FONCAND].ensure(sizeof(unsigned long long)));
+  CK(B[B_FOOVF].ensure(sizeof(int)));
+  CK(cudaMemsetAsync(B[B_FOOVF].p, 0, sizeof(int), st));
+  CK(cudaMemcpyAsync(B[B_FOACT].p, act.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  s2_base(p, bs, a.s);
+  a.act = B[B_FOACT].as<int>();
+  a.cls = B[B_FOCLS].as<FoCls>();
+  a.ncls = B[B_FONCLS].as<int>();
+  a.F = B[B_FOF].as<double>();
+  a.b0best = B[B_FOB0].as<double>();
+  a.tau = B[B_FOTAU].as<double>();
+  a.cand = B[B_FOCAND].as<FoCand>();
+  a.ncand = B[B_FONCAND].as<unsigned long long>();
+  a.cand_cap = cap;
+  a.overflow = B[B_FOOVF].as<int>();
+  c.stats.kernel_launches += launch_fanout_prep(a, st);
+  c.stats.kernel_launches += launch_fanout_tau(a, 1e-9, st);
+  CK(cudaGetLastError());
+  std::vector<double> tau(n);
+  std::vector<BestRec> best(n);
+  std::vector<double> step(n, 1e-6);
+  for (int round = 0; round < 12; ++round) {
+    long long nc = 0;
+    c.stats.kernel_launches += launch_fanout_round(a, &nc, st);
+    CK(cudaGetLastError());
+    if (nc < 0) return fail(JSV_ERR_CAPACITY, "fan-out solver: candidate capacity exceeded");
+    c.stats.leaves += nc;
+    CK(cudaMemcpyAsync(best.data(), B[B_BEST].p, sizeof(BestRec) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(tau.data(), a.tau, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool more = false;
+    if (getenv("JSV_DEBUG"))
+      for (int i = 0; i < n; ++i)
+        if (act[i])
+          fprintf(stderr, "[jsv fanout] round %d probe %d cand %lld tau %.17g has %d obj %.17g\n",
+                  round, i, nc, tau[i], best[i].has, best[i].obj);
+    for (int i = 0; i < n; ++i) {
+      if (!act[i]) continue;
+      if (!std::isfinite(tau[i])) {  // no entry bundle reaches the accuracy SLO: infeasible
+        act[i] = 0;
+        continue;
+      }
+      if (best[i].has) {
+        const double eps = 1e-11 * (1.0 + std::fabs(best[i].obj));
+        if (tau[i] <= best[i].obj - eps) {
+          act[i] = 0;  // every candidate that could beat or tie the optimum was evaluated
+          active[i] = 0;
+          continue;
+        }
+        tau[i] = best[i].obj - 2.0 * eps;
+      } else {
+        tau[i] -= step[i];
+        step[i] *= 100.0;
+      }
+      more = true;
+    }
+    if (!more) break;
+    CK(cudaMemcpyAsync(a.tau, tau.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(B[B_FOACT].p, act.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  }
+  // probes left active (no feasible plan found) go to the branch-and-bound, whose
+  // diagnostic re-run also supplies the binding constraint
+  return JSV_OK;
+}
+
 // plan() for a batch of probes sharing one request
 static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, const jsv_probe* in,
                                jsv_plan_out* out, bool want_config) {
@@ -1169,6 +1285,8 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     if (rc) return rc;
     std::vector<int> active(n, 1);
     rc = run_exhaustive(p, bs, want_config, active);
+    if (rc) return rc;
+    rc = run_fanout(p, bs, active);
     if (rc) return rc;
     long long nn = 0;
     bool any_search = false;

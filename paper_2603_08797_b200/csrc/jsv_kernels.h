@@ -6,7 +6,7 @@
 // Per-kernel CUDA-event timing on the launching stream (bench.py roofline).
 enum KernelId {
   K_GENERATE, K_STATS, K_PAIRS_A, K_COMPACT, K_PAIRS_B, K_TRUNCATE, K_MRANK, K_S2_PREP,
-  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_S2_EXH, K_S2_XREDUCE, K_S2_XSORT, K_COUNT_
+  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_S2_EXH, K_S2_XREDUCE, K_S2_XSORT, K_FO_PREP, K_FO_ENUM, K_FO_EVAL, K_COUNT_
 };
 
 struct Prof {
@@ -224,6 +224,45 @@ __host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) 
 size_t x_smem_bytes(int max_pn_last, int P, bool rank);
 int launch_stage2_exhaustive(const XArgs& a, long long n_blocks, int P, size_t smem,
                              cudaStream_t st);
+
+// fan-out graphs (jsv_fanout.cuh)
+#define FO_DELTA_W 1e-9   // slack on real-valued accuracy sums (>> float error)
+#define FO_EPS_OBJ 1e-11  // |float objective - real objective| bound used for convergence
+
+struct FoCls {
+  double acc;  // accuracy of the class (bundle accuracy)
+  int s;       // slices
+  int pad_;
+};
+
+struct FoCand {
+  int probe, b0;
+  uint16_t cls[MAXT];  // class index per leaf position (0xFFFF: no instances)
+};
+
+struct FoArgs {
+  S2Args s;
+  int k;                   // leaves
+  int entry;               // entry task index
+  int leaf[MAXT];          // leaf task index per path (graph.paths order)
+  int edge[MAXT];          // edge entry -> leaf
+  int P0max;               // largest entry pool of the batch
+  int SB;                  // slice budget (DP range 0..SB)
+  const int* act;          // [n_probes] 1 = solve with this path
+  FoCls* cls;              // [probe][b0][leafpos][W]
+  int* ncls;               // [probe][b0][leafpos]
+  double* F;               // [probe][b0][leafpos + 1][SB + 1]
+  double* b0best;          // [probe][b0] best real objective (-inf: none)
+  double* tau;             // [n_probes]
+  FoCand* cand;            // candidate buffer
+  unsigned long long* ncand;
+  long long cand_cap;
+  int* overflow;
+};
+
+int launch_fanout_prep(const FoArgs& a, cudaStream_t st);
+int launch_fanout_tau(const FoArgs& a, double delta, cudaStream_t st);
+int launch_fanout_round(const FoArgs& a, long long* n_cand_host, cudaStream_t st);
 
 int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st);
 int launch_stage2_reduce(const S2Args& a, cudaStream_t st);

@@ -96,6 +96,7 @@ __device__ inline void load_leaf(const S2Args& a, int probe, const uint16_t* ch_
 
 #include "jsv_search.cuh"
 #include "jsv_exhaustive.cuh"
+#include "jsv_fanout.cuh"
 
 
 __device__ void write_config(const FinArgs& a, int probe, const uint16_t* cb_task,
