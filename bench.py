@@ -268,6 +268,49 @@ def c3_apps(app):
     return [dataclasses.replace(app, latency_slo_ms=L, accuracy_slo=a) for L in C3_LAT for a in C3_ACC]
 
 
+def star12_solve(P, torch, flush) -> dict:
+    """configs[3]: the 12-task star at 200 rps / 84 slices (reference: no result in 600 s)."""
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    app, table = workloads.star(12)
+    req = PlanRequest(200.0, 84, SearchSpace(True, True, True))
+    P.plan(app, table, req)
+    dev, wall = [], []
+    for _ in range(5):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = P.plan(app, table, req)
+        wall.append((time.perf_counter() - t0) * 1e3)
+        dev.append(P.last_stats()["ms_total"])
+    return {"solve_ms": statistics.median(dev), "solve_wall_ms": statistics.median(wall),
+            "objective": r.objective, "total_slices": r.config.total_slices,
+            "solver": "fan-out knapsack-DP bounded enumeration + exact evaluation"}
+
+
+def traffic840(P) -> dict:
+    """configs[4]: traffic-analysis on 840 slices -- max_demand in all 8 spaces, then the
+    288-bin day trace planned for A+S+T and the three ablations (one batch per space)."""
+    from paper_2603_08797_b200 import workload, workloads
+    from paper_2603_08797_b200.plan_types import ALL_SPACES, SearchSpace
+
+    app, table = workloads.traffic()
+    t0 = time.perf_counter()
+    md = {sp.label: P.max_demand(app, table, 840, sp).demand_rps for sp in ALL_SPACES}
+    md_ms = (time.perf_counter() - t0) * 1e3
+    trace = workload.gen_trace(workload.TraceShape(0.35, 0.65, 0.03, 288), md["A+S+T"], 21)
+    spaces = [SearchSpace.from_label(x) for x in ("A+S+T", "S+T", "A+T", "A+S")]
+    workload.plan_day(app, table, trace, 840, spaces[0])  # warm-up
+    t0 = time.perf_counter()
+    days = {sp.label: workload.plan_day(app, table, trace, 840, sp) for sp in spaces}
+    day_ms = (time.perf_counter() - t0) * 1e3
+    return {"max_demand_8_spaces_ms": md_ms, "max_demand_rps": md,
+            "trace_bins": len(trace), "trace_plans": len(trace) * len(spaces), "trace_ms": day_ms,
+            "trace_plans_per_s": len(trace) * len(spaces) / (day_ms / 1e3),
+            "fallback_bins": {k: sum(d.used_fallback for d in v) for k, v in days.items()}}
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -391,6 +434,9 @@ def main() -> None:
         sweep_ms = min(sw)
         probes = sum(r.probes for r in mres)
         extras["sweep_local"] = (len(grid), sweep_ms, probes)
+        if rank == 0:
+            extras["configs3_star12"] = star12_solve(P, torch, flush)
+            extras["configs4_traffic840"] = traffic840(P)
 
     t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1]],
                      dtype=torch.float64, device="cuda")
