@@ -62,7 +62,7 @@ enum BufId {
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
-  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_COUNT
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_COUNT
 };
 
 struct jsv_context {
@@ -658,6 +658,10 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_SCR].ensure(sizeof(int) * C1));
   CK(B[B_ORDER].ensure(sizeof(int) * C1));
   CK(B[B_BSTART].ensure(sizeof(int) * jobs * (rq.budget + 2)));
+  CK(B[B_SURV].ensure(sizeof(int) * C1));
+  CK(B[B_PCNT].ensure(sizeof(int) * C1));
+  CK(B[B_SBST].ensure(sizeof(int) * jobs * (rq.budget + 2)));
+  CK(B[B_SCNT].ensure(sizeof(int) * jobs));
   CK(B[B_CNT].ensure(sizeof(int) * jobs));
   CK(B[B_FCNT].ensure(sizeof(int) * jobs));
   CK(B[B_POOLC].ensure(sizeof(int) * jobs * W));
@@ -724,6 +728,10 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.S = rq.budget;
   a.order = B[B_ORDER].as<int>();
   a.bstart = B[B_BSTART].as<int>();
+  a.surv = B[B_SURV].as<int>();
+  a.pcnt = B[B_PCNT].as<int>();
+  a.sbst = B[B_SBST].as<int>();
+  a.scnt = B[B_SCNT].as<int>();
   S1Launch L{};
   L.tile_task = B[B_TILE_TASK].as<int>();
   L.tile_start = B[B_TILE_START].as<int>();

@@ -86,6 +86,10 @@ struct S1Args {
   int S;          // slice budget
   int* order;     // [Ctot] per-job candidate order by slices
   int* bstart;    // [jobs * (S+2)] slice bucket starts
+  int* surv;      // [Ctot] survivors of the same-bucket skyline pass, slices order
+  int* pcnt;      // [Ctot] survivors before each sorted position
+  int* sbst;      // [jobs * (S+2)] survivor bucket starts
+  int* scnt;      // [jobs] survivors
 };
 
 struct S1Launch {

@@ -246,42 +246,68 @@ __device__ __forceinline__ int cmp_items(const S1Args& a, long long c1, long lon
 
 #define TJ 128
 
+// Skyline test in two passes (the dominance relation is transitive, so a
+// candidate is dominated iff some skyline candidate dominates it):
+//   mode 0  every candidate against the candidates of its own slices bucket
+//           (>90% of dominated candidates have a same-slices dominator);
+//   mode 1  the survivors of mode 0 against the survivors with fewer slices.
+// A candidate dies if another weakly dominates it with a different row, or has
+// an identical row and smaller items (the reference's dedup); by transitivity
+// this equals the reference's sequential "not dominated by an earlier kept
+// row" filter.  i runs over the slices-sorted list so a block's candidates
+// have similar slices and the j range a block stages in shared memory is short.
 template <int D>
 __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
-                                                 const int* tile_start, int tiles_pp, int jchunk) {
+                                                 const int* tile_start, int tiles_pp, int jchunk,
+                                                 int mode) {
   __shared__ double sh[D * TJ];
   __shared__ int shj[TJ];
-  __shared__ int s_end;
+  __shared__ int s_lo, s_hi;
   const int probe = blockIdx.x / tiles_pp;
   const int tl = blockIdx.x % tiles_pp;
   const int t = tile_task[tl];
   const int i0 = tile_start[tl];
   const int job = probe * a.T + t;
-  const int n = a.cnt[job];
+  const int n = mode == 0 ? a.cnt[job] : a.scnt[job];
   if (i0 >= n) return;
   const int j0 = blockIdx.y * jchunk;
   if (j0 >= n) return;
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long base = job_base(a, probe, t);
-  const int* order = a.order + base;
+  const int* list = (mode == 0 ? a.order : a.surv) + base;
   const int* bst = a.bstart + (long long)job * (a.S + 2);
-  // i runs over the slices-sorted order so a block's candidates have similar slices
+  const int* sbst = a.sbst + (long long)job * (a.S + 2);
   const bool act = i0 + (int)threadIdx.x < n;
-  const int i = act ? order[i0 + threadIdx.x] : 0;
+  const int i = act ? list[i0 + threadIdx.x] : 0;
   double xi[D];
 #pragma unroll
   for (int d = 0; d < D; ++d) xi[d] = act ? a.arr[d * tot + base + i] : 0.0;
-  // only candidates with no more slices can dominate: scan order[0 .. end_i)
-  const int end_i = act ? bst[(int)xi[0] + 1] : 0;
-  if (threadIdx.x == 0) s_end = 0;
+  int lo_i = 0, hi_i = 0;
+  if (act) {
+    const int si = (int)xi[0];
+    if (mode == 0) {
+      lo_i = bst[si];
+      hi_i = bst[si + 1];
+    } else {
+      hi_i = sbst[si];
+    }
+  }
+  if (threadIdx.x == 0) {
+    s_lo = 0x7FFFFFFF;
+    s_hi = 0;
+  }
   __syncthreads();
-  if (act) atomicMax(&s_end, end_i);
+  if (act && hi_i > lo_i) {
+    atomicMin(&s_lo, lo_i);
+    atomicMax(&s_hi, hi_i);
+  }
   __syncthreads();
-  const int j1 = min(min(n, j0 + jchunk), s_end);
+  const int jbeg = max(j0, s_lo);
+  const int j1 = min(min(n, j0 + jchunk), s_hi);
   unsigned fl = 0;
-  for (int jt = j0; jt < j1; jt += TJ) {
+  for (int jt = jbeg; jt < j1; jt += TJ) {
     const int nj = min(TJ, j1 - jt);
-    for (int x = threadIdx.x; x < TJ; x += blockDim.x) shj[x] = x < nj ? order[jt + x] : 0;
+    for (int x = threadIdx.x; x < TJ; x += blockDim.x) shj[x] = x < nj ? list[jt + x] : 0;
     __syncthreads();
     for (int x = threadIdx.x; x < D * TJ; x += blockDim.x) {
       int d = x / TJ, jj = x % TJ;
@@ -289,8 +315,8 @@ __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
     }
     __syncthreads();
     if (act && !fl) {
-      const int lim = min(nj, end_i - jt);
-      for (int jj = 0; jj < lim; ++jj) {
+      const int jlo = max(0, lo_i - jt), jhi = min(nj, hi_i - jt);
+      for (int jj = jlo; jj < jhi; ++jj) {
         bool le = true, eq = true;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
@@ -317,6 +343,39 @@ __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
     __syncthreads();
   }
   if (act && fl) atomicOr(&a.flag[base + i], fl);
+}
+
+// Survivors of the same-bucket pass, in slices order, and their bucket starts
+// sbst[s] = #survivors with fewer than s slices.
+__global__ void __launch_bounds__(1024) k_surv(S1Args a) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int n = a.cnt[job];
+  const long long base = job_base(a, probe, t);
+  const int* order = a.order + base;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int s0 = 0; s0 < n; s0 += 1024) {
+    const int p = s0 + threadIdx.x;
+    const int i = p < n ? order[p] : 0;
+    const int alive = (p < n && a.flag[base + i] == 0u) ? 1 : 0;
+    int off, total;
+    Scan(tmp).ExclusiveSum(alive, off, total);
+    if (p < n) a.pcnt[base + p] = carry + off;
+    if (alive) a.surv[base + carry + off] = i;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  const int total = carry;
+  const int NB = a.S + 2;
+  const int* bst = a.bstart + (long long)job * NB;
+  int* sb = a.sbst + (long long)job * NB;
+  for (int s = threadIdx.x; s < NB; s += blockDim.x) sb[s] = bst[s] >= n ? total : a.pcnt[base + bst[s]];
+  if (threadIdx.x == 0) a.scnt[job] = total;
 }
 
 __global__ void __launch_bounds__(1024) k_compact(S1Args a) {
@@ -590,9 +649,11 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   if (L.tiles_pp > 0) {
     dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
     PROF_BEGIN(K_PAIRS_A);
-    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a);
+    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a, 0);
+    k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a, 1);
     PROF_END();
-    ++launches;
+    launches += 3;
   }
   PROF_BEGIN(K_COMPACT);
   k_compact<<<a.n_probes * a.T, 1024, 0, st>>>(a);
