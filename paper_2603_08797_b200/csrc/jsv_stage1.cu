@@ -45,24 +45,46 @@ __device__ __forceinline__ long long job_base(const S1Args& a, int probe, int t)
   return (long long)probe * a.C_probe + a.task_base[t];
 }
 
-__device__ inline void append_candidate(const S1Args& a, int probe, int t, const uint32_t* it,
-                                        int n) {
-  int job = probe * a.T + t;
-  int pos = atomicAdd(&a.cnt[job], 1);
+// Slots for the m candidates of this thread in its job's slab: one atomicAdd per
+// (warp, job) group instead of one per candidate (the slab counter is hot).
+__device__ __forceinline__ int reserve_slots(const S1Args& a, int job, int m, bool active) {
+  const unsigned full = 0xffffffffu;
+  const int key = active ? job : -1;
+  const unsigned grp = __match_any_sync(full, key);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(grp) - 1;
+  // exclusive prefix of m over the group's lanes below this one
+  int pre = 0, tot = 0;
+  unsigned g = grp;
+  while (g) {
+    const int l = __ffs(g) - 1;
+    g &= g - 1;
+    const int v = __shfl_sync(grp, m, l);
+    if (l < lane) pre += v;
+    tot += v;
+  }
+  int basepos = 0;
+  if (lane == leader && active && tot > 0) basepos = atomicAdd(&a.cnt[job], tot);
+  basepos = __shfl_sync(grp, basepos, leader);
+  return basepos + pre;
+}
+
+__device__ __forceinline__ void store_candidate(const S1Args& a, int probe, int t, int pos,
+                                                const uint32_t* it, int n) {
   if (pos >= a.task_cap[t]) {
     atomicExch(a.err, 1);
     return;
   }
-  long long c = job_base(a, probe, t) + pos;
+  const long long c = job_base(a, probe, t) + pos;
   a.nitems[c] = n;
   for (int k = 0; k < n; ++k) a.items[c * a.maxi + k] = it[k];
 }
 
 __global__ void k_generate(S1Args a) {
-  long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (gtid >= (long long)a.n_probes * a.U) return;
-  const int probe = (int)(gtid / a.U);
-  const int u = (int)(gtid % a.U);
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const bool in = gtid < (long long)a.n_probes * a.U;
+  const int probe = in ? (int)(gtid / a.U) : 0;
+  const int u = in ? (int)(gtid % a.U) : 0;
   int d = 0;
   while (d + 1 < a.n_desc && a.desc[d + 1].unit_off <= u) ++d;
   const GenDesc D = a.desc[d];
@@ -73,92 +95,105 @@ __global__ void k_generate(S1Args a) {
   const int S = rq.S;
   const int kb = g.key_off[t];
   const int* tup = a.tb.sub_key + D.key_base;
+  // this unit's candidates: one item list (n items), or m singletons of key `key1`
   uint32_t it[MAXI];
-  int n = 0;
-  if (D.mode == 0) {
-    // unrank count vector lu+1 (0 is the empty vector) -- _exhaustive_counts
-    unsigned long long idx = (unsigned long long)lu + 1ull;
-    int left = S;
-    const unsigned* W = a.ways + D.w_off;
-    for (int i = 0; i < D.n_tuples; ++i) {
-      const int cost = a.tb.key_cost[kb + tup[i]];
-      int c = 0;
-      while (true) {
-        unsigned long long w = W[(i + 1) * (S + 1) + (left - c * cost)];
-        if (idx < w) break;
-        idx -= w;
-        ++c;
+  int n = 0, m = 0, key1 = -1;
+  int counts[N_LEVELS + 1];
+  if (in) {
+    if (D.mode == 0) {
+      // unrank count vector lu+1 (0 is the empty vector) -- _exhaustive_counts
+      unsigned long long idx = (unsigned long long)lu + 1ull;
+      int left = S;
+      const unsigned* W = a.ways + D.w_off;
+      bool ok = true;
+      for (int i = 0; i < D.n_tuples && ok; ++i) {
+        const int cost = a.tb.key_cost[kb + tup[i]];
+        int c = 0;
+        while (true) {
+          unsigned long long w = W[(i + 1) * (S + 1) + (left - c * cost)];
+          if (idx < w) break;
+          idx -= w;
+          ++c;
+        }
+        if (c > 0) {
+          if (n >= MAXI) { atomicExch(a.err, 2); ok = false; break; }
+          it[n++] = ((uint32_t)tup[i] << 16) | (uint32_t)c;
+        }
+        left -= c * cost;
       }
-      if (c > 0) {
-        if (n >= MAXI) { atomicExch(a.err, 2); return; }
-        it[n++] = ((uint32_t)tup[i] << 16) | (uint32_t)c;
+      m = ok ? 1 : 0;
+    } else {
+      const DProbe& pr = a.probes[probe];
+      const double target = pr.r_upper[D.a][t] * (1.0 + rq.slack);
+      const bool has_lv = target > 0;
+      if (lu < D.n_tuple_units) {
+        // singleton + homogeneous covers of one tuple, distinct counts only
+        key1 = tup[lu];
+        const int cost = a.tb.key_cost[kb + key1];
+        const double h = a.tb.key_thr[kb + key1];
+        int mm = 0;
+        if (cost <= S) counts[mm++] = 1;
+        if (has_lv) {
+          for (int k = 0; k < N_LEVELS; ++k) {
+            int c = cover_count(target * c_grid[k], h, cost, S);
+            if (c > 0) counts[mm++] = c;
+          }
+        }
+        for (int x = 0; x < mm; ++x) {
+          bool dup = false;
+          for (int y = 0; y < m; ++y) dup |= counts[y] == counts[x];
+          if (!dup) counts[m++] = counts[x];
+        }
+      } else if (has_lv) {
+        // two-variant mix unit: (pair, phi, level, rep_a, rep_b)
+        int mu = lu - D.n_tuple_units;
+        const int per_pair = rq.n_mix * N_LEVELS * 4;
+        int pi = mu / per_pair;
+        int rem = mu % per_pair;
+        const int rsel = rem & 3;
+        rem >>= 2;
+        const int lvk = rem % N_LEVELS;
+        const int ph = rem / N_LEVELS;
+        int ga = 0, gb = 1;
+        {
+          // pair index -> (ga < gb) in row-major order
+          int G = D.n_groups;
+          int acc = 0;
+          for (ga = 0; ga < G; ++ga) {
+            int cnt = G - 1 - ga;
+            if (pi < acc + cnt) { gb = ga + 1 + (pi - acc); break; }
+            acc += cnt;
+          }
+        }
+        const int ia = a.tb.grp_rep[2 * (D.grp_base + ga) + (rsel & 1)];
+        const int ib = a.tb.grp_rep[2 * (D.grp_base + gb) + (rsel >> 1)];
+        if (ia >= 0 && ib >= 0) {
+          const double phi = rq.mix[ph];
+          const double lvl = target * c_grid[lvk];
+          const int ka = tup[ia], kbb = tup[ib];
+          const int costa = a.tb.key_cost[kb + ka], costb = a.tb.key_cost[kb + kbb];
+          const int ca = cover_count(phi * lvl, a.tb.key_thr[kb + ka], costa, S);
+          const int cb = cover_count((1.0 - phi) * lvl, a.tb.key_thr[kb + kbb], costb, S);
+          if (ca != 0 && cb != 0 && ca * costa + cb * costb <= S) {
+            it[0] = ((uint32_t)ka << 16) | (uint32_t)ca;
+            it[1] = ((uint32_t)kbb << 16) | (uint32_t)cb;
+            n = 2;
+            m = 1;
+          }
+        }
       }
-      left -= c * cost;
     }
-    append_candidate(a, probe, t, it, n);
-    return;
   }
-  const DProbe& pr = a.probes[probe];
-  const double target = pr.r_upper[D.a][t] * (1.0 + rq.slack);
-  const bool has_lv = target > 0;
-  if (lu < D.n_tuple_units) {
-    // singleton + homogeneous covers of one tuple, distinct counts only
-    const int key = tup[lu];
-    const int cost = a.tb.key_cost[kb + key];
-    const double h = a.tb.key_thr[kb + key];
-    int counts[N_LEVELS + 1];
-    int m = 0;
-    if (cost <= S) counts[m++] = 1;
-    if (has_lv) {
-      for (int k = 0; k < N_LEVELS; ++k) {
-        int c = cover_count(target * c_grid[k], h, cost, S);
-        if (c > 0) counts[m++] = c;
-      }
-    }
+  const int job = probe * a.T + t;
+  const int pos = reserve_slots(a, job, m, in);
+  if (key1 >= 0) {
     for (int x = 0; x < m; ++x) {
-      bool dup = false;
-      for (int y = 0; y < x; ++y) dup |= counts[y] == counts[x];
-      if (dup) continue;
-      uint32_t one = ((uint32_t)key << 16) | (uint32_t)counts[x];
-      append_candidate(a, probe, t, &one, 1);
+      const uint32_t one = ((uint32_t)key1 << 16) | (uint32_t)counts[x];
+      store_candidate(a, probe, t, pos + x, &one, 1);
     }
-    return;
+  } else if (m > 0) {
+    store_candidate(a, probe, t, pos, it, n);
   }
-  if (!has_lv) return;
-  // two-variant mix unit: (pair, phi, level, rep_a, rep_b)
-  int mu = lu - D.n_tuple_units;
-  const int per_pair = rq.n_mix * N_LEVELS * 4;
-  int pi = mu / per_pair;
-  int rem = mu % per_pair;
-  const int rsel = rem & 3;
-  rem >>= 2;
-  const int lvk = rem % N_LEVELS;
-  const int ph = rem / N_LEVELS;
-  int ga = 0, gb = 1;
-  {
-    // pair index -> (ga < gb) in row-major order
-    int G = D.n_groups;
-    int acc = 0;
-    for (ga = 0; ga < G; ++ga) {
-      int cnt = G - 1 - ga;
-      if (pi < acc + cnt) { gb = ga + 1 + (pi - acc); break; }
-      acc += cnt;
-    }
-  }
-  const int ia = a.tb.grp_rep[2 * (D.grp_base + ga) + (rsel & 1)];
-  const int ib = a.tb.grp_rep[2 * (D.grp_base + gb) + (rsel >> 1)];
-  if (ia < 0 || ib < 0) return;
-  const double phi = rq.mix[ph];
-  const double lvl = target * c_grid[lvk];
-  const int ka = tup[ia], kbb = tup[ib];
-  const int costa = a.tb.key_cost[kb + ka], costb = a.tb.key_cost[kb + kbb];
-  int ca = cover_count(phi * lvl, a.tb.key_thr[kb + ka], costa, S);
-  int cb = cover_count((1.0 - phi) * lvl, a.tb.key_thr[kb + kbb], costb, S);
-  if (ca == 0 || cb == 0) return;
-  if (ca * costa + cb * costb > S) return;
-  it[0] = ((uint32_t)ka << 16) | (uint32_t)ca;
-  it[1] = ((uint32_t)kbb << 16) | (uint32_t)cb;
-  append_candidate(a, probe, t, it, 2);
 }
 
 __device__ __forceinline__ int locate_task(const S1Args& a, long long local) {
