@@ -552,21 +552,23 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
       } else if (RANK && RPL > 0) {
         if (lane < pn) leaves += (unsigned)((pn - lane + 31) >> 5);
         const uint4 th = ws.th[j];
-        if (th.z == 0) goto next_prefix;  // latency or resources fail for every bundle
+        // (a prefix whose own verdicts fail has th.z = 0: every record then fails the
+        // latency field, but its four sink compares are still evaluated)
         // SWAR: two 15-bit fields per word, all "x >= threshold" with a guard bit;
         // (w | H) - B keeps bit 15 of a field iff that field passes
         const unsigned rem = th.w < 0x7FFFu ? th.w : 0x7FFFu;
         const unsigned B0 = (th.x << 16) | th.y;
         const unsigned B1 = ((0x8000u - th.z) << 16) | (0x7FFFu - rem);
-        unsigned m = 0xFFFFFFFFu;
+        // v = guard bits of both words: a record passes iff v == H, the largest value
+        // v can take, so one running max decides whether any of them passes
+        unsigned m = 0u;
 #pragma unroll
-        for (int k = 0; k < RPL; ++k)
-          m = min(m, 0x80008000u & ~((rec[k].x - B0) & (rec[k].y - B1)));
+        for (int k = 0; k < RPL; ++k) m = max(m, (rec[k].x - B0) & (rec[k].y - B1) & 0x80008000u);
         unsigned mask = 0;
-        if (m == 0) {
+        if (m == 0x80008000u) {
 #pragma unroll
           for (int k = 0; k < RPL; ++k)
-            mask |= ((0x80008000u & ~((rec[k].x - B0) & (rec[k].y - B1))) == 0 ? 1u : 0u) << k;
+            mask |= (((rec[k].x - B0) & (rec[k].y - B1) & 0x80008000u) == 0x80008000u ? 1u : 0u) << k;
         }
         if (mask) {
           double lo[PM];
@@ -653,7 +655,6 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
             break;
         }
       }
-    next_prefix:
       if (x_better(a, xp, probe, rb, best)) best = rb;
     }
     __syncwarp();
