@@ -524,22 +524,32 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
 #pragma unroll
     for (int k = 0; k < RPL; ++k) rec[k] = rv.pack[lane + 32 * k];
     // ---- groups of G lanes sweep the sink pool for each prefix
+    unsigned nswept = 0;  // RPL sweeps: valid prefixes swept by the whole warp this round
     for (int j = gi; j < NS; j += gw) {
       const int fl = ws.flags[j];
       if (!(fl & 1)) continue;  // not a leaf prefix (group-uniform)
-      const long long qp = ws.q[j];
-      const double need = ws.need[j];
-      const int sl_pre = ws.sl[j];
-      const bool ok_pre = (fl & 2) != 0, later = (fl & 4) != 0;
+      // prefix state, read from shared memory where a path needs it
+      long long qp;
+      double need;
+      int sl_pre;
+      bool ok_pre, later;
       double f[PM], c[PM], pp[PM];
+      auto load_state = [&]() {
+        qp = ws.q[j];
+        need = ws.need[j];
+        sl_pre = ws.sl[j];
+        ok_pre = (fl & 2) != 0;
+        later = (fl & 4) != 0;
 #pragma unroll
-      for (int p = 0; p < PM; ++p) {
-        f[p] = ws.s0[p][j];
-        c[p] = ws.s1[p][j];
-        pp[p] = ws.s2[p][j];
-      }
+        for (int p = 0; p < PM; ++p) {
+          f[p] = ws.s0[p][j];
+          c[p] = ws.s1[p][j];
+          pp[p] = ws.s2[p][j];
+        }
+      };
       XBest rb;
       rb.has = 0; rb.sl = 0; rb.obj = 0.0; rb.idx = 0;
+      if (!(RANK && RPL > 0) || (fl & 8)) load_state();
       if (fl & 8) {
         // sink demand 0: its only child is "no instances" (planner.py:868-875)
         if (lane_g == 0) {
@@ -550,7 +560,7 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
                        a_max, later, rb);
         }
       } else if (RANK && RPL > 0) {
-        if (lane < pn) leaves += (unsigned)((pn - lane + 31) >> 5);
+        ++nswept;
         const uint4 th = ws.th[j];
         // (a prefix whose own verdicts fail has th.z = 0: every record then fails the
         // latency field, but its four sink compares are still evaluated)
@@ -571,6 +581,7 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
             mask |= (((rec[k].x - B0) & (rec[k].y - B1) & 0x80008000u) == 0x80008000u ? 1u : 0u) << k;
         }
         if (mask) {
+          load_state();
           double lo[PM];
 #pragma unroll
           for (int p = 0; p < PM; ++p) lo[p] = ws.lo[p][j];
@@ -655,8 +666,9 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
             break;
         }
       }
-      if (x_better(a, xp, probe, rb, best)) best = rb;
+      if (rb.has && x_better(a, xp, probe, rb, best)) best = rb;
     }
+    if (RANK && RPL > 0 && lane < pn) leaves += (unsigned long long)nswept * ((pn - lane + 31) >> 5);
     __syncwarp();
   }
   if (a.mode == LEAF_ANY && best.has) found[probe] = 1;
