@@ -21,6 +21,21 @@
 
 static thread_local std::string g_err;
 
+#include <chrono>
+// JSV_TIMING=1: host-side timestamps of the batch pipeline on stderr (diagnostics)
+static double host_ms() {
+  using namespace std::chrono;
+  return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+static bool timing_on() {
+  static const bool on = getenv("JSV_TIMING") != nullptr;
+  return on;
+}
+#define JSV_T(label)                                                              \
+  do {                                                                            \
+    if (timing_on()) fprintf(stderr, "[jsv t] %10.3f %s\n", host_ms(), label); \
+  } while (0)
+
 static int fail(int code, const std::string& msg) {
   g_err = msg;
   return code;
@@ -430,7 +445,18 @@ static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_pr
   o.acc_slo = in.acc_slo;
   o.alpha = in.alpha;
   o.beta = in.beta;
-  acc_threshold(p.a_max, in.acc_slo, o.acc_thr, o.acc_thr_ok);
+  {
+    // one bisection per distinct (a_max, acc_slo): probes of a sweep share them
+    static thread_local double c_amax = NAN, c_slo = NAN, c_thr = 0.0;
+    static thread_local int c_ok = 0;
+    if (!(p.a_max == c_amax && in.acc_slo == c_slo)) {
+      acc_threshold(p.a_max, in.acc_slo, c_thr, c_ok);
+      c_amax = p.a_max;
+      c_slo = in.acc_slo;
+    }
+    o.acc_thr = c_thr;
+    o.acc_thr_ok = c_ok;
+  }
   double fac[MAXE], r[MAXT];
   for (int a = 0; a < 2; ++a) {
     host_factors(p, rq, a == 1, true, fac);
@@ -835,6 +861,8 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   DevBuf* ncnt = &B[B_NXTCNT];   // counts of the next frontier
   long long nodes = 0;
   for (int L = 0; L < T; ++L) {
+    JSV_T("s2 level begin");
+    if (timing_on()) fprintf(stderr, "[jsv t] level %d slots %lld\n", L, n_slots);
     const bool last = (L == T - 1);
     const size_t S1 = (size_t)std::max<long long>(1, n_slots);
     CK(B[B_FOFF].ensure(sizeof(long long) * n));
@@ -1039,6 +1067,10 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
                           std::vector<int>& active) {
   jsv_context& c = *p.ctx;
   if (c.strategy == JSV_STRATEGY_SEARCH) return JSV_OK;
+  // feasibility probes (max_demand): the branch-and-bound stops at the first
+  // feasible leaf and prunes infeasible probes early; the sweep would prove
+  // infeasibility by visiting everything.  Auto keeps the sweep for full plans.
+  if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) return JSV_OK;
   cudaStream_t st = c.st;
   auto& B = c.buf;
   const int n = bs.n, T = p.T;
@@ -1282,9 +1314,12 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   bs.feasible_only = rq.feasible_only;
   bs.probes.resize(n);
   for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], bs.probes[i]);
+  JSV_T("batch begin");
+  if (timing_on()) fprintf(stderr, "[jsv t] probes %d\n", n);
   CK(cudaEventRecord(c.ev[0], st));
   int rc = run_stage1(p, rq, n, bs.probes.data(), bs);
   if (rc) return rc;
+  JSV_T("stage1 done");
   CK(cudaEventRecord(c.ev[1], st));
   const bool informed = (rq.space & JSV_SPACE_T) != 0;
   std::vector<long long> nodes(n, 0);
@@ -1327,11 +1362,13 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
       if (rc) return rc;
     }
   }
+  JSV_T("stage2 done");
   CK(cudaEventRecord(c.ev[2], st));
   rc = finalize(p, bs, !informed, out, &nodes);
   if (rc) return rc;
   CK(cudaEventRecord(c.ev[3], st));
   CK(cudaEventSynchronize(c.ev[3]));
+  JSV_T("finalize done");
   collect_prof(c);
   float ms1 = 0, ms2 = 0, mst = 0;
   cudaEventElapsedTime(&ms1, c.ev[0], c.ev[1]);
@@ -1456,13 +1493,23 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
       }
     }
   }
-  const int budget_probes = 4096;
+  // speculation depth: a round costs ~F of latency (launches, host round trips)
+  // plus ~c per probe; a depth-d bisection subtree resolves d levels with
+  // 2^d - 1 probes, so pick d minimising (F + active (2^d - 1) c) / d
+  const double round_ms = 1.0, probe_ms = 0.01;
   while (true) {
     int active = 0;
     for (auto& s : ps) active += (s.phase == 1 || s.phase == 2);
     if (!active) break;
     int depth = 1;
-    while (depth < 8 && (long long)active * ((1 << (depth + 1)) - 1) <= budget_probes) ++depth;
+    double best_rate = 1e300;
+    for (int d = 1; d <= 8; ++d) {
+      const double r = (round_ms + (double)active * ((1 << d) - 1) * probe_ms) / d;
+      if (r < best_rate) {
+        best_rate = r;
+        depth = d;
+      }
+    }
     std::vector<std::pair<int, double>> w;
     std::vector<std::vector<double>> tree(n);
     for (int i = 0; i < n; ++i) {
