@@ -189,6 +189,9 @@ def cpu_sample(args) -> dict:
     from multiprocessing import Pool
 
     n = args.cpu_sample
+    if args.impl == "reference":
+        # all host cores, ~24 solves (~4 s of CPU work) per core per step
+        n = max(n, 24 * (os.cpu_count() or 1))
     dem = demand_points(n, 0, 1)
     cores = min(os.cpu_count() or 1, n) if args.impl == "reference" else 1
     if cores > 1:
