@@ -244,3 +244,76 @@ def test_workloads_c3_grid_matches_golden_slos():
     docs = load("max_demand_c3.json")
     assert [(a.latency_slo_ms, a.accuracy_slo) for a in grid] == \
         [(d["app"]["slo"]["latency_ms"], d["app"]["slo"]["accuracy_frac"]) for d in docs]
+
+
+def _fake_result(feasible, objective, slices, m):
+    from paper_2603_08797_b200.plan_types import Configuration, PlanResult, SolverStats
+
+    cfg = None
+    if feasible:
+        cfg = Configuration(m, 1.0, {}, {}, {}, {}, {}, {}, {}, {}, slices, 1.0, 1.0, objective, ())
+    return PlanResult(feasible, cfg, objective if feasible else None, 1.0,
+                      None if feasible else "throughput", (), SolverStats(0, 0.0))
+
+
+def _gloo_plan_sharded_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2603_08797_b200 import _native as N
+    from paper_2603_08797_b200 import planner, shard
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    seen = {}
+    # the GPU solve of one shard, faked per rank: rank 0 and 2 tie on (objective,
+    # slices) and differ in m; rank 1 has fewer slices at a lower objective;
+    # rank 3's shard is infeasible
+    local = {0: _fake_result(True, 0.5, 7, ((("t", "v1", "1g", 4), 2),)),
+             1: _fake_result(True, 0.4, 3, ((("t", "v0", "1g", 1), 1),)),
+             2: _fake_result(True, 0.5, 7, ((("t", "v0", "2g", 4), 2),)),
+             3: _fake_result(False, 0.0, 0, ())}[rank]
+    N.context = lambda device=None: "ctx"
+    N.set_shard = lambda ctx, r, w: seen.setdefault("shards", []).append((r, w))
+    planner.plan_batch = lambda app, prof, reqs, opt=None, device=None: [local]
+    res = shard.plan_sharded(None, None, None)
+    q.put((rank, seen["shards"], res.objective, res.config.total_slices, res.config.m))
+    dist.destroy_process_group()
+
+
+def test_gloo_four_rank_plan_sharded_combine():
+    """plan_sharded: each rank sweeps its shard, one all-gather, the reference
+    tie-break (objective, slices, m) on every rank; an infeasible shard never wins."""
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29500 + random.Random().randrange(2000, 4000)
+    procs = [ctx.Process(target=_gloo_plan_sharded_worker, args=(r, 4, port, q)) for r in range(4)]
+    for p in procs:
+        p.start()
+    outs = sorted(q.get(timeout=180) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, shards, obj, sl, m in outs:
+        assert shards == [(rank, 4), (0, 1)]  # set for the solve, reset afterwards
+        assert (obj, sl) == (0.5, 7)
+        assert m == ((("t", "v0", "2g", 4), 2),)  # the smaller m of the two ties
+
+
+def test_profile_csv_byte_identical_to_reference(tmp_path):
+    """Profile ingestion: our save_profile writes the reference's
+    bytes (digests from tools/make_golden_profiles.py) and load_profile reads them back."""
+    import hashlib
+
+    from golden_io import load
+
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.profiles import load_profile, profile_to_rows, save_profile
+
+    for name, doc in load("profile_csv.json").items():
+        _app, table = workloads.bundled(name)
+        p = tmp_path / f"{name}.csv"
+        save_profile(table, p)
+        data = p.read_bytes()
+        assert hashlib.sha256(data).hexdigest() == doc["sha256"], name
+        assert profile_to_rows(load_profile(p)) == profile_to_rows(table)
