@@ -1104,8 +1104,8 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     int glog = 0;
     while ((1 << glog) < x.R && glog < 5) ++glog;
     x.glog = glog;
-    // ~32k candidates per block so the TMA staging of the sink pool is amortised
-    // ~1M candidates per block amortise the sink-pool staging and the block prologue
+    // chunks of ~1M candidates: persistent blocks take them from a counter, the
+    // block's warps take the chunk's rounds from a shared counter
     x.rounds = (int)std::max<long long>(1, (1LL << 20) / ((long long)(XBLOCK / 32) * x_slots(p.P) * x.R));
     cand += x.nq * x.R;
     max_pn_last = std::max(max_pn_last, x.pn[T - 1]);
@@ -1113,7 +1113,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     ++nx;
   }
   if (nx == 0) return JSV_OK;
-  // keep >= 4 blocks per SM when the batch is small
+  // keep >= 16 chunks per SM for the persistent blocks' balance when the batch is small
   for (int it = 0; it < 16; ++it) {
     nb = 0;
     bool can = false;
@@ -1125,24 +1125,38 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
       can = can || xp[i].rounds > 1;
     }
     boff[n] = nb;
-    if (nb >= 148 * 4 || !can) break;
+    if (nb >= 148 * 8 || !can) break;
     for (int i = 0; i < n; ++i)
       if (xp[i].rounds > 1) xp[i].rounds = (xp[i].rounds + 1) / 2;
   }
   c.stats.exh_candidates += cand;
   c.stats.exh_probes += nx;
+  // register records need whole-warp prefix groups (every sink pool >= 32) and <= 512 bundles;
+  // each probe sweeps ceil(pool / 32) records per lane
+  int reg = 0;
+  if (p.P <= 4 && max_pn_last <= 512 && bs.s1.S < 0x7FFF) {
+    reg = 1;
+    for (int i = 0; i < n; ++i)
+      if (xp[i].rounds > 0 && xp[i].glog < 5) reg = 0;
+  }
+  if (getenv("JSV_NO_RPL")) reg = 0;
+  for (int i = 0; i < n; ++i)
+    if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
   CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
   CK(B[B_XBOFF].ensure(sizeof(long long) * (n + 1)));
   CK(B[B_XPART].ensure(sizeof(XPart) * std::max<long long>(1, nb)));
   CK(cudaMemcpyAsync(B[B_XPROBE].p, xp.data(), sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(B[B_XBOFF].p, boff.data(), sizeof(long long) * (n + 1),
                      cudaMemcpyHostToDevice, st));
-  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
-  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
+  // active flags [n] + the persistent kernel's chunk counter (8-byte aligned)
+  const size_t work_off = ((sizeof(int) * n + 7) / 8) * 8;
+  CK(B[B_ACTIVE].ensure(work_off + sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, work_off + sizeof(unsigned long long), st));
   XArgs a;
   memset(&a, 0, sizeof(a));
   s2_base(p, bs, a.s);
   a.s.active = B[B_ACTIVE].as<int>();
+  a.work = reinterpret_cast<unsigned long long*>(static_cast<char*>(B[B_ACTIVE].p) + work_off);
   const bool fonly = bs.feasible_only != 0;
   a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
   a.xp = B[B_XPROBE].as<XProbe>();
@@ -1159,15 +1173,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     a.lat2_max = 2.0 * mx;
   }
   a.max_pn_last = max_pn_last;
-  // register records need whole-warp prefix groups (every sink pool >= 32) and <= 512 bundles
-  a.rpl = 0;
-  if (p.P <= 4 && max_pn_last <= 512 && bs.s1.S < 0x7FFF) {
-    bool all32 = true;
-    for (int i = 0; i < n; ++i)
-      if (xp[i].rounds > 0 && xp[i].glog < 5) all32 = false;
-    if (all32) a.rpl = ((max_pn_last + 127) / 128) * 4;
-  }
-  if (getenv("JSV_NO_RPL")) a.rpl = 0;
+  a.rpl = reg;
   if (a.fast) {
     CK(B[B_XSACC].ensure(sizeof(double) * (size_t)n * W));
     CK(B[B_XSCAP].ensure(sizeof(double) * (size_t)n * W));

@@ -163,6 +163,7 @@ struct XWarpState {
   // verdict iff rank(cap) >= a_cap, rank(acc) >= a_acc, rank(2L) < l_lat (then
   // the exact latency test if t > lo) and slices <= rem
   uint4 th[NS];
+  uint2 sw[NS];           // the same thresholds as the SWAR subtrahends of the packed records
   double s0[PM][NS];      // path through the sink: Neumaier f; other path: frac * product
   double s1[PM][NS];      // path through the sink: Neumaier c
   double s2[PM][NS];      // path through the sink: accuracy product before the sink
@@ -203,11 +204,11 @@ __device__ __forceinline__ int x_first(int n, F pred) {
 // involve the sink, and the per-path partial latency sums / accuracy products;
 // in rank space also the sink-verdict thresholds.
 template <int PM, int NS, bool RANK>
-__device__ __forceinline__ void x_prefix(const S2Args& s, const XProbe& xp, const DProbe& pr,
-                                         int probe, long long qp, const double* frac, int slot,
+__device__ __forceinline__ void x_prefix(const S2Args& s, const DGraph& g, const XProbe& xp,
+                                         const DProbe& pr, int probe, long long qp,
+                                         const double* frac, unsigned thru, int slot,
                                          double lat2_max, const XRankView& rv,
                                          XWarpState<PM, NS>& ws) {
-  const DGraph& g = *s.g;
   const DReq& rq = *s.rq;
   const int T = s.T, P = g.P, tl = g.topo[T - 1], jb = probe * T;
   uint16_t ch[MAXT];
@@ -268,7 +269,7 @@ __device__ __forceinline__ void x_prefix(const S2Args& s, const XProbe& xp, cons
     if (p < P) {
       PySum ps;
       double prod = 1.0;
-      const bool through = (g.path_mask[p] >> tl) & 1u;
+      const bool through = (thru >> p) & 1u;
       for (int k = g.path_off[p]; k < g.path_off[p + 1]; ++k) {
         const int u = g.path_task[k];
         if (u == tl) break;  // the sink ends every path through it
@@ -299,37 +300,86 @@ __device__ __forceinline__ void x_prefix(const S2Args& s, const XProbe& xp, cons
   }
   const double need = dem[tl] * sf;
   if (RANK) {
-    // capacity: cap - need >= 0 <=> cap >= need (finite) <=> rank(cap) >= #{caps < need}
-    const int a_cap = x_first(rv.n, [&](int k) { return rv.scap[k] >= need; });
-    // accuracy: W is non-decreasing in the sink accuracy (fractions, products >= 0)
-    const int a_acc = x_first(rv.n, [&](int k) {
-      const double acc = rv.sacc[k];
-      double W = 0.0;
-#pragma unroll
-      for (int p = 0; p < PM; ++p)
-        if (p < P) W += ((g.path_mask[p] >> tl) & 1u) ? frac[p] * (pp[p] * acc) : px[p];
-      return x_acc_ok(W, pr, g.a_max);
-    });
-    // latency: the exact compensated sum differs from t = fl(f + 2L) by at most
-    // 1.01 (|c| + 2^-52 (f + 2L)); with M = 4x that (+ the rounding of slo -/+ M)
-    // t <= slo - M passes, t > slo + M fails, in between the exact sum decides
+    // Every sink verdict is monotone in one sorted column; the thresholds are
+    // found by lockstep binary lifting (first k in [0, n] whose predicate holds,
+    // the same count as a bisection), the searches interleaved for latency.
+    //  capacity: cap - need >= 0 <=> cap >= need (finite) <=> rank(cap) >= #{caps < need}
+    //  accuracy: W is non-decreasing in the sink accuracy (fractions, products >= 0)
+    //  latency: the exact compensated sum differs from t = fl(f + 2L) by at most
+    //    1.01 (|c| + 2^-52 (f + 2L)); with M = 4x that (+ the rounding of slo -/+ M)
+    //    t <= slo - M passes, t > slo + M fails, in between the exact sum decides
     const double slo = pr.slo_eff;
-    int l_lat = ok_pre ? rv.n : 0;
+    const bool thr_ok = pr.acc_thr_ok != 0;
+    const double acc_thr = pr.acc_thr, acc_slo = pr.acc_slo, a_max = g.a_max;
+    double hi[PM];
+    int pl[PM];
 #pragma unroll
     for (int p = 0; p < PM; ++p) {
-      if (p < P && ((g.path_mask[p] >> tl) & 1u)) {
+      pl[p] = 0;
+      hi[p] = 0.0;
+      if ((thru >> p) & 1u) {
         const double M = 4.0 * (fabs(c[p]) + 2.220446049250313e-16 * (f[p] + lat2_max + fabs(slo))) +
                          1e-300;
-        const double hi = slo + M, fp = f[p];
+        hi[p] = slo + M;
         ws.lo[p][slot] = slo - M;
-        const int l = x_first(rv.n, [&](int k) { return !(fp + rv.slat2[k] <= hi); });
-        l_lat = l < l_lat ? l : l_lat;
       }
     }
+    // binary lifting with the probe index clamped to n - 1 (a clamped probe repeats
+    // the last predicate, which keeps every sequence monotone), result clamped to n
+    const int n = rv.n, nm1 = n - 1;
+    const int top = n > 0 ? (1 << (31 - __clz(n))) : 0;
+    int pc = 0, pa = 0;
+    const double* __restrict__ scap = rv.scap;
+    const double* __restrict__ sacc = rv.sacc;
+    const double* __restrict__ slat = rv.slat2;
+    if (thr_ok) {
+      for (int step = top; step > 0; step >>= 1) {
+        pc += (scap[min(pc + step - 1, nm1)] >= need) ? 0 : step;
+        const double acc = sacc[min(pa + step - 1, nm1)];
+        double W = 0.0;
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          if (p < P) W += ((thru >> p) & 1u) ? frac[p] * (pp[p] * acc) : px[p];
+        pa += (W >= acc_thr) ? 0 : step;
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          if ((thru >> p) & 1u) pl[p] += (f[p] + slat[min(pl[p] + step - 1, nm1)] <= hi[p]) ? step : 0;
+      }
+    } else {
+      for (int step = top; step > 0; step >>= 1) {
+        pc += (scap[min(pc + step - 1, nm1)] >= need) ? 0 : step;
+        const double acc = sacc[min(pa + step - 1, nm1)];
+        double W = 0.0;
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          if (p < P) W += ((thru >> p) & 1u) ? frac[p] * (pp[p] * acc) : px[p];
+        pa += (W / a_max - acc_slo >= 0) ? 0 : step;
+#pragma unroll
+        for (int p = 0; p < PM; ++p)
+          if ((thru >> p) & 1u) pl[p] += (f[p] + slat[min(pl[p] + step - 1, nm1)] <= hi[p]) ? step : 0;
+      }
+    }
+    pc = min(pc, n);
+    pa = min(pa, n);
+#pragma unroll
+    for (int p = 0; p < PM; ++p) pl[p] = min(pl[p], n);
+    int l_lat = ok_pre ? n : 0;
+#pragma unroll
+    for (int p = 0; p < PM; ++p)
+      if ((thru >> p) & 1u) l_lat = pl[p] < l_lat ? pl[p] : l_lat;
     // resources: float(S - total) >= 0 <=> slices <= S - prefix; negative fails all
     const int rem = rq.S - sl_pre;
-    ws.th[slot] = make_uint4((unsigned)a_cap, (unsigned)a_acc, rem >= 0 ? (unsigned)l_lat : 0u,
-                             rem >= 0 ? (unsigned)rem : 0u);
+    const uint4 th = make_uint4((unsigned)pc, (unsigned)pa, rem >= 0 ? (unsigned)l_lat : 0u,
+                                rem >= 0 ? (unsigned)rem : 0u);
+    ws.th[slot] = th;
+    // SWAR: two 15-bit fields per word, all "x >= threshold" with a guard bit;
+    // (w | H) - B keeps bit 15 of a field iff that field passes
+    const unsigned rm = th.w < 0x7FFFu ? th.w : 0x7FFFu;
+    // (a slot that is not swept -- not a leaf prefix, or sink demand 0 -- gets
+    // l_lat = 0, which no record passes: rank(2L) field 0x7FFF - r never reaches 0x8000)
+    const bool swept = valid && dem[tl] != 0.0;
+    ws.sw[slot] = make_uint2((th.x << 16) | th.y,
+                             ((0x8000u - (swept ? th.z : 0u)) << 16) | (0x7FFFu - rm));
   }
   ws.need[slot] = need;
   ws.sl[slot] = sl_pre;
@@ -405,98 +455,209 @@ __device__ __forceinline__ bool x_take(const XArgs& a, int probe, int tl, long l
 
 constexpr int XU = 4;  // candidates per lane and iteration in rank space (independent chains)
 
-template <int PM, bool RANK, int RPL>
-__global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
+// Block-invariant context of the rare feasible path of the register sweep.
+template <int PM>
+struct XCtx {
+  const XArgs* a;
+  const XProbe* xp;
+  int probe, tl, P;
+  long long q, R;
+  double slo, a_max, alpha, beta;
+  unsigned thru;
+  double frac[PM];
+};
+
+// Register sweep, feasible records of prefix slot j: `mask` bit k = record
+// lane + 32 k passed the four rank compares.  Exact latency step where t is
+// within the margin, then the exact objective and the (obj, slices, m) fold
+// (kept out of line: ~2% of the (lane, prefix) pairs reach it).
+template <int PM, int NS>
+__device__ __noinline__ void x_slow_reg(const XCtx<PM>& cx, const XWarpState<PM, NS>& ws, int j,
+                                        unsigned mask, XBest& best) {
+  const XArgs& a = *cx.a;
+  const S2Args& s = a.s;
+  const int lane = threadIdx.x & 31;
+  const long long qp = ws.q[j];
+  const int sl_pre = ws.sl[j];
+  const bool later = (ws.flags[j] & 4) != 0;
+  double f[PM], c[PM], pp[PM], lo[PM];
+#pragma unroll
+  for (int p = 0; p < PM; ++p) {
+    f[p] = ws.s0[p][j];
+    c[p] = ws.s1[p][j];
+    pp[p] = ws.s2[p][j];
+    lo[p] = ws.lo[p][j];
+  }
+  XBest rb;
+  rb.has = 0; rb.sl = 0; rb.obj = 0.0; rb.idx = 0;
+  while (mask) {
+    const int k = __ffs(mask) - 1;
+    mask &= mask - 1;
+    const int b = lane + 32 * k;
+    const double lat2 = 2.0 * s.p_lat[cx.q + b];
+    // t within the margin of the SLO: CPython 3.12 sum() step exactly
+    bool lat_ok = true;
+#pragma unroll
+    for (int p = 0; p < PM; ++p) {
+      if ((cx.thru >> p) & 1u) {
+        const double t = f[p] + lat2;
+        if (t <= lo[p]) continue;
+        const bool fb = fabs(f[p]) >= fabs(lat2);
+        const double big = fb ? f[p] : lat2, small = fb ? lat2 : f[p];
+        const double cc = c[p] + ((big - t) + small);
+        lat_ok &= (t + cc <= cx.slo);  // c finite and +0 when zero (RANK problems)
+      }
+    }
+    if (!lat_ok) continue;
+    if (x_take<PM>(a, cx.probe, cx.tl, qp, cx.R, b, s.p_acc[cx.q + b], sl_pre, (int)s.p_sl[cx.q + b],
+                   f, pp, cx.frac, cx.thru, cx.P, cx.alpha, cx.beta, cx.a_max, later, rb))
+      break;
+  }
+  if (rb.has && x_better(a, *cx.xp, cx.probe, rb, best)) best = rb;
+}
+
+// Register sweep, prefixes whose sink demand is 0 (bit j of zmask): the only
+// child is "no instances" (planner.py:868-875); lane 0 derives each leaf.
+template <int PM, int NS>
+__device__ __noinline__ unsigned x_zero_reg(const XCtx<PM>& cx, const DProbe& pr, int S,
+                                            const XWarpState<PM, NS>& ws, unsigned zmask,
+                                            XBest& best) {
+  const XArgs& a = *cx.a;
+  unsigned n = 0;
+  while (zmask) {
+    const int j = __ffs(zmask) - 1;
+    zmask &= zmask - 1;
+    ++n;
+    double f[PM], c[PM], pp[PM];
+#pragma unroll
+    for (int p = 0; p < PM; ++p) {
+      f[p] = ws.s0[p][j];
+      c[p] = ws.s1[p][j];
+      pp[p] = ws.s2[p][j];
+    }
+    const int fl = ws.flags[j];
+    XBest rb;
+    rb.has = 0; rb.sl = 0; rb.obj = 0.0; rb.idx = 0;
+    if (x_sink_eval<PM, true>(0.0, 0.0, 1.0, 0, ws.need[j], ws.sl[j], (fl & 2) != 0, f, c, pp,
+                              cx.frac, cx.thru, cx.P, cx.slo, S, pr, cx.a_max))
+      x_take<PM>(a, cx.probe, cx.tl, ws.q[j], cx.R, cx.xp->pn[a.s.T - 1], 1.0, ws.sl[j], 0, f, pp,
+                 cx.frac, cx.thru, cx.P, cx.alpha, cx.beta, cx.a_max, (fl & 4) != 0, rb);
+    if (rb.has && x_better(a, *cx.xp, cx.probe, rb, best)) best = rb;
+  }
+  return n;
+}
+
+#define X_H 0x80008000u
+// guard bits of record r against SWAR subtrahends B: X_H iff all four verdicts pass
+#define X_V(r, B) (((r).x - (B).x) & ((r).y - (B).y) & X_H)
+
+// Register sweep of one round: every lane keeps records lane + 32 k (k < K =
+// ceil(pool / 32), the probe's count) of the sink pool in registers and tests
+// them against each leaf prefix of the warp (bit j of vmask), two prefixes per
+// iteration (independent max chains).  Per candidate: two IADD (often issued as
+// IMAD.IADD on the FMA pipe), one LOP3 and half a three-input VIMNMX.
+template <int PM, int NS, int K>
+__device__ __forceinline__ void x_sweep_k(const XCtx<PM>& cx, const uint2* __restrict__ pack,
+                                          const XWarpState<PM, NS>& ws, unsigned vmask,
+                                          XBest& best) {
+  const int lane = threadIdx.x & 31;
+  uint2 rec[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) rec[k] = pack[lane + 32 * k];
+  while (vmask) {
+    const int j0 = __ffs(vmask) - 1;
+    vmask &= vmask - 1;
+    const int j1 = vmask ? __ffs(vmask) - 1 : j0;
+    vmask &= vmask - 1;
+    const uint2 b0 = ws.sw[j0], b1 = ws.sw[j1];
+    unsigned m0 = 0u, m1 = 0u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      m0 = max(m0, X_V(rec[k], b0));
+      m1 = max(m1, X_V(rec[k], b1));
+    }
+    if (m0 == X_H) {
+      unsigned mask = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) mask |= (X_V(rec[k], b0) == X_H ? 1u : 0u) << k;
+      x_slow_reg<PM, NS>(cx, ws, j0, mask, best);
+    }
+    if (m1 == X_H && j1 != j0) {
+      unsigned mask = 0;
+#pragma unroll
+      for (int k = 0; k < K; ++k) mask |= (X_V(rec[k], b1) == X_H ? 1u : 0u) << k;
+      x_slow_reg<PM, NS>(cx, ws, j1, mask, best);
+    }
+  }
+}
+
+template <int PM, int NS>
+__device__ __forceinline__ void x_sweep_reg(const XCtx<PM>& cx, const uint2* __restrict__ pack,
+                                            const XWarpState<PM, NS>& ws, unsigned vmask, int rpl,
+                                            XBest& best) {
+  switch (rpl) {
+#define JSV_XSW(K) \
+  case K: x_sweep_k<PM, NS, K>(cx, pack, ws, vmask, best); break;
+    JSV_XSW(1) JSV_XSW(2) JSV_XSW(3) JSV_XSW(4) JSV_XSW(5) JSV_XSW(6) JSV_XSW(7) JSV_XSW(8)
+    JSV_XSW(9) JSV_XSW(10) JSV_XSW(11) JSV_XSW(12) JSV_XSW(13) JSV_XSW(14) JSV_XSW(15) JSV_XSW(16)
+#undef JSV_XSW
+    default: break;
+  }
+}
+
+// Persistent blocks (one per resident slot of the SMs) take chunks -- a
+// contiguous prefix range of one probe -- from a device-wide counter, in
+// increasing order, so every block sees the probes in order.  The sink pool of
+// a probe is staged into shared memory when a block's chunk changes probe; the
+// block's best of a probe segment is reduced and written into the XPart of the
+// segment's last chunk (other chunks get empty parts).
+template <int PM, bool RANK, bool REG>
+__global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
+    k_s2_exh(const __grid_constant__ XArgs a) {
   constexpr int NS = x_slots(PM);
   using WS = XWarpState<PM, NS>;
   extern __shared__ __align__(16) unsigned char x_smem[];
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ XBest s_warp[XBLOCK / 32];
   __shared__ unsigned long long s_leaves;
+  __shared__ long long s_chunk;
+  __shared__ int s_round;  // next round of the chunk (warps take rounds dynamically)
+  __shared__ __align__(16) DGraph s_g;  // the graph, read by every prefix derivation
   const S2Args& s = a.s;
-  const DGraph& g = *s.g;
+  {
+    const int2* src = reinterpret_cast<const int2*>(s.g);
+    int2* dst = reinterpret_cast<int2*>(&s_g);
+    for (int i = threadIdx.x; i < (int)(sizeof(DGraph) / 8); i += blockDim.x) dst[i] = src[i];
+    static_assert(sizeof(DGraph) % 8 == 0, "DGraph copy granularity");
+  }
+  if (threadIdx.x == 0) {
+    s_leaves = 0;
+    if (RANK && a.tma) mbar_init(&s_bar, 1);
+  }
+  __syncthreads();
+  const DGraph& g = s_g;
   const int T = s.T, P = g.P;
-  const long long blk = blockIdx.x;
-  const int probe = find_probe(a.boff, s.n_probes, blk);
-  const XProbe& xp = a.xp[probe];
-  const DProbe& pr = s.probes[probe];
   const int tl = g.topo[T - 1];
-  const int pn = xp.pn[T - 1];
-  const long long q = (long long)(probe * T + tl) * s.W;
-  // records are padded up to the register sweep of the batch's largest pool
-  const int npad = x_pad(pn) > 32 * RPL ? x_pad(pn) : 32 * RPL;
-
-  // ---- stage the sink task's pool in shared memory (TMA bulk copies + mbarrier)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int max_np = x_pad(a.max_pn_last);  // shared-memory layout is fixed for the launch
   XRankView rv;
-  rv.n = pn;
   double2* s_lc = nullptr;  // float: (2 L, capacity)
   double2* s_as = nullptr;  // float: (accuracy, slices)
   unsigned char* tail;
   if (RANK) {
     uint4* s_rank = reinterpret_cast<uint4*>(x_smem);
-    double* s_scap = reinterpret_cast<double*>(s_rank + npad);
-    double* s_sacc = s_scap + npad;
-    double* s_slat = s_sacc + npad;
-    uint2* s_pack = reinterpret_cast<uint2*>(s_slat + npad);
-    tail = reinterpret_cast<unsigned char*>(s_pack + npad);
+    double* s_scap = reinterpret_cast<double*>(s_rank + max_np);
+    double* s_sacc = s_scap + max_np;
+    double* s_slat = s_sacc + max_np;
+    uint2* s_pack = reinterpret_cast<uint2*>(s_slat + max_np);
+    tail = reinterpret_cast<unsigned char*>(s_pack + max_np);
     rv.rank = s_rank; rv.scap = s_scap; rv.sacc = s_sacc; rv.slat2 = s_slat; rv.pack = s_pack;
-    const long long o = (long long)probe * s.W;
-    if (a.tma && pn > 0) {
-      const unsigned b16 = (unsigned)pn * 16u, b8 = (unsigned)((pn * 8 + 15) & ~15);
-      if (threadIdx.x == 0) {
-        mbar_init(&s_bar, 1);
-        mbar_expect_tx(&s_bar, b16 + 4 * b8);
-        bulk_g2s(s_rank, a.xrank + o, b16, &s_bar);
-        bulk_g2s(s_pack, a.xpack + o, b8, &s_bar);
-        bulk_g2s(s_scap, a.scap + o, b8, &s_bar);
-        bulk_g2s(s_sacc, a.sacc + o, b8, &s_bar);
-        bulk_g2s(s_slat, a.slat2 + o, b8, &s_bar);
-      }
-    } else {
-      for (int i = threadIdx.x; i < pn; i += blockDim.x) {
-        s_rank[i] = a.xrank[o + i];
-        s_scap[i] = a.scap[o + i];
-        s_sacc[i] = a.sacc[o + i];
-        s_slat[i] = a.slat2[o + i];
-        s_pack[i] = a.xpack[o + i];
-      }
-    }
-    __syncthreads();
-    if (a.tma && pn > 0) mbar_wait(&s_bar, 0);
-    // padding records always fail (rank(2L) = max) so the sweep needs no bound test;
-    // written after the copies land (the bulk sizes round up to 16 bytes)
-    for (int i = pn + threadIdx.x; i < npad; i += blockDim.x) {
-      s_rank[i] = make_uint4(0u, 0u, 0xFFFFFFFFu, 0xFFFFFFFFu);
-      s_pack[i] = make_uint2(0x80008000u, 0x80008000u);  // rank(2L) field 0x7FFF fails
-    }
   } else {
     s_lc = reinterpret_cast<double2*>(x_smem);
-    s_as = s_lc + npad;
-    tail = reinterpret_cast<unsigned char*>(s_as + npad);
-    for (int i = threadIdx.x; i < pn; i += blockDim.x) {
-      s_lc[i] = make_double2(2.0 * s.p_lat[q + i], s.p_cap[q + i]);
-      s_as[i] = make_double2(s.p_acc[q + i], __longlong_as_double((long long)(unsigned)s.p_sl[q + i]));
-    }
+    s_as = s_lc + max_np;
+    tail = reinterpret_cast<unsigned char*>(s_as + max_np);
   }
-  WS* s_ws = reinterpret_cast<WS*>(tail);
-  if (threadIdx.x == 0) s_leaves = 0;
-  __syncthreads();
-
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  WS& ws = s_ws[wid];
-  const int glog = xp.glog, G = 1 << glog;
-  const int gw = 32 >> glog;  // prefix groups per warp
-  const int gi = lane >> glog, lane_g = lane & (G - 1);
-  const long long per_round = (long long)(XBLOCK / 32) * NS;
-  const long long qbase = (blk - a.boff[probe]) * per_round * xp.rounds;
-  XBest best;
-  best.has = 0; best.sl = 0; best.obj = 0.0; best.idx = 0;
-  unsigned long long leaves = 0;
-  volatile int* found = s.active;
-  const double slo = pr.slo_eff, a_max = g.a_max;
-  const double alpha = pr.alpha, beta = pr.beta;
-  const int S = s.rq->S;
-  const long long R = xp.R;
+  WS& ws = reinterpret_cast<WS*>(tail)[wid];
   double frac[PM];
   unsigned thru = 0;
 #pragma unroll
@@ -504,197 +665,261 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_exh(XArgs a) {
     frac[p] = (p < P) ? g.path_frac[p] : 0.0;
     if (p < P && ((g.path_mask[p] >> tl) & 1u)) thru |= 1u << p;
   }
+  const int S = s.rq->S;
+  volatile int* found = s.active;
+  const long long nb = a.boff[s.n_probes];
+  const long long per_round = (long long)(XBLOCK / 32) * NS;
 
-  for (int rd = 0; rd < xp.rounds; ++rd) {
-    const long long qw = qbase + ((long long)rd * (XBLOCK / 32) + wid) * NS;
-    if (qw >= xp.nq) break;  // warp-uniform
-    if (a.mode == LEAF_ANY && __shfl_sync(0xffffffffu, lane == 0 ? found[probe] : 0, 0)) break;
-    // ---- one prefix per lane -> shared memory
-    if (lane < NS) {
-      const long long qi = qw + lane;
-      if (qi < xp.nq)
-        x_prefix<PM, NS, RANK>(s, xp, pr, probe, xp.q0 + qi, frac, lane, a.lat2_max, rv, ws);
-      else
-        ws.flags[lane] = 0;
-    }
-    __syncwarp();
-    // rank space, pools of >= 32 bundles: each lane keeps records lane + 32 k in
-    // registers for the whole round and tests them against every prefix
-    uint2 rec[RPL > 0 ? RPL : 1];
+  int probe = -1;
+  unsigned stage_phase = 0;
+  long long last_chunk = -1;
+  XBest best;
+  best.has = 0; best.sl = 0; best.obj = 0.0; best.idx = 0;
+  unsigned long long leaves = 0;
+
+  // block reduction of the current probe segment into part[last_chunk]
+  auto flush = [&]() {
+    const XProbe& xp = a.xp[probe];
+    if (a.mode == LEAF_ANY && best.has) found[probe] = 1;
 #pragma unroll
-    for (int k = 0; k < RPL; ++k) rec[k] = rv.pack[lane + 32 * k];
-    // ---- groups of G lanes sweep the sink pool for each prefix
-    unsigned nswept = 0;  // RPL sweeps: valid prefixes swept by the whole warp this round
-    for (int j = gi; j < NS; j += gw) {
-      const int fl = ws.flags[j];
-      if (!(fl & 1)) continue;  // not a leaf prefix (group-uniform)
-      // prefix state, read from shared memory where a path needs it
-      long long qp;
-      double need;
-      int sl_pre;
-      bool ok_pre, later;
-      double f[PM], c[PM], pp[PM];
-      auto load_state = [&]() {
-        qp = ws.q[j];
-        need = ws.need[j];
-        sl_pre = ws.sl[j];
-        ok_pre = (fl & 2) != 0;
-        later = (fl & 4) != 0;
+    for (int d = 16; d > 0; d >>= 1) {
+      const XBest o = x_shfl_down(best, d);
+      if (x_better(a, xp, probe, o, best)) best = o;
+    }
+    for (int d = 16; d > 0; d >>= 1) leaves += __shfl_down_sync(0xffffffffu, leaves, d);
+    if (lane == 0) {
+      s_warp[wid] = best;
+      atomicAdd(&s_leaves, leaves);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      XBest b = s_warp[0];
+      for (int w = 1; w < XBLOCK / 32; ++w)
+        if (x_better(a, xp, probe, s_warp[w], b)) b = s_warp[w];
+      XPart& o = a.part[last_chunk];
+      o.has = b.has; o.sl = b.sl; o.obj = b.obj; o.idx = b.idx; o.leaves = s_leaves;
+      s_leaves = 0;
+    }
+    best.has = 0; best.sl = 0; best.obj = 0.0; best.idx = 0;
+    leaves = 0;
+  };
+
+  while (true) {
+    if (threadIdx.x == 0) {
+      s_chunk = (long long)atomicAdd(a.work, 1ull);
+      s_round = 0;
+    }
+    __syncthreads();
+    const long long chunk = s_chunk;
+    const int cp = chunk < nb ? find_probe(a.boff, s.n_probes, chunk) : -1;
+    if (cp != probe) {
+      if (probe >= 0) flush();  // (ends with the block barrier inside)
+      if (cp < 0) break;
+      probe = cp;
+      // ---- stage the sink task's pool in shared memory (TMA bulk copies + mbarrier)
+      const int pn = a.xp[probe].pn[T - 1];
+      const int npad = x_pad(pn);
+      const long long q = (long long)(probe * T + tl) * s.W;
+      rv.n = pn;
+      if (RANK) {
+        const long long o = (long long)probe * s.W;
+        uint4* s_rank = const_cast<uint4*>(rv.rank);
+        uint2* s_pack = const_cast<uint2*>(rv.pack);
+        double* s_scap = const_cast<double*>(rv.scap);
+        double* s_sacc = const_cast<double*>(rv.sacc);
+        double* s_slat = const_cast<double*>(rv.slat2);
+        if (a.tma && pn > 0) {
+          const unsigned b16 = (unsigned)pn * 16u, b8 = (unsigned)((pn * 8 + 15) & ~15);
+          if (threadIdx.x == 0) {
+            mbar_expect_tx(&s_bar, b16 + 4 * b8);
+            bulk_g2s(s_rank, a.xrank + o, b16, &s_bar);
+            bulk_g2s(s_pack, a.xpack + o, b8, &s_bar);
+            bulk_g2s(s_scap, a.scap + o, b8, &s_bar);
+            bulk_g2s(s_sacc, a.sacc + o, b8, &s_bar);
+            bulk_g2s(s_slat, a.slat2 + o, b8, &s_bar);
+          }
+          mbar_wait(&s_bar, stage_phase);
+          stage_phase ^= 1u;
+        } else {
+          for (int i = threadIdx.x; i < pn; i += blockDim.x) {
+            s_rank[i] = a.xrank[o + i];
+            s_scap[i] = a.scap[o + i];
+            s_sacc[i] = a.sacc[o + i];
+            s_slat[i] = a.slat2[o + i];
+            s_pack[i] = a.xpack[o + i];
+          }
+        }
+        __syncthreads();
+        // padding records always fail (rank(2L) = max) so the sweep needs no bound test;
+        // written after the copies land (the bulk sizes round up to 16 bytes)
+        for (int i = pn + threadIdx.x; i < npad; i += blockDim.x) {
+          s_rank[i] = make_uint4(0u, 0u, 0xFFFFFFFFu, 0xFFFFFFFFu);
+          s_pack[i] = make_uint2(0x80008000u, 0x80008000u);  // rank(2L) field 0x7FFF fails
+        }
+      } else {
+        for (int i = threadIdx.x; i < pn; i += blockDim.x) {
+          s_lc[i] = make_double2(2.0 * s.p_lat[q + i], s.p_cap[q + i]);
+          s_as[i] = make_double2(s.p_acc[q + i],
+                                 __longlong_as_double((long long)(unsigned)s.p_sl[q + i]));
+        }
+      }
+      __syncthreads();
+    }
+    // chunks that do not end a segment carry an empty part
+    if (threadIdx.x == 0) {
+      XPart& o = a.part[chunk];
+      o.has = 0; o.sl = 0; o.obj = 0.0; o.idx = 0; o.leaves = 0;
+    }
+    last_chunk = chunk;
+
+    const XProbe& xp = a.xp[probe];
+    const DProbe& pr = s.probes[probe];
+    const int pn = xp.pn[T - 1];
+    const long long q = (long long)(probe * T + tl) * s.W;
+    const int glog = xp.glog, G = 1 << glog;
+    const int gw = 32 >> glog;  // prefix groups per warp
+    const int gi = lane >> glog, lane_g = lane & (G - 1);
+    const long long qbase = (chunk - a.boff[probe]) * per_round * xp.rounds;
+    const double slo = pr.slo_eff, a_max = g.a_max;
+    const double alpha = pr.alpha, beta = pr.beta;
+    const long long R = xp.R;
+    XCtx<PM> cx;
+    if (REG) {
+      cx.a = &a; cx.xp = &xp; cx.probe = probe; cx.tl = tl; cx.P = P; cx.q = q; cx.R = R;
+      cx.slo = slo; cx.a_max = a_max; cx.alpha = alpha; cx.beta = beta; cx.thru = thru;
+#pragma unroll
+      for (int p = 0; p < PM; ++p) cx.frac[p] = frac[p];
+    }
+    const int rpl = xp.rpl;
+    unsigned nswept = 0;  // register sweeps: leaf prefixes swept by the whole warp
+
+    // rounds of NS prefixes, taken by the warps from a block counter (balance)
+    while (true) {
+      int rd = 0;
+      if (lane == 0) rd = atomicAdd(&s_round, 1);
+      rd = __shfl_sync(0xffffffffu, rd, 0);
+      if (rd >= xp.rounds * (XBLOCK / 32)) break;
+      const long long qw = qbase + (long long)rd * NS;
+      if (qw >= xp.nq) break;  // warp-uniform
+      if (a.mode == LEAF_ANY && __shfl_sync(0xffffffffu, lane == 0 ? found[probe] : 0, 0)) break;
+      // ---- one prefix per lane -> shared memory
+      if (lane < NS) {
+        const long long qi = qw + lane;
+        if (qi < xp.nq)
+          x_prefix<PM, NS, RANK>(s, g, xp, pr, probe, xp.q0 + qi, frac, thru, lane, a.lat2_max, rv, ws);
+        else {
+          ws.flags[lane] = 0;
+          if (RANK) ws.sw[lane] = make_uint2(0u, 0x80000000u);  // fails every record
+        }
+      }
+      __syncwarp();
+      if constexpr (RANK && REG && NS == 32) {
+        // NS == 32 here: lane j derived prefix j
+        const int myfl = ws.flags[lane];
+        const unsigned vmask = __ballot_sync(0xffffffffu, (myfl & 9) == 1);
+        const unsigned zmask = __ballot_sync(0xffffffffu, (myfl & 9) == 9);
+        nswept += (unsigned)__popc(vmask);
+        x_sweep_reg<PM, NS>(cx, rv.pack, ws, vmask, rpl, best);
+        // sink demand 0: the only child is "no instances" (planner.py:868-875)
+        if (zmask && lane == 0) leaves += x_zero_reg<PM, NS>(cx, pr, S, ws, zmask, best);
+        __syncwarp();
+        continue;
+      }
+      // ---- groups of G lanes sweep the sink pool for each prefix
+      for (int j = gi; j < NS; j += gw) {
+        const int fl = ws.flags[j];
+        if (!(fl & 1)) continue;  // not a leaf prefix (group-uniform)
+        // prefix state, read from shared memory
+        const long long qp = ws.q[j];
+        const double need = ws.need[j];
+        const int sl_pre = ws.sl[j];
+        const bool ok_pre = (fl & 2) != 0, later = (fl & 4) != 0;
+        double f[PM], c[PM], pp[PM];
 #pragma unroll
         for (int p = 0; p < PM; ++p) {
           f[p] = ws.s0[p][j];
           c[p] = ws.s1[p][j];
           pp[p] = ws.s2[p][j];
         }
-      };
-      XBest rb;
-      rb.has = 0; rb.sl = 0; rb.obj = 0.0; rb.idx = 0;
-      if (!(RANK && RPL > 0) || (fl & 8)) load_state();
-      if (fl & 8) {
-        // sink demand 0: its only child is "no instances" (planner.py:868-875)
-        if (lane_g == 0) {
-          ++leaves;
-          if (x_sink_eval<PM, RANK>(0.0, 0.0, 1.0, 0, need, sl_pre, ok_pre, f, c, pp, frac, thru,
-                                    P, slo, S, pr, a_max))
-            x_take<PM>(a, probe, tl, qp, R, pn, 1.0, sl_pre, 0, f, pp, frac, thru, P, alpha, beta,
-                       a_max, later, rb);
-        }
-      } else if (RANK && RPL > 0) {
-        ++nswept;
-        const uint4 th = ws.th[j];
-        // (a prefix whose own verdicts fail has th.z = 0: every record then fails the
-        // latency field, but its four sink compares are still evaluated)
-        // SWAR: two 15-bit fields per word, all "x >= threshold" with a guard bit;
-        // (w | H) - B keeps bit 15 of a field iff that field passes
-        const unsigned rem = th.w < 0x7FFFu ? th.w : 0x7FFFu;
-        const unsigned B0 = (th.x << 16) | th.y;
-        const unsigned B1 = ((0x8000u - th.z) << 16) | (0x7FFFu - rem);
-        // v = guard bits of both words: a record passes iff v == H, the largest value
-        // v can take, so one running max decides whether any of them passes
-        unsigned m = 0u;
-#pragma unroll
-        for (int k = 0; k < RPL; ++k) m = max(m, (rec[k].x - B0) & (rec[k].y - B1) & 0x80008000u);
-        unsigned mask = 0;
-        if (m == 0x80008000u) {
-#pragma unroll
-          for (int k = 0; k < RPL; ++k)
-            mask |= (((rec[k].x - B0) & (rec[k].y - B1) & 0x80008000u) == 0x80008000u ? 1u : 0u) << k;
-        }
-        if (mask) {
-          load_state();
+        XBest rb;
+        rb.has = 0; rb.sl = 0; rb.obj = 0.0; rb.idx = 0;
+        if (fl & 8) {
+          // sink demand 0: its only child is "no instances" (planner.py:868-875)
+          if (lane_g == 0) {
+            ++leaves;
+            if (x_sink_eval<PM, RANK>(0.0, 0.0, 1.0, 0, need, sl_pre, ok_pre, f, c, pp, frac, thru,
+                                      P, slo, S, pr, a_max))
+              x_take<PM>(a, probe, tl, qp, R, pn, 1.0, sl_pre, 0, f, pp, frac, thru, P, alpha, beta,
+                         a_max, later, rb);
+          }
+        } else if (RANK) {
+          if (lane_g < pn) leaves += (unsigned)((pn - lane_g + G - 1) >> glog);
+          const uint4 th = ws.th[j];
+          const unsigned a_cap = th.x, a_acc = th.y, l_lat = th.z, rem = th.w;
           double lo[PM];
 #pragma unroll
           for (int p = 0; p < PM; ++p) lo[p] = ws.lo[p][j];
-          while (mask) {
-            const int k = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const int b = lane + 32 * k;
-            const double lat2 = 2.0 * s.p_lat[q + b];
-            // t within the margin of the SLO: CPython 3.12 sum() step exactly
-            bool lat_ok = true;
+          // every verdict of every candidate: four integer compares on its record
+          for (int b0 = lane_g; b0 < pn; b0 += XU * G) {
+            bool ok[XU], any = false;
+            unsigned slv[XU];
 #pragma unroll
-            for (int p = 0; p < PM; ++p) {
-              if ((thru >> p) & 1u) {
-                const double t = f[p] + lat2;
-                if (t <= lo[p]) continue;
-                const bool fb = fabs(f[p]) >= fabs(lat2);
-                const double big = fb ? f[p] : lat2, small = fb ? lat2 : f[p];
-                const double cc = c[p] + ((big - t) + small);
-                lat_ok &= (t + cc <= slo);  // c finite and +0 when zero (RANK problems)
-              }
+            for (int u = 0; u < XU; ++u) {
+              const uint4 r = rv.rank[b0 + u * G];
+              ok[u] = (r.x >= a_cap) & (r.y >= a_acc) & (r.z < l_lat) & (r.w <= rem);
+              slv[u] = r.w;
+              any |= ok[u];
             }
-            if (!lat_ok) continue;
-            if (x_take<PM>(a, probe, tl, qp, R, b, s.p_acc[q + b], sl_pre, (int)s.p_sl[q + b], f, pp,
-                           frac, thru, P, alpha, beta, a_max, later, rb))
+            if (!any) continue;
+            bool stop = false;
+#pragma unroll
+            for (int u = 0; u < XU; ++u) {
+              if (stop || !ok[u]) continue;
+              const int b = b0 + u * G;
+              const double lat2 = 2.0 * s.p_lat[q + b];
+              // t within the margin of the SLO: CPython 3.12 sum() step exactly
+              bool lat_ok = true;
+#pragma unroll
+              for (int p = 0; p < PM; ++p) {
+                if ((thru >> p) & 1u) {
+                  const double t = f[p] + lat2;
+                  if (t <= lo[p]) continue;
+                  const bool fb = fabs(f[p]) >= fabs(lat2);
+                  const double big = fb ? f[p] : lat2, small = fb ? lat2 : f[p];
+                  const double cc = c[p] + ((big - t) + small);
+                  lat_ok &= (t + cc <= slo);  // c finite and +0 when zero (RANK problems)
+                }
+              }
+              if (!lat_ok) continue;
+              stop = x_take<PM>(a, probe, tl, qp, R, b, s.p_acc[q + b], sl_pre, (int)slv[u], f, pp,
+                                frac, thru, P, alpha, beta, a_max, later, rb);
+            }
+            if (stop) break;
+          }
+        } else {
+          if (lane_g < pn) leaves += (unsigned)((pn - lane_g + G - 1) >> glog);
+          for (int b = lane_g; b < pn; b += G) {
+            const double2 lc = s_lc[b], as = s_as[b];
+            const int sl = (int)(unsigned)__double_as_longlong(as.y);
+            if (!x_sink_eval<PM, false>(lc.x, lc.y, as.x, sl, need, sl_pre, ok_pre, f, c, pp, frac,
+                                        thru, P, slo, S, pr, a_max))
+              continue;
+            if (x_take<PM>(a, probe, tl, qp, R, b, as.x, sl_pre, sl, f, pp, frac, thru, P, alpha,
+                           beta, a_max, later, rb))
               break;
           }
         }
-      } else if (RANK) {
-        if (lane_g < pn) leaves += (unsigned)((pn - lane_g + G - 1) >> glog);
-        const uint4 th = ws.th[j];
-        const unsigned a_cap = th.x, a_acc = th.y, l_lat = th.z, rem = th.w;
-        double lo[PM];
-#pragma unroll
-        for (int p = 0; p < PM; ++p) lo[p] = ws.lo[p][j];
-        // every verdict of every candidate: four integer compares on its record
-        for (int b0 = lane_g; b0 < pn; b0 += XU * G) {
-          bool ok[XU], any = false;
-          unsigned slv[XU];
-#pragma unroll
-          for (int u = 0; u < XU; ++u) {
-            const uint4 r = rv.rank[b0 + u * G];
-            ok[u] = (r.x >= a_cap) & (r.y >= a_acc) & (r.z < l_lat) & (r.w <= rem);
-            slv[u] = r.w;
-            any |= ok[u];
-          }
-          if (!any) continue;
-          bool stop = false;
-#pragma unroll
-          for (int u = 0; u < XU; ++u) {
-            if (stop || !ok[u]) continue;
-            const int b = b0 + u * G;
-            const double lat2 = 2.0 * s.p_lat[q + b];
-            // t within the margin of the SLO: CPython 3.12 sum() step exactly
-            bool lat_ok = true;
-#pragma unroll
-            for (int p = 0; p < PM; ++p) {
-              if ((thru >> p) & 1u) {
-                const double t = f[p] + lat2;
-                if (t <= lo[p]) continue;
-                const bool fb = fabs(f[p]) >= fabs(lat2);
-                const double big = fb ? f[p] : lat2, small = fb ? lat2 : f[p];
-                const double cc = c[p] + ((big - t) + small);
-                lat_ok &= (t + cc <= slo);  // c finite and +0 when zero (RANK problems)
-              }
-            }
-            if (!lat_ok) continue;
-            stop = x_take<PM>(a, probe, tl, qp, R, b, s.p_acc[q + b], sl_pre, (int)slv[u], f, pp,
-                              frac, thru, P, alpha, beta, a_max, later, rb);
-          }
-          if (stop) break;
-        }
-      } else {
-        if (lane_g < pn) leaves += (unsigned)((pn - lane_g + G - 1) >> glog);
-        for (int b = lane_g; b < pn; b += G) {
-          const double2 lc = s_lc[b], as = s_as[b];
-          const int sl = (int)(unsigned)__double_as_longlong(as.y);
-          if (!x_sink_eval<PM, false>(lc.x, lc.y, as.x, sl, need, sl_pre, ok_pre, f, c, pp, frac,
-                                      thru, P, slo, S, pr, a_max))
-            continue;
-          if (x_take<PM>(a, probe, tl, qp, R, b, as.x, sl_pre, sl, f, pp, frac, thru, P, alpha, beta,
-                         a_max, later, rb))
-            break;
-        }
+        if (rb.has && x_better(a, xp, probe, rb, best)) best = rb;
       }
-      if (rb.has && x_better(a, xp, probe, rb, best)) best = rb;
+      __syncwarp();
     }
-    if (RANK && RPL > 0 && lane < pn) leaves += (unsigned long long)nswept * ((pn - lane + 31) >> 5);
-    __syncwarp();
-  }
-  if (a.mode == LEAF_ANY && best.has) found[probe] = 1;
-  // ---- reduction: warp shuffles, shared memory, block partial
-#pragma unroll
-  for (int d = 16; d > 0; d >>= 1) {
-    const XBest o = x_shfl_down(best, d);
-    if (x_better(a, xp, probe, o, best)) best = o;
-  }
-  for (int d = 16; d > 0; d >>= 1) leaves += __shfl_down_sync(0xffffffffu, leaves, d);
-  if (lane == 0) {
-    s_warp[wid] = best;
-    atomicAdd(&s_leaves, leaves);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    XBest b = s_warp[0];
-    for (int w = 1; w < XBLOCK / 32; ++w)
-      if (x_better(a, xp, probe, s_warp[w], b)) b = s_warp[w];
-    XPart& o = a.part[blk];
-    o.has = b.has; o.sl = b.sl; o.obj = b.obj; o.idx = b.idx; o.leaves = s_leaves;
+    if (RANK && REG && lane < pn) leaves += (unsigned long long)nswept * ((pn - lane + 31) >> 5);
+    __syncthreads();  // the chunk's rounds are done before s_chunk / s_round are rewritten
   }
 }
 
 // per-probe fold of the block partials into BestRec (choices by topo position)
-__global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(XArgs a) {
+__global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(const __grid_constant__ XArgs a) {
   __shared__ XBest s_warp[XBLOCK / 32];
   __shared__ unsigned long long s_leaves;
   const int probe = blockIdx.x;
@@ -747,7 +972,7 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(XArgs a) {
 // per probe).  For a verdict "x >= v" that holds on an up-set of the sorted
 // values, x passes iff rank(x) >= #{failing values}; for a down-set ("t(x) <=
 // hi"), iff rank(x) < #{passing values}.
-__global__ void __launch_bounds__(512) k_x_rank(XArgs a, int n2) {
+__global__ void __launch_bounds__(512) k_x_rank(const __grid_constant__ XArgs a, int n2) {
   extern __shared__ __align__(16) unsigned char k_smem[];
   double* v = reinterpret_cast<double*>(k_smem);
   int* ix = reinterpret_cast<int*>(v + n2);
@@ -818,9 +1043,9 @@ size_t x_smem_bytes(int max_pn_last, int P, bool rank) {
   return n * per + (XBLOCK / 32) * ws;
 }
 
-int launch_stage2_exhaustive(const XArgs& a, long long n_blocks, int P, size_t smem,
+int launch_stage2_exhaustive(const XArgs& a, long long n_chunks, int P, size_t smem,
                              cudaStream_t st) {
-  if (n_blocks <= 0) return 0;
+  if (n_chunks <= 0) return 0;
   int launches = 0;
   if (a.fast) {
     int n2 = 1;
@@ -833,27 +1058,31 @@ int launch_stage2_exhaustive(const XArgs& a, long long n_blocks, int P, size_t s
     PROF_END();
     ++launches;
   }
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   PROF_BEGIN(K_S2_EXH);
+  // persistent blocks: every resident slot of every SM, at most one per chunk
 #define JSV_XL3(PMV, F, RP)                                                                 \
   do {                                                                                      \
     if (smem > 40 * 1024)                                                                   \
       cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                            (int)smem);                                                      \
-    k_s2_exh<PMV, F, RP><<<(unsigned)n_blocks, XBLOCK, smem, st>>>(a);                      \
+    int per_sm = 1;                                                                         \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_s2_exh<PMV, F, RP>, XBLOCK, smem); \
+    const long long grid = std::min<long long>(n_chunks, (long long)std::max(1, per_sm) * n_sm); \
+    k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a);                          \
   } while (0)
-#define JSV_XLR(PMV)                         \
-  do {                                       \
-    if (!a.fast) JSV_XL3(PMV, false, 0);     \
-    else if (a.rpl == 4) JSV_XL3(PMV, true, 4);   \
-    else if (a.rpl == 8) JSV_XL3(PMV, true, 8);   \
-    else if (a.rpl == 12) JSV_XL3(PMV, true, 12); \
-    else if (a.rpl == 16) JSV_XL3(PMV, true, 16); \
-    else JSV_XL3(PMV, true, 0);              \
+#define JSV_XLR(PMV)                                     \
+  do {                                                   \
+    if (!a.fast) JSV_XL3(PMV, false, false);             \
+    else if (a.rpl) JSV_XL3(PMV, true, true);            \
+    else JSV_XL3(PMV, true, false);                      \
   } while (0)
 #define JSV_XL(PMV)                          \
   do {                                       \
-    if (a.fast) JSV_XL3(PMV, true, 0);       \
-    else JSV_XL3(PMV, false, 0);             \
+    if (a.fast) JSV_XL3(PMV, true, false);   \
+    else JSV_XL3(PMV, false, false);         \
   } while (0)
   if (P <= 1) JSV_XLR(1);
   else if (P <= 2) JSV_XLR(2);

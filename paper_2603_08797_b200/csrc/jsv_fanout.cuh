@@ -67,7 +67,7 @@ __device__ __forceinline__ bool fo_leaf_ok(const FoArgs& a, int probe, int b0, i
   return s.probes[probe].slo_eff - ps.result() >= 0;
 }
 
-__global__ void __launch_bounds__(256) k_fo_prep(FoArgs a) {
+__global__ void __launch_bounds__(256) k_fo_prep(const __grid_constant__ FoArgs a) {
   __shared__ double sacc[1024];  // feasible bundles of one leaf as (slices, accuracy) pairs
   __shared__ int ssl[1024];
   __shared__ int sflag[1024];
@@ -194,7 +194,7 @@ __global__ void __launch_bounds__(256) k_fo_prep(FoArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_fo_tau(FoArgs a, double delta) {
+__global__ void __launch_bounds__(256) k_fo_tau(const __grid_constant__ FoArgs a, double delta) {
   __shared__ double sb[256];
   const int probe = blockIdx.x;
   double best = -INFINITY;
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) k_fo_tau(FoArgs a, double delta) {
 
 // one thread per (probe, b0, total leaf slices); DFS stacks in shared memory
 #define FO_ENUM_THREADS 128
-__global__ void __launch_bounds__(FO_ENUM_THREADS) k_fo_enum(FoArgs a) {
+__global__ void __launch_bounds__(FO_ENUM_THREADS) k_fo_enum(const __grid_constant__ FoArgs a) {
   __shared__ double s_part[MAXT + 1][FO_ENUM_THREADS];
   __shared__ int s_rem[MAXT + 1][FO_ENUM_THREADS];
   __shared__ int s_cur[MAXT][FO_ENUM_THREADS];
@@ -322,7 +322,7 @@ __device__ inline int fo_cmp_m(const S2Args& a, int probe, const uint16_t* x, co
   }
 }
 
-__global__ void __launch_bounds__(128) k_fo_eval(FoArgs a, long long n) {
+__global__ void __launch_bounds__(128) k_fo_eval(const __grid_constant__ FoArgs a, long long n) {
   const long long id = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (id >= n) return;
   const FoCand& cd = a.cand[id];

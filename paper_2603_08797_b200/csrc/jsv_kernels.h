@@ -199,7 +199,7 @@ struct XProbe {
   int R;                // radix of the last position
   int rounds;           // prefix rounds per block (amortises the sink-pool staging)
                         // (a round = 8 warps x x_slots(P) prefixes)
-  int pad_;
+  int rpl;              // register sweep: sink records per lane, ceil(pool / 32) (0: loop)
 };
 
 struct XArgs {
@@ -217,8 +217,10 @@ struct XArgs {
   double* scap;           // sink-pool capacities sorted ascending
   double* sacc;           // sink-pool accuracies sorted ascending
   double* slat2;          // sink-pool 2 L sorted ascending
+  unsigned long long* work;  // chunk counter of the persistent blocks (zeroed per launch)
   int max_pn_last;        // largest sink pool of the batch
-  int rpl;                // rank space: sink records per lane kept in registers (0 = loop)
+  int rpl;                // rank space: 1 = sink records kept in registers (XProbe::rpl per
+                          // lane), 0 = loop over the shared-memory records
 };
 
 // prefix-state slots per warp of the exhaustive kernel for a graph with P paths
@@ -226,7 +228,7 @@ __host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <=
 // sink-pool records padded to a whole number of 4 x 32-lane sweeps
 __host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) & ~127; }
 size_t x_smem_bytes(int max_pn_last, int P, bool rank);
-int launch_stage2_exhaustive(const XArgs& a, long long n_blocks, int P, size_t smem,
+int launch_stage2_exhaustive(const XArgs& a, long long n_chunks, int P, size_t smem,
                              cudaStream_t st);
 
 // fan-out graphs (jsv_fanout.cuh)

@@ -55,7 +55,7 @@ __device__ __forceinline__ long long find_slot(const long long* pfx, long long l
 
 // ------------------------------------------------------------ prefix state
 
-__global__ void __launch_bounds__(256) k_s2_prefix(S2Args a) {
+__global__ void __launch_bounds__(256) k_s2_prefix(const __grid_constant__ S2Args a) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= a.n_slots) return;
   const DGraph& g = *a.g;
@@ -215,7 +215,7 @@ __device__ __forceinline__ int filter_item(const S2Args& a, int probe, long long
   return ST_PASS;
 }
 
-__global__ void __launch_bounds__(256) k_s2_level(S2Args a) {
+__global__ void __launch_bounds__(256) k_s2_level(const __grid_constant__ S2Args a) {
   const int T = a.T, L = a.level;
   const long long total = a.pfx[a.n_slots];
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -341,7 +341,7 @@ __device__ inline void merge(const S2Args& a, int probe, Cand& X, const Cand& Y)
   }
 }
 
-__global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
+__global__ void __launch_bounds__(256) k_s2_leaf(const __grid_constant__ S2Args a) {
   __shared__ int sk[5];
   __shared__ Cand sc[256];
   __shared__ unsigned long long s_leaves;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(256) k_s2_leaf(S2Args a) {
 }
 
 // per-probe fold of the leaf-block partials into BestRec
-__global__ void __launch_bounds__(256) k_s2_reduce(S2Args a) {
+__global__ void __launch_bounds__(256) k_s2_reduce(const __grid_constant__ S2Args a) {
   __shared__ Cand sc[256];
   __shared__ unsigned long long s_leaves;
   const int probe = blockIdx.x;
@@ -494,7 +494,7 @@ __global__ void __launch_bounds__(256) k_s2_reduce(S2Args a) {
 }
 
 // deepest blocked level: a prefix with r > 0 whose children all died (planner.py:910-911)
-__global__ void k_s2_blocked(S2Args a) {
+__global__ void k_s2_blocked(const __grid_constant__ S2Args a) {
   const long long s = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   if (s >= a.n_slots) return;
   const int f = a.cur_flag[s];

@@ -80,7 +80,7 @@ __device__ __forceinline__ void store_candidate(const S1Args& a, int probe, int 
   for (int k = 0; k < n; ++k) a.items[c * a.maxi + k] = it[k];
 }
 
-__global__ void k_generate(S1Args a) {
+__global__ void k_generate(const __grid_constant__ S1Args a) {
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool in = gtid < (long long)a.n_probes * a.U;
   const int probe = in ? (int)(gtid / a.U) : 0;
@@ -202,7 +202,7 @@ __device__ __forceinline__ int locate_task(const S1Args& a, long long local) {
   return t;
 }
 
-__global__ void k_stats(S1Args a) {
+__global__ void k_stats(const __grid_constant__ S1Args a) {
   long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long tot = (long long)a.n_probes * a.C_probe;
   if (c >= tot) return;
@@ -230,7 +230,7 @@ __global__ void k_stats(S1Args a) {
 // Counting sort of a job's candidates by slice count: order[] and bucket starts
 // bstart[s] = #candidates with fewer than s slices (s = 0 .. S+1).
 #define BUCKET_SMEM_MAX 12288
-__global__ void __launch_bounds__(1024) k_bucket(S1Args a) {
+__global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args a) {
   extern __shared__ int hist[];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
@@ -292,7 +292,7 @@ __device__ __forceinline__ int cmp_items(const S1Args& a, long long c1, long lon
 // row" filter.  i runs over the slices-sorted list so a block's candidates
 // have similar slices and the j range a block stages in shared memory is short.
 template <int D>
-__global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
+__global__ void __launch_bounds__(256) k_pairs_a(const __grid_constant__ S1Args a, const int* tile_task,
                                                  const int* tile_start, int tiles_pp, int jchunk,
                                                  int mode) {
   __shared__ double sh[D * TJ];
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(256) k_pairs_a(S1Args a, const int* tile_task,
 
 // Survivors of the same-bucket pass, in slices order, and their bucket starts
 // sbst[s] = #survivors with fewer than s slices.
-__global__ void __launch_bounds__(1024) k_surv(S1Args a) {
+__global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(1024) k_surv(S1Args a) {
   if (threadIdx.x == 0) a.scnt[job] = total;
 }
 
-__global__ void __launch_bounds__(1024) k_compact(S1Args a) {
+__global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args a) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(1024) k_compact(S1Args a) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_pairs_b(S1Args a, const int* tile_task,
+__global__ void __launch_bounds__(256) k_pairs_b(const __grid_constant__ S1Args a, const int* tile_task,
                                                  const int* tile_start, int tiles_pp, int jchunk) {
   __shared__ double sh[D * TJ];
   __shared__ int shc[TJ];
@@ -506,7 +506,7 @@ __global__ void __launch_bounds__(256) k_pairs_b(S1Args a, const int* tile_task,
   }
 }
 
-__global__ void __launch_bounds__(1024) k_truncate(S1Args a) {
+__global__ void __launch_bounds__(1024) k_truncate(const __grid_constant__ S1Args a) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry_nontop, carry_kept;
@@ -602,7 +602,7 @@ __device__ __forceinline__ uint32_t item_word(const S1Args& a, long long c, int 
   return sign ? 0xFFFFFFFFu : 0u;
 }
 
-__global__ void k_mrank(S1Args a) {
+__global__ void k_mrank(const __grid_constant__ S1Args a) {
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int P = a.pool_n[job];

@@ -20,7 +20,7 @@
 #include "jsv_internal.cuh"
 #include "jsv_kernels.h"
 
-__global__ void k_s2_prep(S2Args a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
+__global__ void k_s2_prep(const __grid_constant__ S2Args a, double* min_lat2, int* min_sl, double* acc_ub, int* future,
                           const double* s1_lat2, const int* s1_sl, const double* s1_acc) {
   const int probe = blockIdx.x * blockDim.x + threadIdx.x;
   if (probe >= a.n_probes) return;
@@ -162,7 +162,7 @@ __device__ int binding_from_kills(const int* k) {
   return k[best] ? best : JSV_BIND_THROUGHPUT;
 }
 
-__global__ void k_finalize(FinArgs a) {
+__global__ void k_finalize(const __grid_constant__ FinArgs a) {
   const int probe = blockIdx.x * blockDim.x + threadIdx.x;
   if (probe >= a.n_probes) return;
   const DGraph& g = *a.g;
@@ -237,7 +237,7 @@ int launch_finalize(const FinArgs& a, cudaStream_t st) {
 
 // One block per (probe, task): exact per-task filters + argmax of
 // (alpha*w_t*acc - beta*s, -s), ties on items (planner.py:1064-1100).
-__global__ void __launch_bounds__(256) k_uni_pick(S2Args a, FinArgs f, int* pick, int* kills) {
+__global__ void __launch_bounds__(256) k_uni_pick(const __grid_constant__ S2Args a, FinArgs f, int* pick, int* kills) {
   __shared__ int sk[5];
   __shared__ double s_score[256];
   __shared__ int s_sl[256];
@@ -333,7 +333,7 @@ int launch_uninformed(const S2Args& a, const FinArgs& f, int* pick, int* kills, 
 
 // ---------------------------------------------------------- derive / validate
 
-__global__ void k_derive(DeriveArgs a) {
+__global__ void k_derive(const __grid_constant__ DeriveArgs a) {
   const DGraph& g = *a.g;
   const int T = g.T;
   jsv_plan_out& o = *a.out;
@@ -387,7 +387,7 @@ int launch_derive(const DeriveArgs& a, cudaStream_t st) {
 }
 
 // validate_configuration on caller-supplied fields (planner.py:329-361)
-__global__ void k_validate(ValidateArgs a) {
+__global__ void k_validate(const __grid_constant__ ValidateArgs a) {
   const DGraph& g = *a.g;
   const DReq& rq = *a.rq;
   const DProbe& pr = *a.probe;
