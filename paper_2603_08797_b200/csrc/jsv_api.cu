@@ -13,6 +13,7 @@
 #include <string>
 #include <tuple>
 #include <vector>
+#include <algorithm>
 
 #include <cub/device/device_scan.cuh>
 
@@ -1077,11 +1078,9 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   const int W = bs.s1.W;
   const size_t smem_cap = 200 * 1024;
   std::vector<XProbe> xp(n);
-  std::vector<long long> boff(n + 1, 0);
-  long long nb = 0, cand = 0;
+  long long cand = 0;
   int max_pn_last = 1, nx = 0;
   for (int i = 0; i < n; ++i) {
-    boff[i] = nb;
     if (!active[i] || bs.dead[i]) continue;
     XProbe& x = xp[i];
     memset(&x, 0, sizeof(x));
@@ -1104,31 +1103,22 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     int glog = 0;
     while ((1 << glog) < x.R && glog < 5) ++glog;
     x.glog = glog;
-    // chunks of ~1M candidates: persistent blocks take them from a counter, the
-    // block's warps take the chunk's rounds from a shared counter
-    x.rounds = (int)std::max<long long>(1, (1LL << 20) / ((long long)(XBLOCK / 32) * x_slots(p.P) * x.R));
+    x.rounds = 1;  // exhaustive probe
     cand += x.nq * x.R;
     max_pn_last = std::max(max_pn_last, x.pn[T - 1]);
     active[i] = 0;
     ++nx;
   }
   if (nx == 0) return JSV_OK;
-  // keep >= 16 chunks per SM for the persistent blocks' balance when the batch is small
-  for (int it = 0; it < 16; ++it) {
-    nb = 0;
-    bool can = false;
-    for (int i = 0; i < n; ++i) {
-      boff[i] = nb;
-      if (xp[i].rounds == 0) continue;
-      const long long per_block = (long long)(XBLOCK / 32) * x_slots(p.P) * xp[i].rounds;
-      nb += (xp[i].nq + per_block - 1) / per_block;
-      can = can || xp[i].rounds > 1;
-    }
-    boff[n] = nb;
-    if (nb >= 148 * 8 || !can) break;
-    for (int i = 0; i < n; ++i)
-      if (xp[i].rounds > 1) xp[i].rounds = (xp[i].rounds + 1) / 2;
+  // warp-rounds (x_slots(P) prefixes each) of every probe, concatenated
+  const int n_slots = x_slots(p.P);
+  std::vector<long long> roff(n + 1, 0), poff(2 * (n + 1), 0);
+  long long n_rounds = 0;
+  for (int i = 0; i < n; ++i) {
+    roff[i] = n_rounds;
+    if (xp[i].rounds) n_rounds += (xp[i].nq + n_slots - 1) / n_slots;
   }
+  roff[n] = n_rounds;
   c.stats.exh_candidates += cand;
   c.stats.exh_probes += nx;
   // register records need whole-warp prefix groups (every sink pool >= 32) and <= 512 bundles;
@@ -1143,25 +1133,16 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   for (int i = 0; i < n; ++i)
     if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
   CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
-  CK(B[B_XBOFF].ensure(sizeof(long long) * (n + 1)));
-  CK(B[B_XPART].ensure(sizeof(XPart) * std::max<long long>(1, nb)));
   CK(cudaMemcpyAsync(B[B_XPROBE].p, xp.data(), sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(B[B_XBOFF].p, boff.data(), sizeof(long long) * (n + 1),
-                     cudaMemcpyHostToDevice, st));
-  // active flags [n] + the persistent kernel's chunk counter (8-byte aligned)
-  const size_t work_off = ((sizeof(int) * n + 7) / 8) * 8;
-  CK(B[B_ACTIVE].ensure(work_off + sizeof(unsigned long long)));
-  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, work_off + sizeof(unsigned long long), st));
+  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
+  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
   XArgs a;
   memset(&a, 0, sizeof(a));
   s2_base(p, bs, a.s);
   a.s.active = B[B_ACTIVE].as<int>();
-  a.work = reinterpret_cast<unsigned long long*>(static_cast<char*>(B[B_ACTIVE].p) + work_off);
   const bool fonly = bs.feasible_only != 0;
   a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
   a.xp = B[B_XPROBE].as<XProbe>();
-  a.boff = B[B_XBOFF].as<long long>();
-  a.part = B[B_XPART].as<XPart>();
   a.tma = (W % 4 == 0) ? 1 : 0;
   a.fast = p.lat_fast ? 1 : 0;
   for (int i = 0; i < n; ++i)
@@ -1188,8 +1169,75 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   }
   if (getenv("JSV_NO_FAST")) a.fast = 0;
   if (getenv("JSV_NO_TMA")) a.tma = 0;
-  c.stats.kernel_launches +=
-      launch_stage2_exhaustive(a, nb, p.P, x_smem_bytes(max_pn_last, p.P, a.fast != 0), st);
+  // persistent blocks take chunks -- contiguous warp-round ranges of the
+  // concatenation -- from a counter; chunk sizes are guided (a fraction of the
+  // remaining modelled cost: prefix derivation + a sweep proportional to the sink
+  // pool), large first and small last, so the blocks finish together.  The
+  // segment of probe i inside chunk o reduces into part slot o + i (unique:
+  // chunks' probe ranges are ordered); probe i folds slots [poff[i], poff[n + 1 + i])
+  const size_t smem = x_smem_bytes(max_pn_last, p.P, a.fast != 0);
+  const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
+  std::vector<double> wr(n, 0.0), wc(n + 1, 0.0);
+  for (int i = 0; i < n; ++i) {
+    const int pn = xp[i].pn[T - 1];
+    wr[i] = a.rpl ? 1000.0 + 112.0 * ((pn + 31) / 32) : 1000.0 + 4.0 * pn;
+    wc[i + 1] = wc[i] + wr[i] * (double)(roff[i + 1] - roff[i]);
+  }
+  std::vector<long long> cstart(1, 0);
+  {
+    const long long min_rounds = 4 * (XBLOCK / 32);
+    long long r = 0;
+    int pi = 0;
+    while (r < n_rounds) {
+      while (pi < n - 1 && roff[pi + 1] <= r) ++pi;
+      const double done = wc[pi] + wr[pi] * (double)(r - roff[pi]);
+      const double target = std::max(0.0, (wc[n] - done) / (2.0 * (double)G));
+      // advance by `target` cost from round r
+      long long e = r;
+      double left = target;
+      int pj = pi;
+      while (e < n_rounds && left > 0) {
+        while (pj < n - 1 && roff[pj + 1] <= e) ++pj;
+        const long long avail = roff[pj + 1] - e;
+        const long long take = std::min<long long>(avail, (long long)std::ceil(left / wr[pj]));
+        e += take;
+        left -= (double)take * wr[pj];
+      }
+      e = std::min(n_rounds, std::max(e, r + min_rounds));
+      cstart.push_back(e);
+      r = e;
+    }
+  }
+  const long long n_chunks = (long long)cstart.size() - 1;
+  for (int i = 0; i < n; ++i) {
+    const long long r0 = roff[i], r1 = roff[i + 1];
+    if (r0 == r1) continue;
+    // chunks containing rounds r0 and r1 - 1: the last o with cstart[o] <= r
+    const long long o_lo = (long long)(std::upper_bound(cstart.begin(), cstart.end() - 1, r0) - cstart.begin()) - 1;
+    const long long o_hi = (long long)(std::upper_bound(cstart.begin(), cstart.end() - 1, r1 - 1) - cstart.begin()) - 1;
+    poff[i] = o_lo + i;
+    poff[n + 1 + i] = o_hi + i + 1;
+  }
+  CK(B[B_XBOFF].ensure(sizeof(long long) * (3 * (n + 1) + n_chunks + 2)));
+  CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)(n_chunks + n)));
+  CK(cudaMemcpyAsync(B[B_XBOFF].p, poff.data(), sizeof(long long) * 2 * (n + 1),
+                     cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_XBOFF].as<long long>() + 2 * (n + 1), roff.data(),
+                     sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_XBOFF].as<long long>() + 3 * (n + 1), cstart.data(),
+                     sizeof(long long) * (n_chunks + 1), cudaMemcpyHostToDevice, st));
+  // the chunk counter (zeroed per launch) follows the chunk starts
+  CK(cudaMemsetAsync(B[B_XBOFF].as<long long>() + 3 * (n + 1) + n_chunks + 1, 0,
+                     sizeof(long long), st));
+  a.boff = B[B_XBOFF].as<long long>();
+  a.roff = B[B_XBOFF].as<long long>() + 2 * (n + 1);
+  a.cstart = B[B_XBOFF].as<long long>() + 3 * (n + 1);
+  a.n_chunks = n_chunks;
+  a.work = reinterpret_cast<unsigned long long*>(B[B_XBOFF].as<long long>() + 3 * (n + 1) +
+                                                 n_chunks + 1);
+  const long long grid = std::min(G, n_chunks);
+  a.part = B[B_XPART].as<XPart>();
+  c.stats.kernel_launches += launch_stage2_exhaustive(a, grid, p.P, smem, st);
   CK(cudaGetLastError());
   return JSV_OK;
 }

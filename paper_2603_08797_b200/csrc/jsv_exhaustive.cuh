@@ -605,12 +605,13 @@ __device__ __forceinline__ void x_sweep_reg(const XCtx<PM>& cx, const uint2* __r
   }
 }
 
-// Persistent blocks (one per resident slot of the SMs) take chunks -- a
-// contiguous prefix range of one probe -- from a device-wide counter, in
-// increasing order, so every block sees the probes in order.  The sink pool of
-// a probe is staged into shared memory when a block's chunk changes probe; the
-// block's best of a probe segment is reduced and written into the XPart of the
-// segment's last chunk (other chunks get empty parts).
+// Persistent blocks (one per resident slot of the SMs) take chunks -- warp-round
+// ranges [cstart[o], cstart[o + 1]) of the concatenation of every probe's rounds
+// (a round = x_slots(P) consecutive prefixes), sized large-first by the host --
+// from a counter.  Per probe segment of a chunk the block stages that probe's
+// sink pool into shared memory, its warps take the segment's rounds from a
+// shared counter (dynamic balance inside the block), and the block's best of the
+// segment is reduced into part slot o + probe.
 template <int PM, bool RANK, bool REG>
 __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
     k_s2_exh(const __grid_constant__ XArgs a) {
@@ -620,8 +621,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
   __shared__ __align__(8) unsigned long long s_bar;
   __shared__ XBest s_warp[XBLOCK / 32];
   __shared__ unsigned long long s_leaves;
-  __shared__ long long s_chunk;
-  __shared__ int s_round;  // next round of the chunk (warps take rounds dynamically)
+  __shared__ long long s_round;  // next round of the segment (warps take rounds dynamically)
   __shared__ __align__(16) DGraph s_g;  // the graph, read by every prefix derivation
   const S2Args& s = a.s;
   {
@@ -667,17 +667,16 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
   }
   const int S = s.rq->S;
   volatile int* found = s.active;
-  const long long nb = a.boff[s.n_probes];
-  const long long per_round = (long long)(XBLOCK / 32) * NS;
+  __shared__ long long s_chunk;
+  long long chunk = -1, r_cur = 0, r_end = 0;
 
   int probe = -1;
   unsigned stage_phase = 0;
-  long long last_chunk = -1;
   XBest best;
   best.has = 0; best.sl = 0; best.obj = 0.0; best.idx = 0;
   unsigned long long leaves = 0;
 
-  // block reduction of the current probe segment into part[last_chunk]
+  // block reduction of the current probe segment into part slot blockIdx.x + probe
   auto flush = [&]() {
     const XProbe& xp = a.xp[probe];
     if (a.mode == LEAF_ANY && best.has) found[probe] = 1;
@@ -696,7 +695,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
       XBest b = s_warp[0];
       for (int w = 1; w < XBLOCK / 32; ++w)
         if (x_better(a, xp, probe, s_warp[w], b)) b = s_warp[w];
-      XPart& o = a.part[last_chunk];
+      XPart& o = a.part[chunk + probe];
       o.has = b.has; o.sl = b.sl; o.obj = b.obj; o.idx = b.idx; o.leaves = s_leaves;
       s_leaves = 0;
     }
@@ -705,17 +704,18 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
   };
 
   while (true) {
-    if (threadIdx.x == 0) {
-      s_chunk = (long long)atomicAdd(a.work, 1ull);
-      s_round = 0;
+    if (r_cur >= r_end) {
+      // next chunk (the previous chunk's last segment ended with a block barrier)
+      if (threadIdx.x == 0) s_chunk = (long long)atomicAdd(a.work, 1ull);
+      __syncthreads();
+      chunk = s_chunk;
+      if (chunk >= a.n_chunks) break;
+      r_cur = a.cstart[chunk];
+      r_end = a.cstart[chunk + 1];
     }
-    __syncthreads();
-    const long long chunk = s_chunk;
-    const int cp = chunk < nb ? find_probe(a.boff, s.n_probes, chunk) : -1;
-    if (cp != probe) {
-      if (probe >= 0) flush();  // (ends with the block barrier inside)
-      if (cp < 0) break;
-      probe = cp;
+    probe = find_probe(a.roff, s.n_probes, r_cur);
+    const long long seg_end = min(r_end, a.roff[probe + 1]);
+    {
       // ---- stage the sink task's pool in shared memory (TMA bulk copies + mbarrier)
       const int pn = a.xp[probe].pn[T - 1];
       const int npad = x_pad(pn);
@@ -763,14 +763,9 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
                                  __longlong_as_double((long long)(unsigned)s.p_sl[q + i]));
         }
       }
+      if (threadIdx.x == 0) s_round = r_cur;
       __syncthreads();
     }
-    // chunks that do not end a segment carry an empty part
-    if (threadIdx.x == 0) {
-      XPart& o = a.part[chunk];
-      o.has = 0; o.sl = 0; o.obj = 0.0; o.idx = 0; o.leaves = 0;
-    }
-    last_chunk = chunk;
 
     const XProbe& xp = a.xp[probe];
     const DProbe& pr = s.probes[probe];
@@ -779,7 +774,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
     const int glog = xp.glog, G = 1 << glog;
     const int gw = 32 >> glog;  // prefix groups per warp
     const int gi = lane >> glog, lane_g = lane & (G - 1);
-    const long long qbase = (chunk - a.boff[probe]) * per_round * xp.rounds;
+    const long long r_probe = a.roff[probe];
     const double slo = pr.slo_eff, a_max = g.a_max;
     const double alpha = pr.alpha, beta = pr.beta;
     const long long R = xp.R;
@@ -793,14 +788,13 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
     const int rpl = xp.rpl;
     unsigned nswept = 0;  // register sweeps: leaf prefixes swept by the whole warp
 
-    // rounds of NS prefixes, taken by the warps from a block counter (balance)
+    // rounds of NS prefixes, taken by the warps from the block counter (balance)
     while (true) {
-      int rd = 0;
-      if (lane == 0) rd = atomicAdd(&s_round, 1);
+      long long rd = 0;
+      if (lane == 0) rd = (long long)atomicAdd((unsigned long long*)&s_round, 1ull);
       rd = __shfl_sync(0xffffffffu, rd, 0);
-      if (rd >= xp.rounds * (XBLOCK / 32)) break;
-      const long long qw = qbase + (long long)rd * NS;
-      if (qw >= xp.nq) break;  // warp-uniform
+      if (rd >= seg_end) break;
+      const long long qw = (rd - r_probe) * NS;
       if (a.mode == LEAF_ANY && __shfl_sync(0xffffffffu, lane == 0 ? found[probe] : 0, 0)) break;
       // ---- one prefix per lane -> shared memory
       if (lane < NS) {
@@ -822,9 +816,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
         x_sweep_reg<PM, NS>(cx, rv.pack, ws, vmask, rpl, best);
         // sink demand 0: the only child is "no instances" (planner.py:868-875)
         if (zmask && lane == 0) leaves += x_zero_reg<PM, NS>(cx, pr, S, ws, zmask, best);
-        __syncwarp();
-        continue;
-      }
+      } else {
       // ---- groups of G lanes sweep the sink pool for each prefix
       for (int j = gi; j < NS; j += gw) {
         const int fl = ws.flags[j];
@@ -911,10 +903,13 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
         }
         if (rb.has && x_better(a, xp, probe, rb, best)) best = rb;
       }
+      }
       __syncwarp();
     }
     if (RANK && REG && lane < pn) leaves += (unsigned long long)nswept * ((pn - lane + 31) >> 5);
-    __syncthreads();  // the chunk's rounds are done before s_chunk / s_round are rewritten
+    __syncthreads();  // the segment's rounds are done before its pool / s_round are rewritten
+    flush();
+    r_cur = seg_end;
   }
 }
 
@@ -923,7 +918,7 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(const __grid_constant__ X
   __shared__ XBest s_warp[XBLOCK / 32];
   __shared__ unsigned long long s_leaves;
   const int probe = blockIdx.x;
-  const long long b0 = a.boff[probe], b1 = a.boff[probe + 1];
+  const long long b0 = a.boff[probe], b1 = a.boff[a.s.n_probes + 1 + probe];
   if (b0 == b1) return;
   const XProbe& xp = a.xp[probe];
   if (threadIdx.x == 0) s_leaves = 0;
@@ -1043,9 +1038,43 @@ size_t x_smem_bytes(int max_pn_last, int P, bool rank) {
   return n * per + (XBLOCK / 32) * ws;
 }
 
-int launch_stage2_exhaustive(const XArgs& a, long long n_chunks, int P, size_t smem,
+// resident blocks of the kernel instance a launch with these arguments uses
+#define JSV_XDISPATCH(MAC)                              \
+  do {                                                  \
+    if (P <= 1) { JSV_XD(1, MAC); }                     \
+    else if (P <= 2) { JSV_XD(2, MAC); }                \
+    else if (P <= 4) { JSV_XD(4, MAC); }                \
+    else if (P <= 8) { JSV_XDN(8, MAC); }               \
+    else if (P <= 16) { JSV_XDN(16, MAC); }             \
+    else { JSV_XDN(MAXP, MAC); }                        \
+  } while (0)
+#define JSV_XD(PMV, MAC)                                \
+  if (!a.fast) MAC(PMV, false, false);                  \
+  else if (a.rpl) MAC(PMV, true, true);                 \
+  else MAC(PMV, true, false)
+#define JSV_XDN(PMV, MAC)                               \
+  if (a.fast) MAC(PMV, true, false);                    \
+  else MAC(PMV, false, false)
+#define JSV_XOCC(PMV, F, RP)                                                                  \
+  do {                                                                                        \
+    if (smem > 40 * 1024)                                                                     \
+      cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                        \
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_s2_exh<PMV, F, RP>, XBLOCK, smem); \
+  } while (0)
+#define JSV_XLAUNCH(PMV, F, RP) k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a)
+
+long long x_resident_blocks(const XArgs& a, int P, size_t smem) {
+  int dev = 0, n_sm = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  JSV_XDISPATCH(JSV_XOCC);
+  return (long long)(per_sm > 0 ? per_sm : 1) * n_sm;
+}
+
+int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
                              cudaStream_t st) {
-  if (n_chunks <= 0) return 0;
+  if (grid <= 0) return 0;
   int launches = 0;
   if (a.fast) {
     int n2 = 1;
@@ -1058,44 +1087,16 @@ int launch_stage2_exhaustive(const XArgs& a, long long n_chunks, int P, size_t s
     PROF_END();
     ++launches;
   }
-  int dev = 0, n_sm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   PROF_BEGIN(K_S2_EXH);
-  // persistent blocks: every resident slot of every SM, at most one per chunk
-#define JSV_XL3(PMV, F, RP)                                                                 \
-  do {                                                                                      \
-    if (smem > 40 * 1024)                                                                   \
-      cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                      \
-    int per_sm = 1;                                                                         \
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_s2_exh<PMV, F, RP>, XBLOCK, smem); \
-    const long long grid = std::min<long long>(n_chunks, (long long)std::max(1, per_sm) * n_sm); \
-    k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a);                          \
-  } while (0)
-#define JSV_XLR(PMV)                                     \
-  do {                                                   \
-    if (!a.fast) JSV_XL3(PMV, false, false);             \
-    else if (a.rpl) JSV_XL3(PMV, true, true);            \
-    else JSV_XL3(PMV, true, false);                      \
-  } while (0)
-#define JSV_XL(PMV)                          \
-  do {                                       \
-    if (a.fast) JSV_XL3(PMV, true, false);   \
-    else JSV_XL3(PMV, false, false);         \
-  } while (0)
-  if (P <= 1) JSV_XLR(1);
-  else if (P <= 2) JSV_XLR(2);
-  else if (P <= 4) JSV_XLR(4);
-  else if (P <= 8) JSV_XL(8);
-  else if (P <= 16) JSV_XL(16);
-  else JSV_XL(MAXP);
-#undef JSV_XL
-#undef JSV_XLR
-#undef JSV_XL3
+  JSV_XDISPATCH(JSV_XLAUNCH);
   PROF_END();
   PROF_BEGIN(K_S2_XREDUCE);
   k_s2_xreduce<<<a.s.n_probes, XBLOCK, 0, st>>>(a);
   PROF_END();
   return launches + 2;
 }
+#undef JSV_XDISPATCH
+#undef JSV_XD
+#undef JSV_XDN
+#undef JSV_XOCC
+#undef JSV_XLAUNCH

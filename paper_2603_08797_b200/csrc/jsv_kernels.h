@@ -197,15 +197,18 @@ struct XProbe {
   long long q0, nq;     // prefix range of this shard
   int glog;             // lanes per prefix group = 1 << glog
   int R;                // radix of the last position
-  int rounds;           // prefix rounds per block (amortises the sink-pool staging)
-                        // (a round = 8 warps x x_slots(P) prefixes)
+  int rounds;           // 1: exhaustive probe (0: not swept)
   int rpl;              // register sweep: sink records per lane, ceil(pool / 32) (0: loop)
 };
 
 struct XArgs {
   S2Args s;
   const XProbe* xp;
-  const long long* boff;  // [n_probes + 1] blocks of each probe
+  const long long* boff;  // [2 (n_probes + 1)]: part slots [boff[i], boff[n_probes + 1 + i]) of probe i
+  const long long* roff;  // [n_probes + 1] first warp-round of each probe (concatenated rounds)
+  const long long* cstart;  // [n_chunks + 1] first warp-round of each chunk
+  long long n_chunks;
+  unsigned long long* work; // chunk counter of the persistent blocks (zeroed per launch)
   XPart* part;            // [blocks]
   int mode;               // LEAF_FULL / LEAF_FIRST / LEAF_ANY
   int tma;                // stage the sink pool with cp.async.bulk (alignment holds)
@@ -217,7 +220,6 @@ struct XArgs {
   double* scap;           // sink-pool capacities sorted ascending
   double* sacc;           // sink-pool accuracies sorted ascending
   double* slat2;          // sink-pool 2 L sorted ascending
-  unsigned long long* work;  // chunk counter of the persistent blocks (zeroed per launch)
   int max_pn_last;        // largest sink pool of the batch
   int rpl;                // rank space: 1 = sink records kept in registers (XProbe::rpl per
                           // lane), 0 = loop over the shared-memory records
@@ -228,7 +230,8 @@ __host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <=
 // sink-pool records padded to a whole number of 4 x 32-lane sweeps
 __host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) & ~127; }
 size_t x_smem_bytes(int max_pn_last, int P, bool rank);
-int launch_stage2_exhaustive(const XArgs& a, long long n_chunks, int P, size_t smem,
+long long x_resident_blocks(const XArgs& a, int P, size_t smem);
+int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
                              cudaStream_t st);
 
 // fan-out graphs (jsv_fanout.cuh)
