@@ -168,24 +168,133 @@ def _verdicts_from(out: N.PlanOut, app, lw: LW.Lowered) -> tuple[ConstraintVerdi
     return tuple(vs)
 
 
+_PLAN_DTYPE = None
+_new = object.__new__
+
+
+def _mk(cls, **fields):
+    # frozen-dataclass instance without the per-field object.__setattr__ of its
+    # __init__ (same __dict__, so ==, repr and dataclasses.* behave identically)
+    o = _new(cls)
+    o.__dict__.update(fields)
+    return o
+
+
 def _result_from(out: N.PlanOut, app, lw: LW.Lowered, request, wall_ms: float) -> PlanResult:
-    g = app.graph
-    sizes = {}
-    cut = []
-    for t in g.topological_order:
-        ti = lw.index[t]
-        if out.pool_present[ti]:
-            sizes[t] = int(out.pool_size[ti])
-            if out.truncated[ti]:
-                cut.append(t)
-    stats = SolverStats(int(out.nodes), wall_ms, sizes, tuple(cut))
-    if not out.has_config:
-        return PlanResult(False, None, None, lw.a_max, _binding(out.binding), (), stats)
-    cfg = _config_from(out, app, lw, request.demand_rps)
-    vs = _verdicts_from(out, app, lw)
-    if out.feasible:
-        return PlanResult(True, cfg, cfg.objective, lw.a_max, None, vs, stats)
-    return PlanResult(False, cfg, None, lw.a_max, _binding(out.binding), vs, stats)
+    return _results_from((N.PlanOut * 1).from_buffer_copy(out), [app], lw, [request], wall_ms)[0]
+
+
+def _results_from(outs, apps, lw: LW.Lowered, requests, wall_ms: float) -> list[PlanResult]:
+    """Decode a ctypes array of jsv_plan_out records into PlanResults.
+
+    Every field is pulled out of the records once, batch-wide, through a numpy
+    view (field access on ctypes structures costs microseconds each); the
+    dataclasses are then built from plain Python lists.  Same values as the
+    per-field decode: ints and IEEE doubles are copied bit-for-bit.
+    """
+    global _PLAN_DTYPE
+    if _PLAN_DTYPE is None:
+        _PLAN_DTYPE = np.dtype(N.PlanOut)
+    arr = np.frombuffer(outs, dtype=_PLAN_DTYPE)
+    T, P = len(lw.ids), len(lw.paths)
+    E = len(lw.edges)
+    col = {}
+    for name in ("feasible", "has_config", "binding", "objective", "a_obj", "nodes",
+                 "total_slices", "uncovered_mask", "res_margin", "acc_margin"):
+        col[name] = arr[name].tolist()
+    for name in ("pool_size", "pool_present", "truncated", "n_items", "latency", "capacity",
+                 "demand", "accuracy", "slices", "thr_margin"):
+        col[name] = arr[name][:, :T].tolist()
+    col["items"] = arr["items"][:, :T].tolist()
+    col["hput"] = arr["hput"][:, :T].tolist()
+    col["fanout"] = arr["fanout"][:, :E].tolist()
+    col["path_acc"] = arr["path_acc"][:, :P].tolist()
+    col["lat_margin"] = arr["lat_margin"][:, :P].tolist()
+    g = apps[0].graph
+    idx = lw.index
+    ids = lw.ids
+    topo_t = list(g.topological_order)
+    topo_i = [idx[t] for t in topo_t]
+    task_i = [idx[t] for t in g.task_ids]
+    edges = [((t, d), lw.edge_index[(t, d)]) for t in g.task_ids for d in g.successors[t]]
+    path_names = ["->".join(p) for p in lw.paths]
+    keys = lw.keys
+    res = []
+    for i, (app, request) in enumerate(zip(apps, requests)):
+        sizes = {}
+        cut = []
+        present, psize, trunc = col["pool_present"][i], col["pool_size"][i], col["truncated"][i]
+        for t, ti in zip(topo_t, topo_i):
+            if present[ti]:
+                sizes[t] = psize[ti]
+                if trunc[ti]:
+                    cut.append(t)
+        stats = _mk(SolverStats, nodes=col["nodes"][i], wall_ms=wall_ms, pool_sizes=sizes,
+                    truncated_tasks=tuple(cut))
+        if not col["has_config"][i]:
+            res.append(_mk(PlanResult, feasible=False, config=None, objective=None, a_max=lw.a_max,
+                           binding_constraint=_binding(col["binding"][i]), verdicts=(),
+                           stats=stats))
+            continue
+        n_items, items, hp = col["n_items"][i], col["items"][i], col["hput"][i]
+        m = []
+        for ti, t in enumerate(ids):
+            row, kt = items[ti], keys[ti]
+            for k in range(n_items[ti]):
+                w = row[k]
+                vid, seg, batch = kt[w >> 16]
+                m.append(((t, vid, seg, batch), w & 0xFFFF))
+        hput = {}
+        for t, ti in zip(topo_t, topo_i):
+            row, kt, hrow = items[ti], keys[ti], hp[ti]
+            for k in range(n_items[ti]):
+                vid, seg, batch = kt[row[k] >> 16]
+                hput[(t, vid, seg, batch)] = hrow[k]
+        lat, cap, dem = col["latency"][i], col["capacity"][i], col["demand"][i]
+        acc, sl, fo, pa = col["accuracy"][i], col["slices"][i], col["fanout"][i], col["path_acc"][i]
+        unc = col["uncovered_mask"][i]
+        bad = tuple(t for t, ti in zip(topo_t, topo_i) if (unc >> ti) & 1)
+        cfg = _mk(
+            Configuration,
+            m=tuple(m),
+            entry_demand_rps=float(request.demand_rps),
+            latency_ms={t: lat[ti] for t, ti in zip(g.task_ids, task_i)},
+            capacity_rps={t: cap[ti] for t, ti in zip(g.task_ids, task_i)},
+            demand_rps={t: dem[ti] for t, ti in zip(topo_t, topo_i)},
+            slices={t: sl[ti] for t, ti in zip(g.task_ids, task_i)},
+            accuracy={t: acc[ti] for t, ti in zip(g.task_ids, task_i)},
+            fanout={e: fo[k] for e, k in edges},
+            hput=hput,
+            path_accuracy={p: pa[k] for k, p in enumerate(lw.paths)},
+            total_slices=col["total_slices"][i],
+            a_obj=col["a_obj"][i],
+            a_max=lw.a_max,
+            objective=col["objective"][i],
+            structurally_infeasible=bad,
+        )
+        vs = []
+        lm, tm = col["lat_margin"][i], col["thr_margin"][i]
+        for k, name in enumerate(path_names):
+            mg = lm[k]
+            vs.append(_mk(ConstraintVerdict, name="latency", subject=name, passed=mg >= 0, margin=mg))
+        for t, ti in zip(topo_t, topo_i):
+            mg = tm[ti]
+            vs.append(_mk(ConstraintVerdict, name="throughput", subject=t, passed=mg >= 0, margin=mg))
+        mg = col["res_margin"][i]
+        vs.append(_mk(ConstraintVerdict, name="resources", subject="", passed=mg >= 0, margin=mg))
+        mg = col["acc_margin"][i]
+        vs.append(_mk(ConstraintVerdict, name="accuracy", subject="", passed=mg >= 0, margin=mg))
+        vs.append(_mk(ConstraintVerdict, name="coverage", subject=",".join(bad), passed=not bad,
+                      margin=0.0 if not bad else -float(len(bad))))
+        vs = tuple(vs)
+        if col["feasible"][i]:
+            res.append(_mk(PlanResult, feasible=True, config=cfg, objective=cfg.objective,
+                           a_max=lw.a_max, binding_constraint=None, verdicts=vs, stats=stats))
+        else:
+            res.append(_mk(PlanResult, feasible=False, config=cfg, objective=None, a_max=lw.a_max,
+                           binding_constraint=_binding(col["binding"][i]), verdicts=vs,
+                           stats=stats))
+    return res
 
 
 # ------------------------------------------------------------------ solves
@@ -236,7 +345,7 @@ def plan_batch(
     N.check(N.load_library().jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests),
                                             probes, outs))
     wall = (time.perf_counter() - t0) * 1000.0
-    return [_result_from(outs[i], apps[i], lw, requests[i], wall) for i in range(len(requests))]
+    return _results_from(outs, apps, lw, requests, wall)
 
 
 def plan(
