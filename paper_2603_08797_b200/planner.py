@@ -198,41 +198,49 @@ def _results_from(outs, apps, lw: LW.Lowered, requests, wall_ms: float) -> list[
     arr = np.frombuffer(outs, dtype=_PLAN_DTYPE)
     T, P = len(lw.ids), len(lw.paths)
     E = len(lw.edges)
-    col = {}
-    for name in ("feasible", "has_config", "binding", "objective", "a_obj", "nodes",
-                 "total_slices", "uncovered_mask", "res_margin", "acc_margin"):
-        col[name] = arr[name].tolist()
-    for name in ("pool_size", "pool_present", "truncated", "n_items", "latency", "capacity",
-                 "demand", "accuracy", "slices", "thr_margin"):
-        col[name] = arr[name][:, :T].tolist()
-    col["items"] = arr["items"][:, :T].tolist()
-    col["hput"] = arr["hput"][:, :T].tolist()
-    col["fanout"] = arr["fanout"][:, :E].tolist()
-    col["path_acc"] = arr["path_acc"][:, :P].tolist()
-    col["lat_margin"] = arr["lat_margin"][:, :P].tolist()
     g = apps[0].graph
     idx = lw.index
     ids = lw.ids
     topo_t = list(g.topological_order)
     topo_i = [idx[t] for t in topo_t]
-    task_i = [idx[t] for t in g.task_ids]
-    edges = [((t, d), lw.edge_index[(t, d)]) for t in g.task_ids for d in g.successors[t]]
+    task_t = list(g.task_ids)
+    task_i = [idx[t] for t in task_t]
+    edge_k = [((t, d), lw.edge_index[(t, d)]) for t in task_t for d in g.successors[t]]
+    edge_names = [e for e, _ in edge_k]
+    col = {}
+    for name in ("feasible", "has_config", "binding", "objective", "a_obj", "nodes",
+                 "total_slices", "uncovered_mask", "res_margin", "acc_margin"):
+        col[name] = arr[name].tolist()
+    # per-task columns in the order the result dicts list them
+    for name in ("latency", "capacity", "accuracy", "slices"):
+        col[name] = arr[name][:, task_i].tolist()
+    for name in ("demand", "thr_margin", "pool_size", "pool_present", "truncated"):
+        col[name] = arr[name][:, topo_i].tolist()
+    col["n_items"] = arr["n_items"][:, :T].tolist()
+    col["items"] = arr["items"][:, :T].tolist()
+    col["hput"] = arr["hput"][:, :T].tolist()
+    col["fanout"] = arr["fanout"][:, [k for _, k in edge_k]].tolist()
+    col["path_acc"] = arr["path_acc"][:, :P].tolist()
+    col["lat_margin"] = arr["lat_margin"][:, :P].tolist()
     path_names = ["->".join(p) for p in lw.paths]
+    paths = list(lw.paths)
+    topo_pos = list(enumerate(topo_i))
     keys = lw.keys
+    a_max = lw.a_max
     res = []
-    for i, (app, request) in enumerate(zip(apps, requests)):
+    for i, request in enumerate(requests):
         sizes = {}
         cut = []
         present, psize, trunc = col["pool_present"][i], col["pool_size"][i], col["truncated"][i]
-        for t, ti in zip(topo_t, topo_i):
-            if present[ti]:
-                sizes[t] = psize[ti]
-                if trunc[ti]:
+        for k, t in enumerate(topo_t):
+            if present[k]:
+                sizes[t] = psize[k]
+                if trunc[k]:
                     cut.append(t)
         stats = _mk(SolverStats, nodes=col["nodes"][i], wall_ms=wall_ms, pool_sizes=sizes,
                     truncated_tasks=tuple(cut))
         if not col["has_config"][i]:
-            res.append(_mk(PlanResult, feasible=False, config=None, objective=None, a_max=lw.a_max,
+            res.append(_mk(PlanResult, feasible=False, config=None, objective=None, a_max=a_max,
                            binding_constraint=_binding(col["binding"][i]), verdicts=(),
                            stats=stats))
             continue
@@ -242,43 +250,37 @@ def _results_from(outs, apps, lw: LW.Lowered, requests, wall_ms: float) -> list[
             row, kt = items[ti], keys[ti]
             for k in range(n_items[ti]):
                 w = row[k]
-                vid, seg, batch = kt[w >> 16]
-                m.append(((t, vid, seg, batch), w & 0xFFFF))
+                m.append(((t,) + kt[w >> 16], w & 0xFFFF))
         hput = {}
         for t, ti in zip(topo_t, topo_i):
             row, kt, hrow = items[ti], keys[ti], hp[ti]
             for k in range(n_items[ti]):
-                vid, seg, batch = kt[row[k] >> 16]
-                hput[(t, vid, seg, batch)] = hrow[k]
-        lat, cap, dem = col["latency"][i], col["capacity"][i], col["demand"][i]
-        acc, sl, fo, pa = col["accuracy"][i], col["slices"][i], col["fanout"][i], col["path_acc"][i]
+                hput[(t,) + kt[row[k] >> 16]] = hrow[k]
         unc = col["uncovered_mask"][i]
-        bad = tuple(t for t, ti in zip(topo_t, topo_i) if (unc >> ti) & 1)
+        bad = tuple(t for t, ti in zip(topo_t, topo_i) if (unc >> ti) & 1) if unc else ()
         cfg = _mk(
             Configuration,
             m=tuple(m),
             entry_demand_rps=float(request.demand_rps),
-            latency_ms={t: lat[ti] for t, ti in zip(g.task_ids, task_i)},
-            capacity_rps={t: cap[ti] for t, ti in zip(g.task_ids, task_i)},
-            demand_rps={t: dem[ti] for t, ti in zip(topo_t, topo_i)},
-            slices={t: sl[ti] for t, ti in zip(g.task_ids, task_i)},
-            accuracy={t: acc[ti] for t, ti in zip(g.task_ids, task_i)},
-            fanout={e: fo[k] for e, k in edges},
+            latency_ms=dict(zip(task_t, col["latency"][i])),
+            capacity_rps=dict(zip(task_t, col["capacity"][i])),
+            demand_rps=dict(zip(topo_t, col["demand"][i])),
+            slices=dict(zip(task_t, col["slices"][i])),
+            accuracy=dict(zip(task_t, col["accuracy"][i])),
+            fanout=dict(zip(edge_names, col["fanout"][i])),
             hput=hput,
-            path_accuracy={p: pa[k] for k, p in enumerate(lw.paths)},
+            path_accuracy=dict(zip(paths, col["path_acc"][i])),
             total_slices=col["total_slices"][i],
             a_obj=col["a_obj"][i],
-            a_max=lw.a_max,
+            a_max=a_max,
             objective=col["objective"][i],
             structurally_infeasible=bad,
         )
         vs = []
         lm, tm = col["lat_margin"][i], col["thr_margin"][i]
-        for k, name in enumerate(path_names):
-            mg = lm[k]
+        for name, mg in zip(path_names, lm):
             vs.append(_mk(ConstraintVerdict, name="latency", subject=name, passed=mg >= 0, margin=mg))
-        for t, ti in zip(topo_t, topo_i):
-            mg = tm[ti]
+        for t, mg in zip(topo_t, tm):
             vs.append(_mk(ConstraintVerdict, name="throughput", subject=t, passed=mg >= 0, margin=mg))
         mg = col["res_margin"][i]
         vs.append(_mk(ConstraintVerdict, name="resources", subject="", passed=mg >= 0, margin=mg))

@@ -317,3 +317,78 @@ def test_profile_csv_byte_identical_to_reference(tmp_path):
         data = p.read_bytes()
         assert hashlib.sha256(data).hexdigest() == doc["sha256"], name
         assert profile_to_rows(load_profile(p)) == profile_to_rows(table)
+
+
+def _legacy_result(out, app, lw, request):
+    """The per-field decode (_config_from/_verdicts_from) the batch decoder replaced."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import PlanResult, SolverStats
+
+    g = app.graph
+    sizes, cut = {}, []
+    for t in g.topological_order:
+        ti = lw.index[t]
+        if out.pool_present[ti]:
+            sizes[t] = int(out.pool_size[ti])
+            if out.truncated[ti]:
+                cut.append(t)
+    stats = SolverStats(int(out.nodes), 0.0, sizes, tuple(cut))
+    if not out.has_config:
+        return PlanResult(False, None, None, lw.a_max, P._binding(out.binding), (), stats)
+    cfg = P._config_from(out, app, lw, request.demand_rps)
+    vs = P._verdicts_from(out, app, lw)
+    if out.feasible:
+        return PlanResult(True, cfg, cfg.objective, lw.a_max, None, vs, stats)
+    return PlanResult(False, cfg, None, lw.a_max, P._binding(out.binding), vs, stats)
+
+
+@pytest.mark.parametrize("name", ["ar-assistant", "traffic-analysis"])
+def test_batch_decode_equals_per_field_decode(name):
+    """planner._results_from (numpy view, batch-wide) == the per-field ctypes decode."""
+    import json
+
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace, plan_result_to_dict
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "apps.json")) as fh:
+        doc = json.load(fh)[name]
+    app = app_from_dict(doc["app"])
+    table = profile_from_rows(doc["profile"])
+    lw = LW.lower(app, table)
+    rng = random.Random(7)
+    n = 24
+    outs = (N.PlanOut * n)()
+    reqs = []
+    T, E, Pn = len(lw.ids), len(lw.edges), len(lw.paths)
+    for i, o in enumerate(outs):
+        o.has_config = int(i % 5 != 0)
+        o.feasible = int(i % 3 != 0)
+        o.binding = rng.randrange(-1, 5)
+        o.objective, o.a_obj = rng.random(), rng.random()
+        o.nodes = rng.randrange(1000)
+        o.total_slices = rng.randrange(40)
+        o.uncovered_mask = rng.randrange(1 << T) if i % 4 == 0 else 0
+        o.res_margin, o.acc_margin = rng.uniform(-5, 5), rng.uniform(-1, 1)
+        for ti in range(T):
+            o.pool_size[ti] = rng.randrange(500)
+            o.pool_present[ti] = rng.randrange(2)
+            o.truncated[ti] = rng.randrange(2)
+            o.n_items[ti] = rng.randrange(4)
+            for k in range(o.n_items[ti]):
+                o.items[ti][k] = (rng.randrange(len(lw.keys[ti])) << 16) | rng.randrange(1, 9)
+                o.hput[ti][k] = rng.uniform(0, 900)
+            o.latency[ti], o.capacity[ti] = rng.uniform(0, 500), rng.uniform(0, 900)
+            o.demand[ti], o.accuracy[ti] = rng.uniform(0, 900), rng.random()
+            o.slices[ti] = rng.randrange(30)
+            o.thr_margin[ti] = rng.uniform(-50, 50)
+        for e in range(E):
+            o.fanout[e] = rng.uniform(0, 3)
+        for p in range(Pn):
+            o.path_acc[p], o.lat_margin[p] = rng.random(), rng.uniform(-100, 100)
+        reqs.append(PlanRequest(100.0 + i, 28, SearchSpace(True, True, True)))
+    got = P._results_from(outs, [app] * n, lw, reqs, 0.0)
+    for i in range(n):
+        want = _legacy_result(outs[i], app, lw, reqs[i])
+        assert got[i] == want
+        assert plan_result_to_dict(got[i]) == plan_result_to_dict(want)
+        assert repr(got[i]) == repr(want)
