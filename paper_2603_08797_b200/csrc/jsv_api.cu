@@ -78,7 +78,7 @@ enum BufId {
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
-  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_COUNT
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_COUNT
 };
 
 struct jsv_context {
@@ -759,7 +759,32 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.pcnt = B[B_PCNT].as<int>();
   a.sbst = B[B_SBST].as<int>();
   a.scnt = B[B_SCNT].as<int>();
+  // pair-pass work lists (filled on the device by the kernels that know each job's count)
+  long long max_items = 0;
+  for (int t = 0; t < T; ++t) {
+    const long long cap = pl.task_cap[t];
+    max_items += ((cap + 255) / 256) * std::max<long long>(1, (cap + 1023) / 1024);
+  }
+  max_items = std::max<long long>(1, max_items * n);
+  CK(B[B_WL0].ensure(sizeof(int4) * max_items));
+  CK(B[B_WL1].ensure(sizeof(int4) * max_items));
+  CK(B[B_WL2].ensure(sizeof(int4) * max_items));
+  CK(B[B_WN].ensure(sizeof(int) * 4));
+  CK(cudaMemsetAsync(B[B_WN].p, 0, sizeof(int) * 4, st));
+  a.wl[0] = B[B_WL0].as<int4>();
+  a.wl[1] = B[B_WL1].as<int4>();
+  a.wl[2] = B[B_WL2].as<int4>();
+  a.wn = B[B_WN].as<int>();
+  CK(B[B_ARRL].ensure(sizeof(double) * C1 * D));
+  a.arrl = B[B_ARRL].as<double>();
   S1Launch L{};
+  L.max_items = max_items;
+  {
+    int dev = 0, n_sm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    L.grid = (long long)n_sm * 8;
+  }
   L.tile_task = B[B_TILE_TASK].as<int>();
   L.tile_start = B[B_TILE_START].as<int>();
   L.tiles_pp = (int)pl.tile_task.size();

@@ -90,6 +90,9 @@ struct S1Args {
   int* pcnt;      // [Ctot] survivors before each sorted position
   int* sbst;      // [jobs * (S+2)] survivor bucket starts
   int* scnt;      // [jobs] survivors
+  double* arrl;   // [D * Ctot] coordinates in list order (slices order, then survivor order)
+  int4* wl[3];    // pair-pass work lists {job, i0, j0}: same-bucket, survivors, frontier
+  int* wn;        // [3] their lengths (zeroed per batch)
 };
 
 struct S1Launch {
@@ -98,6 +101,8 @@ struct S1Launch {
   int tiles_pp;
   int jchunks_a, jchunk_a;
   int jchunks_b, jchunk_b;
+  long long max_items;  // capacity of each work list
+  long long grid;       // blocks of the grid-stride pair kernels
 };
 
 int stage1_padded_dims(int D);

@@ -22,6 +22,8 @@
 //                pool SoA + per-pool bounds for Stage 2.
 //   k_mrank      per-pool ranks of the item lists with end = -inf / +inf; the
 //                Stage-2 tie-break on m compares these.
+#include <algorithm>
+#include <cstdlib>
 #include <cub/block/block_scan.cuh>
 #include "jsv_internal.cuh"
 #include "jsv_kernels.h"
@@ -227,6 +229,17 @@ __global__ void k_stats(const __grid_constant__ S1Args a) {
   a.flag[c] = 0u;
 }
 
+// append the work items of one job: i tiles of 256, j chunks of jchunk over [0, jend(i0))
+__device__ __forceinline__ void push_items(int4* list, int* count, int job, int n, int jchunk,
+                                           bool triangular) {
+  for (int i0 = 0; i0 < n; i0 += 256) {
+    const int jend = triangular ? min(n, i0 + 256) : n;
+    const int nj = max(1, (jend + jchunk - 1) / jchunk);
+    const int at = atomicAdd(count, nj);
+    for (int c = 0; c < nj; ++c) list[at + c] = make_int4(job, i0, c * jchunk, 0);
+  }
+}
+
 // Counting sort of a job's candidates by slice count: order[] and bucket starts
 // bstart[s] = #candidates with fewer than s slices (s = 0 .. S+1).
 #define BUCKET_SMEM_MAX 12288
@@ -242,7 +255,10 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
   if (NB > BUCKET_SMEM_MAX) {
     // huge budgets: identity order, every candidate scanned
     for (int s = threadIdx.x; s < NB; s += blockDim.x) bst[s] = (s == 0) ? 0 : n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) a.order[base + i] = i;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      a.order[base + i] = i;
+      for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + i] = a.arr[d * tot + base + i];
+    }
     return;
   }
   for (int s = threadIdx.x; s < NB; s += blockDim.x) hist[s] = 0;
@@ -259,13 +275,14 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
     }
   }
   __syncthreads();
+  if (threadIdx.x == 0) push_items(a.wl[0], a.wn + 0, job, n, 1 << 30, false);
   // hist[s] is now the start of bucket s; scatter (order inside a bucket is irrelevant)
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int s = (int)a.arr[base + i];
     const int pos = atomicAdd(&hist[s], 1);
     a.order[base + pos] = i;
+    for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
   }
-  (void)tot;
 }
 
 // items(c1) < items(c2) lexicographically over ((key, count), ...) tuples
@@ -292,21 +309,11 @@ __device__ __forceinline__ int cmp_items(const S1Args& a, long long c1, long lon
 // row" filter.  i runs over the slices-sorted list so a block's candidates
 // have similar slices and the j range a block stages in shared memory is short.
 template <int D>
-__global__ void __launch_bounds__(256) k_pairs_a(const __grid_constant__ S1Args a, const int* tile_task,
-                                                 const int* tile_start, int tiles_pp, int jchunk,
-                                                 int mode) {
-  __shared__ double sh[D * TJ];
-  __shared__ int shj[TJ];
-  __shared__ int s_lo, s_hi;
-  const int probe = blockIdx.x / tiles_pp;
-  const int tl = blockIdx.x % tiles_pp;
-  const int t = tile_task[tl];
-  const int i0 = tile_start[tl];
-  const int job = probe * a.T + t;
+__device__ __forceinline__ void pairs_a_tile(const S1Args& a, int job, int i0, int j0, int jchunk,
+                                             int mode, double* sh, int* shj, int& s_lo, int& s_hi) {
+  const int probe = job / a.T, t = job % a.T;
   const int n = mode == 0 ? a.cnt[job] : a.scnt[job];
-  if (i0 >= n) return;
-  const int j0 = blockIdx.y * jchunk;
-  if (j0 >= n) return;
+  if (i0 >= n || j0 >= n) return;  // (block-uniform)
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long base = job_base(a, probe, t);
   const int* list = (mode == 0 ? a.order : a.surv) + base;
@@ -380,6 +387,84 @@ __global__ void __launch_bounds__(256) k_pairs_a(const __grid_constant__ S1Args 
   if (act && fl) atomicOr(&a.flag[base + i], fl);
 }
 
+// Work items {job, i0, j0} of a pass come from a device list built by the
+// kernel that knew the job's count (k_bucket / k_surv / k_compact), so no block
+// is launched for the empty tail of a job's candidate capacity.
+template <int D>
+__global__ void __launch_bounds__(256) k_pairs_a(const __grid_constant__ S1Args a,
+                                                 const int4* items, const int* n_items, int jchunk,
+                                                 int mode) {
+  __shared__ double sh[D * TJ];
+  __shared__ int shj[TJ];
+  __shared__ int s_lo, s_hi;
+  const int nw = *n_items;
+  for (int w = blockIdx.x; w < nw; w += gridDim.x) {
+    const int4 it = items[w];
+    pairs_a_tile<D>(a, it.x, it.y, it.z, jchunk, mode, sh, shj, s_lo, s_hi);
+    __syncthreads();
+  }
+}
+
+// The same skyline test without shared-memory staging or barriers: one thread
+// per list position i scans its own j range straight from the list-ordered
+// coordinates (arrl, L1-resident).  Lanes of a warp hold neighbouring list
+// positions -- the same or adjacent slices buckets -- so they read the same j
+// in step (broadcast loads) and each leaves its loop at its first dominator.
+template <int D>
+__global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args a, int mode) {
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (gid >= tot) return;
+  const int probe = (int)(gid / a.C_probe);
+  const long long local = gid % a.C_probe;
+  const int t = locate_task(a, local);
+  const int p = (int)(local - a.task_base[t]);
+  const int job = probe * a.T + t;
+  const int n = mode == 0 ? a.cnt[job] : a.scnt[job];
+  if (p >= n) return;
+  const long long base = job_base(a, probe, t);
+  const double* __restrict__ xl = a.arrl + base;
+  double xi[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) xi[d] = xl[d * tot + p];
+  const int si = (int)xi[0];
+  int lo, hi;
+  if (mode == 0) {
+    const int* bst = a.bstart + (long long)job * (a.S + 2);
+    lo = bst[si];
+    hi = bst[si + 1];
+  } else {
+    lo = 0;
+    hi = a.sbst[(long long)job * (a.S + 2) + si];
+  }
+  const int* list = (mode == 0 ? a.order : a.surv) + base;
+  unsigned fl = 0;
+  for (int j = lo; j < hi; ++j) {
+    bool le = true, eq = true;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const double xj = xl[d * tot + j];
+      le = le && (xj <= xi[d]);
+      eq = eq && (xj == xi[d]);
+    }
+    if (le) {
+      if (!eq) {
+        fl = 1u;
+        break;
+      }
+      if (j != p) {
+        const int ci = list[p], cj = list[j];
+        const int c = cmp_items(a, base + cj, base + ci);
+        if (c < 0 || (c == 0 && cj < ci)) {
+          fl = 2u;
+          break;
+        }
+      }
+    }
+  }
+  if (fl) atomicOr(&a.flag[base + list[p]], fl);
+}
+
 // Survivors of the same-bucket pass, in slices order, and their bucket starts
 // sbst[s] = #survivors with fewer than s slices.
 __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a) {
@@ -390,6 +475,7 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
   const long long base = job_base(a, probe, t);
+  const long long tot = (long long)a.n_probes * a.C_probe;
   const int* order = a.order + base;
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
@@ -400,7 +486,10 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
     int off, total;
     Scan(tmp).ExclusiveSum(alive, off, total);
     if (p < n) a.pcnt[base + p] = carry + off;
-    if (alive) a.surv[base + carry + off] = i;
+    if (alive) {
+      a.surv[base + carry + off] = i;
+      for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + carry + off] = a.arr[d * tot + base + i];
+    }
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
@@ -410,7 +499,11 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
   const int* bst = a.bstart + (long long)job * NB;
   int* sb = a.sbst + (long long)job * NB;
   for (int s = threadIdx.x; s < NB; s += blockDim.x) sb[s] = bst[s] >= n ? total : a.pcnt[base + bst[s]];
-  if (threadIdx.x == 0) a.scnt[job] = total;
+  if (threadIdx.x == 0) {
+    a.scnt[job] = total;
+    // survivors with fewer slices precede i in the list: j < i0 + 256
+    push_items(a.wl[1], a.wn + 1, job, total, 1024, true);
+  }
 }
 
 __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args a) {
@@ -437,23 +530,18 @@ __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) a.fcnt[job] = carry;
+  if (threadIdx.x == 0) {
+    a.fcnt[job] = carry;
+    push_items(a.wl[2], a.wn + 2, job, carry, 1024, false);
+  }
 }
 
 template <int D>
-__global__ void __launch_bounds__(256) k_pairs_b(const __grid_constant__ S1Args a, const int* tile_task,
-                                                 const int* tile_start, int tiles_pp, int jchunk) {
-  __shared__ double sh[D * TJ];
-  __shared__ int shc[TJ];
-  const int probe = blockIdx.x / tiles_pp;
-  const int tl = blockIdx.x % tiles_pp;
-  const int t = tile_task[tl];
-  const int i0 = tile_start[tl];
-  const int job = probe * a.T + t;
+__device__ __forceinline__ void pairs_b_tile(const S1Args& a, int job, int i0, int j0, int jchunk,
+                                             double* sh, int* shc) {
+  const int probe = job / a.T, t = job % a.T;
   const int F = a.fcnt[job];
-  if (i0 >= F) return;
-  const int j0 = blockIdx.y * jchunk;
-  if (j0 >= F) return;
+  if (i0 >= F || j0 >= F) return;  // (block-uniform)
   const int j1 = min(F, j0 + jchunk);
   const bool need_cap = F > a.W;
   const long long tot = (long long)a.n_probes * a.C_probe;
@@ -503,6 +591,19 @@ __global__ void __launch_bounds__(256) k_pairs_b(const __grid_constant__ S1Args 
   if (act) {
     if (pos) atomicAdd(&a.fpos[base + i], pos);
     if (cr) atomicAdd(&a.fcr[base + i], cr);
+  }
+}
+
+template <int D>
+__global__ void __launch_bounds__(256) k_pairs_b(const __grid_constant__ S1Args a,
+                                                 const int4* items, const int* n_items, int jchunk) {
+  __shared__ double sh[D * TJ];
+  __shared__ int shc[TJ];
+  const int nw = *n_items;
+  for (int w = blockIdx.x; w < nw; w += gridDim.x) {
+    const int4 it = items[w];
+    pairs_b_tile<D>(a, it.x, it.y, it.z, jchunk, sh, shc);
+    __syncthreads();
   }
 }
 
@@ -682,11 +783,21 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     ++launches;
   }
   if (L.tiles_pp > 0) {
-    dim3 ga((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_a);
+    // grid-stride over the device work lists: enough blocks to fill the SMs
+    const unsigned ga = (unsigned)std::max<long long>(1, std::min<long long>(L.max_items, L.grid));
     PROF_BEGIN(K_PAIRS_A);
-    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a, 0);
+    const unsigned gl = (unsigned)((tot + 255) / 256);
+    if (getenv("JSV_PAIRS_TILED")) {
+      DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1 << 30, 0);
+    } else {
+      DISPATCH_D(a.D, k_pairs_l, gl, a, 0);
+    }
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
-    DISPATCH_D(a.D, k_pairs_a, ga, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_a, 1);
+    if (getenv("JSV_PAIRS_TILED")) {
+      DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
+    } else {
+      DISPATCH_D(a.D, k_pairs_l, gl, a, 1);
+    }
     PROF_END();
     launches += 3;
   }
@@ -695,9 +806,9 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   PROF_END();
   ++launches;
   if (L.tiles_pp > 0) {
-    dim3 gb((unsigned)(a.n_probes * L.tiles_pp), (unsigned)L.jchunks_b);
+    const unsigned gb = (unsigned)std::max<long long>(1, std::min<long long>(L.max_items, L.grid));
     PROF_BEGIN(K_PAIRS_B);
-    DISPATCH_D(a.D, k_pairs_b, gb, a, L.tile_task, L.tile_start, L.tiles_pp, L.jchunk_b);
+    DISPATCH_D(a.D, k_pairs_b, gb, a, a.wl[2], a.wn + 2, 1024);
     PROF_END();
     ++launches;
   }
