@@ -153,19 +153,23 @@ def load_peaks() -> dict:
 
 
 def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
-    """The exhaustive kernel against the SM integer-compare roof.
+    """The exhaustive kernel against the SM instruction-issue roof.
 
     Per candidate the kernel decides four verdicts (capacity, accuracy, latency,
     resources) with one integer comparison each on the candidate's rank record
     -- the per-candidate algorithmic work once the prefix-invariant parts of
-    derive/validate are hoisted.  Roof: the ALU pipe's integer throughput,
-    148 SMs x 64 lanes x 1.965 GHz = 18.6 Tops/s (derived; MEASURED_PEAKS.json
-    holds only HBM and bf16 tensor peaks, neither of which this kernel uses).
+    derive/validate are hoisted.  These are integer lane operations that may
+    issue on either the ALU or the FMA pipe (the SWAR subtractions compile to
+    IMAD.IADD), so the roof is instruction issue: 148 SMs x 4 schedulers x 32
+    lanes x 1.965 GHz = 37.2 T lane-ops/s (derived; MEASURED_PEAKS.json holds
+    only HBM and bf16 tensor peaks, neither of which this kernel uses).
+    `alu_pipe_frac` is the same work against the 64-lane ALU pipe alone.
     """
     ms, cnt = kt.get(dom, (0.0, 0))
     per_launch_ms = ms / max(1, cnt)
     f_clk = 1.965e9
-    peak = 148 * 64 * f_clk / 1e12
+    peak = 148 * 4 * 32 * f_clk / 1e12
+    peak_alu = 148 * 64 * f_clk / 1e12
     ops = tot["exh_candidates"] * 4 / max(1, cnt)
     achieved = ops / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else 0.0
     traffic = None
@@ -175,13 +179,16 @@ def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
             d = json.load(fh).get("k_s2_exh")
         if d:
             traffic = d["dram_read_bytes"] + d["dram_write_bytes"]
-    return {"bound": "int", "kernel": "k_s2_exh", "achieved": achieved, "peak": peak,
+    return {"bound": "issue", "kernel": "k_s2_exh", "achieved": achieved, "peak": peak,
             "unit": "Tops/s", "frac": achieved / peak if peak else None, "traffic": traffic,
             "traffic_note": "DRAM bytes per launch (64 solves) from profiles/ncu_traffic.json; "
                             "algorithmic DRAM bytes ~0 (pools staged in shared memory)",
             "ops_per_candidate": 4, "per_launch_ms": per_launch_ms,
+            "candidates_per_launch": tot["exh_candidates"] / max(1, cnt),
             "share_of_step": ms / max(1e-9, tot["ms_total"]),
-            "peak_source": "derived: 148 SM x 64 ALU lanes x 1.965 GHz (not in MEASURED_PEAKS)"}
+            "alu_pipe_frac": achieved / peak_alu if peak_alu else None,
+            "peak_source": "derived: 148 SM x 4 schedulers x 32 lanes x 1.965 GHz issue "
+                           "(not in MEASURED_PEAKS); ALU pipe alone 148 x 64 x 1.965 GHz"}
 
 
 def cpu_sample(args) -> dict:
