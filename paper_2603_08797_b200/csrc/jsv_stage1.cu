@@ -787,13 +787,15 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     const unsigned ga = (unsigned)std::max<long long>(1, std::min<long long>(L.max_items, L.grid));
     PROF_BEGIN(K_PAIRS_A);
     const unsigned gl = (unsigned)((tot + 255) / 256);
-    if (getenv("JSV_PAIRS_TILED")) {
+    // wide rows (many out-edges) stage j tiles in shared memory instead
+    const bool tiled = a.D > 8 || getenv("JSV_PAIRS_TILED") != nullptr;
+    if (tiled) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1 << 30, 0);
     } else {
       DISPATCH_D(a.D, k_pairs_l, gl, a, 0);
     }
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
-    if (getenv("JSV_PAIRS_TILED")) {
+    if (tiled) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
     } else {
       DISPATCH_D(a.D, k_pairs_l, gl, a, 1);
