@@ -191,6 +191,24 @@ def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
                            "(not in MEASURED_PEAKS); ALU pipe alone 148 x 64 x 1.965 GHz"}
 
 
+def place_plans(app, table, reqs) -> dict:
+    """the cli `plan` tail (cli.py:173-174) -- every plan's
+    instance_segments -> min_gpus -> pack, through placement.py (libjsv host code)."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.placement import instance_segments, min_gpus, pack
+
+    res = P.plan_batch(app, table, reqs)
+    segs = [instance_segments(r.config) for r in res if r.config is not None]
+    reps = 5
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        plans = [pack(s, min_gpus(s)) for s in segs]
+    ms = (time.perf_counter() - t0) * 1e3 / reps
+    return {"plans": len(segs), "ms": ms, "plans_per_s": len(segs) / (ms / 1e3),
+            "instances": sum(len(s) for s in segs), "gpus": sum(p.gpu_count for p in plans),
+            "all_placed": all(p.fully_placed for p in plans)}
+
+
 def cpu_sample(args) -> dict:
     """Oracle port (pure CPython restatement of the reference planner) on the host."""
     from multiprocessing import Pool
@@ -460,6 +478,7 @@ def main() -> None:
         if rank == 0:
             extras["configs3_star12"] = star12_solve(P, torch, flush)
             extras["configs4_traffic840"] = traffic840(P)
+            extras["placement"] = place_plans(app, table, reqs)
 
     t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1]],
                      dtype=torch.float64, device="cuda")

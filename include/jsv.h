@@ -14,11 +14,15 @@
  *                            + validate_configuration() planner.py:329-361
  *   jsv_validate          <- validate_configuration() on a caller-built Configuration
  *   jsv_pool_dump         <- _Search.pools (Stage 1, _candidate_pool 586-635) for parity tests
+ *   jsv_pack              <- placement.pack()      placement.py:163-216 (+ _exact_pack 219-266)
+ *   jsv_min_gpus          <- placement.min_gpus()  placement.py:269-290
  *
  * Conventions: plain C types only, caller-owned host buffers, integer status
  * codes (0 = ok) plus jsv_last_error() (thread-local message).  No C++
- * exception crosses this boundary.  All arithmetic happens on the GPU; the
- * library refuses to run without a CUDA device (there is no CPU fallback).
+ * exception crosses this boundary.  All planner arithmetic happens on the GPU;
+ * the planner entry points refuse to run without a CUDA device (there is no CPU
+ * fallback).  The placement entry points (jsv_pack, jsv_min_gpus) are host
+ * code: sequential bitmask tree walks over a plan's few MIG instances.
  */
 #ifndef JSV_H
 #define JSV_H
@@ -261,6 +265,36 @@ int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
   "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket", "s2_prefix", "s2_exh", \
   "s2_xreduce", "s2_xsort", \
   "fo_prep", "fo_enum", "fo_eval"
+
+/*
+ * Placement of MIG instances onto GPUs (reference placement.py).  A geometry
+ * lists per MIG profile p its allowed (start, footprint width) pairs
+ * [start_off[p], start_off[p+1]) and its first-fit-decreasing rank
+ * order_rank[p] (the reference sorts instances by (-max width, -compute cost,
+ * profile name, index); ranks are that order over profiles, computed by the
+ * caller).  Instances are given as profile indices (MPS never affects packing).
+ */
+typedef struct jsv_geometry {
+  int32_t n_profiles;
+  int32_t slices_per_gpu;      /* <= 30 */
+  const int32_t* start_off;    /* [n_profiles + 1] */
+  const int32_t* start_pos;    /* allowed start offsets */
+  const int32_t* start_width;  /* footprint width per start */
+  const int32_t* order_rank;   /* [n_profiles] */
+} jsv_geometry;
+
+/* pack(instances, gpu_count, geometry, node_budget): per input instance i,
+ * placed[i] = 1 with (gpu[i], start[i], width[i]), or 0 (unplaced).
+ * gpu_count < 0 -> JSV_ERR_CONFIG (GeometryError "gpu_count must be non-negative"). */
+int jsv_pack(const jsv_geometry* geometry, const int32_t* inst_profile, int32_t n,
+             int32_t gpu_count, int64_t node_budget, int32_t* gpu, int32_t* start,
+             int32_t* width, int32_t* placed);
+
+/* min_gpus(instances, geometry, node_budget): *out = the smallest count that
+ * fits every instance, or -1 - i when instance i fits no empty GPU
+ * (GeometryError "instance ... does not fit an empty GPU"). */
+int jsv_min_gpus(const jsv_geometry* geometry, const int32_t* inst_profile, int32_t n,
+                 int64_t node_budget, int32_t* out);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjsv.so")
-SOURCES = ["jsv_api.cu", "jsv_stage1.cu", "jsv_stage2.cu"]
+SOURCES = ["jsv_api.cu", "jsv_stage1.cu", "jsv_stage2.cu", "jsv_place.cu"]
 HEADERS = ["jsv_internal.cuh", "jsv_kernels.h", "jsv_search.cuh", "jsv_exhaustive.cuh", "jsv_fanout.cuh", os.path.join("..", "..", "include", "jsv.h")]
 
 NVCC_FLAGS = [

@@ -74,6 +74,11 @@ class PlanOut(C.Structure):
     ]
 
 
+class Geometry(C.Structure):
+    _fields_ = [("n_profiles", C.c_int32), ("slices_per_gpu", C.c_int32), ("start_off", _I32P),
+                ("start_pos", _I32P), ("start_width", _I32P), ("order_rank", _I32P)]
+
+
 class DemandOut(C.Structure):
     _fields_ = [("demand", C.c_double), ("probes", C.c_int32), ("status", C.c_int32),
                 ("gpu_probes", C.c_int64)]
@@ -113,6 +118,9 @@ EXPORTS = {
     "jsv_set_shard": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
     "jsv_kernel_times": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double),
                                    C.POINTER(C.c_int64)]),
+    "jsv_pack": (C.c_int, [C.POINTER(Geometry), _I32P, C.c_int32, C.c_int32, C.c_int64, _I32P,
+                           _I32P, _I32P, _I32P]),
+    "jsv_min_gpus": (C.c_int, [C.POINTER(Geometry), _I32P, C.c_int32, C.c_int64, _I32P]),
 }
 
 KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",

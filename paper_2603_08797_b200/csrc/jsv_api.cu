@@ -183,6 +183,9 @@ static cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
 }
 
 extern "C" const char* jsv_last_error(void) { return g_err.c_str(); }
+
+// error reporting for the other translation units (jsv_place.cu)
+int jsv_fail_msg(int code, const std::string& msg) { return fail(code, msg); }
 extern "C" int jsv_version(void) { return 1; }
 extern "C" int jsv_device_count(void) {
   int n = 0;
