@@ -46,6 +46,21 @@ def _stale() -> bool:
     return False
 
 
+def build_decoder(verbose: bool = False) -> str:
+    """The CPython result decoder (csrc/jsv_decode.c -> _jsvdecode*.so, in-tree)."""
+    import sysconfig
+
+    out = os.path.join(HERE, "_jsvdecode" + sysconfig.get_config_var("EXT_SUFFIX"))
+    cmd = [shutil.which("gcc") or "gcc", "-O2", "-shared", "-fPIC", "-Wall",
+           "-I" + sysconfig.get_paths()["include"], os.path.join(CSRC, "jsv_decode.c"),
+           "-o", out + ".tmp"]
+    if verbose:
+        print(" ".join(cmd), file=sys.stderr)
+    subprocess.run(cmd, check=True)
+    os.replace(out + ".tmp", out)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
@@ -54,6 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)
     os.replace(LIB + ".tmp", LIB)
+    build_decoder(verbose)
     return LIB
 
 

@@ -184,7 +184,48 @@ def _result_from(out: N.PlanOut, app, lw: LW.Lowered, request, wall_ms: float) -
     return _results_from((N.PlanOut * 1).from_buffer_copy(out), [app], lw, [request], wall_ms)[0]
 
 
+try:  # C decoder (csrc/jsv_decode.c); the Python decoder below is its reference
+    from . import _jsvdecode as _DEC
+except ImportError:  # pragma: no cover - built by __graft_entry__.build()
+    _DEC = None
+_DEC_LAYOUT = None
+
+
+def _dec_meta(app, lw: LW.Lowered) -> tuple:
+    """Per-(graph, lowering) tables of the C decoder, cached on the lowering."""
+    g = app.graph
+    hit = lw.arrays.get("_dec_meta")
+    if hit is not None and hit[0] is g:
+        return hit[1]
+    idx = lw.index
+    topo_t = tuple(g.topological_order)
+    task_t = tuple(g.task_ids)
+    edges = [((t, d), lw.edge_index[(t, d)]) for t in task_t for d in g.successors[t]]
+    keys_full = tuple(tuple((t,) + k for k in lw.keys[ti]) for ti, t in enumerate(lw.ids))
+    meta = (tuple(lw.ids), keys_full, topo_t, tuple(idx[t] for t in topo_t), task_t,
+            tuple(idx[t] for t in task_t), tuple(e for e, _ in edges), tuple(k for _, k in edges),
+            tuple(lw.paths), tuple("->".join(p) for p in lw.paths), float(lw.a_max),
+            tuple(N.BINDING_NAMES[k] for k in range(len(N.BINDING_NAMES))),
+            PlanResult, Configuration, ConstraintVerdict, SolverStats)
+    lw.arrays["_dec_meta"] = (g, meta)
+    return meta
+
+
 def _results_from(outs, apps, lw: LW.Lowered, requests, wall_ms: float) -> list[PlanResult]:
+    """jsv_plan_out records -> PlanResults (C decoder when built, else _results_py)."""
+    global _DEC_LAYOUT
+    if _DEC is None:
+        return _results_py(outs, apps, lw, requests, wall_ms)
+    if _DEC_LAYOUT is None:
+        lay = {name: getattr(N.PlanOut, name).offset for name, _ in N.PlanOut._fields_}
+        lay["size"] = C.sizeof(N.PlanOut)
+        lay["max_items"] = N.MAX_ITEMS
+        _DEC_LAYOUT = lay
+    return _DEC.decode(outs, len(requests), _DEC_LAYOUT, _dec_meta(apps[0], lw),
+                       [r.demand_rps for r in requests], float(wall_ms))
+
+
+def _results_py(outs, apps, lw: LW.Lowered, requests, wall_ms: float) -> list[PlanResult]:
     """Decode a ctypes array of jsv_plan_out records into PlanResults.
 
     Every field is pulled out of the records once, batch-wide, through a numpy

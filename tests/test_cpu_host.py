@@ -392,3 +392,61 @@ def test_batch_decode_equals_per_field_decode(name):
         assert got[i] == want
         assert plan_result_to_dict(got[i]) == plan_result_to_dict(want)
         assert repr(got[i]) == repr(want)
+
+
+@pytest.mark.parametrize("name", ["ar-assistant", "traffic-analysis", "social-media"])
+def test_c_decoder_equals_python_decoder(name):
+    """csrc/jsv_decode.c builds exactly the objects planner._results_py builds."""
+    import json
+
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace, plan_result_to_dict
+
+    assert P._DEC is not None, "the C decoder (_jsvdecode) is not built"
+    with open(os.path.join(os.path.dirname(__file__), "golden", "apps.json")) as fh:
+        doc = json.load(fh)[name]
+    app = app_from_dict(doc["app"])
+    lw = LW.lower(app, profile_from_rows(doc["profile"]))
+    rng = random.Random(11)
+    n = 40
+    outs = (N.PlanOut * n)()
+    T, E, Pn = len(lw.ids), len(lw.edges), len(lw.paths)
+    reqs = []
+    for i, o in enumerate(outs):
+        o.has_config = int(i % 6 != 0)
+        o.feasible = int(i % 3 != 0)
+        o.binding = rng.randrange(-1, 5)
+        o.objective, o.a_obj = rng.random(), rng.random()
+        o.nodes = rng.randrange(1 << 40)
+        o.total_slices = rng.randrange(900)
+        o.uncovered_mask = rng.randrange(1 << T) if i % 4 == 0 else 0
+        o.res_margin = rng.choice([rng.uniform(-5, 5), 0.0, -0.0, float("nan")])
+        o.acc_margin = rng.uniform(-1, 1)
+        for ti in range(T):
+            o.pool_size[ti] = rng.randrange(500)
+            o.pool_present[ti] = rng.randrange(2)
+            o.truncated[ti] = rng.randrange(2)
+            o.n_items[ti] = rng.randrange(N.MAX_ITEMS + 1)
+            for k in range(o.n_items[ti]):
+                o.items[ti][k] = (rng.randrange(len(lw.keys[ti])) << 16) | rng.randrange(1, 900)
+                o.hput[ti][k] = rng.uniform(0, 900)
+            o.latency[ti], o.capacity[ti] = rng.uniform(0, 500), rng.uniform(0, 900)
+            o.demand[ti], o.accuracy[ti] = rng.uniform(0, 900), rng.random()
+            o.slices[ti] = rng.randrange(30)
+            o.thr_margin[ti] = rng.uniform(-50, 50)
+        for e in range(E):
+            o.fanout[e] = rng.uniform(0, 3)
+        for p in range(Pn):
+            o.path_acc[p], o.lat_margin[p] = rng.random(), rng.uniform(-100, 100)
+        reqs.append(PlanRequest(100.0 + i * 0.5, 28, SearchSpace(True, True, True)))
+    got = P._results_from(outs, [app] * n, lw, reqs, 1.25)
+    want = P._results_py(outs, [app] * n, lw, reqs, 1.25)
+    assert len(got) == n
+    for g, w in zip(got, want):
+        assert repr(g) == repr(w)
+        # (json text: NaN margins compare equal as text, not as floats)
+        assert json.dumps(plan_result_to_dict(g)) == json.dumps(plan_result_to_dict(w))
+        assert type(g) is type(w) and type(g.stats) is type(w.stats)
+        if w.config is not None:
+            assert g.config.m == w.config.m and list(g.config.hput) == list(w.config.hput)
+            assert list(g.config.demand_rps) == list(w.config.demand_rps)
