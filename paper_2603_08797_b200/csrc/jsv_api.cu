@@ -78,7 +78,7 @@ enum BufId {
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
-  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_COUNT
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_COUNT
 };
 
 struct jsv_context {
@@ -642,7 +642,7 @@ struct BatchState {
 };
 
 static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe* probes,
-                      BatchState& bs) {
+                      BatchState& bs, int n_s1, const std::vector<int>& rep) {
   jsv_context& c = *p.ctx;
   cudaStream_t st = c.st;
   int rc = get_s1plan(p, rq, bs.pl);
@@ -716,7 +716,9 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.tb = p.dt;
   a.rq = B[B_REQ].as<DReq>();
   a.probes = B[B_PROBES].as<DProbe>();
-  a.n_probes = n; a.T = T; a.maxi = pl.maxi; a.D = D; a.W = W; a.maxout = p.maxout;
+  // Stage 1 runs on the first n_s1 probes (distinct Stage-1 inputs); k_s1_expand
+  // copies their pools to the duplicate probes n_s1 .. n-1 afterwards
+  a.n_probes = n_s1; a.T = T; a.maxi = pl.maxi; a.D = D; a.W = W; a.maxout = p.maxout;
   a.C_probe = pl.C_probe;
   long long acc = 0;
   for (int t = 0; t < T; ++t) {
@@ -797,6 +799,12 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   L.jchunks_b = L.jchunks_a;
   c.stats.kernel_launches += launch_stage1(a, L, st);
   CK(cudaGetLastError());
+  if (n_s1 < n) {
+    CK(B[B_REP].ensure(sizeof(int) * n));
+    CK(cudaMemcpyAsync(B[B_REP].p, rep.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    c.stats.kernel_launches += launch_stage1_expand(a, B[B_REP].as<int>(), n_s1, n, st);
+    CK(cudaGetLastError());
+  }
   bs.n = n;
   bs.pool_n.resize(jobs);
   CK(cudaMemcpyAsync(bs.pool_n.data(), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
@@ -1096,10 +1104,20 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
                           std::vector<int>& active) {
   jsv_context& c = *p.ctx;
   if (c.strategy == JSV_STRATEGY_SEARCH) return JSV_OK;
-  // feasibility probes (max_demand): the branch-and-bound stops at the first
-  // feasible leaf and prunes infeasible probes early; the sweep would prove
-  // infeasibility by visiting everything.  Auto keeps the sweep for full plans.
-  if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) return JSV_OK;
+  // Feasibility probes (max_demand) under auto: the level-synchronous
+  // branch-and-bound prunes infeasible probes early but cannot stop at the first
+  // feasible leaf (it materialises whole levels: millions of prefixes at low
+  // demand), while the sweep stops as soon as any block finds one.  So the sweep
+  // first scans a budget of each probe's index space from the front (DFS order:
+  // a leaf found there is the first feasible leaf overall); probes decided there
+  // -- found, or swept completely -- are done, the rest go to the search.
+  long long fo_budget = 0;
+  if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) {
+    if (c.shard_world > 1 || getenv("JSV_NO_FEAS_SWEEP")) return JSV_OK;
+    fo_budget = 1LL << 20;
+    if (const char* e = getenv("JSV_FEAS_BUDGET")) fo_budget = std::max(1LL, atoll(e));
+  }
+  std::vector<int> truncated(bs.n, 0);
   cudaStream_t st = c.st;
   auto& B = c.buf;
   const int n = bs.n, T = p.T;
@@ -1128,6 +1146,13 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     x.q0 = (long long)((__int128)Q * c.shard_rank / c.shard_world);
     const long long q1 = (long long)((__int128)Q * (c.shard_rank + 1) / c.shard_world);
     x.nq = q1 - x.q0;
+    if (fo_budget > 0) {
+      const long long cap = std::max<long long>(1, fo_budget / x.R);
+      if (x.nq > cap) {
+        x.nq = cap;
+        truncated[i] = 1;
+      }
+    }
     int glog = 0;
     while ((1 << glog) < x.R && glog < 5) ++glog;
     x.glog = glog;
@@ -1267,6 +1292,17 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   a.part = B[B_XPART].as<XPart>();
   c.stats.kernel_launches += launch_stage2_exhaustive(a, grid, p.P, smem, st);
   CK(cudaGetLastError());
+  bool any_trunc = false;
+  for (int i = 0; i < n; ++i) any_trunc = any_trunc || truncated[i];
+  if (any_trunc) {
+    // budgeted feasibility sweep: undecided probes (nothing found in the scanned
+    // front of a larger space) continue with the branch-and-bound
+    std::vector<BestRec> best(n);
+    CK(cudaMemcpyAsync(best.data(), B[B_BEST].p, sizeof(BestRec) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int i = 0; i < n; ++i)
+      if (truncated[i] && !best[i].has) active[i] = 1;
+  }
   return JSV_OK;
 }
 
@@ -1394,12 +1430,50 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   if (rq.n_mix < 0 || rq.n_mix > JSV_MAX_MIX) return fail(JSV_ERR_ARG, "too many mix fractions");
   BatchState bs;
   bs.feasible_only = rq.feasible_only;
+  // Stage 1 (planner.py:586-635) reads a probe only through its demand upper
+  // bounds r_upper: probes with identical bounds (a sweep's shared doubling
+  // points, coinciding bisection brackets) get one Stage-1 computation.  The
+  // batch is permuted so the distinct probes come first; outputs are permuted
+  // back at the end.
+  std::vector<DProbe> fp(n);
+  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i]);
+  std::vector<int> perm;  // batch slot -> caller index
+  std::vector<int> rep;   // batch slot -> slot whose Stage-1 pools it shares
+  int n_s1 = n;
+  {
+    std::map<std::string, int> seen;
+    std::vector<int> first, dups, dup_rep;
+    for (int i = 0; i < n; ++i) {
+      std::string key(reinterpret_cast<const char*>(fp[i].r_upper[0]), sizeof(double) * p.T);
+      key.append(reinterpret_cast<const char*>(fp[i].r_upper[1]), sizeof(double) * p.T);
+      auto it = seen.find(key);
+      if (it == seen.end() || getenv("JSV_NO_S1DEDUP")) {
+        seen.emplace(key, (int)first.size());
+        first.push_back(i);
+      } else {
+        dups.push_back(i);
+        dup_rep.push_back(it->second);
+      }
+    }
+    n_s1 = (int)first.size();
+    perm = first;
+    perm.insert(perm.end(), dups.begin(), dups.end());
+    rep.resize(n);
+    for (int k = 0; k < n_s1; ++k) rep[k] = k;
+    for (size_t k = 0; k < dups.size(); ++k) rep[n_s1 + k] = dup_rep[k];
+  }
   bs.probes.resize(n);
-  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], bs.probes[i]);
+  for (int k = 0; k < n; ++k) bs.probes[k] = fp[perm[k]];
+  std::vector<jsv_plan_out> pout;
+  jsv_plan_out* out_caller = out;
+  if (n_s1 < n) {
+    pout.resize(n);
+    out = pout.data();
+  }
   JSV_T("batch begin");
-  if (timing_on()) fprintf(stderr, "[jsv t] probes %d\n", n);
+  if (timing_on()) fprintf(stderr, "[jsv t] probes %d (stage-1 distinct %d)\n", n, n_s1);
   CK(cudaEventRecord(c.ev[0], st));
-  int rc = run_stage1(p, rq, n, bs.probes.data(), bs);
+  int rc = run_stage1(p, rq, n, bs.probes.data(), bs, n_s1, rep);
   if (rc) return rc;
   JSV_T("stage1 done");
   CK(cudaEventRecord(c.ev[1], st));
@@ -1448,6 +1522,8 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   CK(cudaEventRecord(c.ev[2], st));
   rc = finalize(p, bs, !informed, out, &nodes);
   if (rc) return rc;
+  if (out != out_caller)
+    for (int k = 0; k < n; ++k) out_caller[perm[k]] = out[k];
   CK(cudaEventRecord(c.ev[3], st));
   CK(cudaEventSynchronize(c.ev[3]));
   JSV_T("finalize done");
@@ -1540,6 +1616,13 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
       pr[k] = points[work[k].first];
       pr[k].demand = work[k].second;
       gpu_probes[work[k].first]++;
+    }
+    if (getenv("JSV_DEBUG_DUP")) {
+      std::vector<double> dd;
+      for (auto& w : work) dd.push_back(w.second);
+      std::sort(dd.begin(), dd.end());
+      const size_t distinct = std::unique(dd.begin(), dd.end()) - dd.begin();
+      fprintf(stderr, "[jsv dup] probes %zu distinct demands %zu\n", work.size(), distinct);
     }
     std::vector<jsv_plan_out> res(work.size());
     int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.data(), false);
@@ -1806,7 +1889,7 @@ extern "C" int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const js
   BatchState bs;
   bs.probes.resize(1);
   fill_probe(p, *req, *probe, bs.probes[0]);
-  int rc = run_stage1(p, *req, 1, bs.probes.data(), bs);
+  int rc = run_stage1(p, *req, 1, bs.probes.data(), bs, 1, std::vector<int>{0});
   if (rc) return rc;
   const S1Args& a = bs.s1;
   const int P = bs.pool_n[task];

@@ -107,6 +107,7 @@ struct S1Launch {
 
 int stage1_padded_dims(int D);
 int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st);
+int launch_stage1_expand(const S1Args& a, const int* rep, int n_s1, int n, cudaStream_t st);
 
 // ------------------------------------------------------------------ stage 2
 

@@ -733,6 +733,48 @@ __global__ void k_mrank(const __grid_constant__ S1Args a) {
   else a.rank_m[q] = (uint16_t)rank;
 }
 
+// Duplicate probes (identical Stage-1 inputs, see plan_batch_internal): copy the
+// representative's pools -- every per-job array Stage 2 and finalize read -- and
+// the item lists of its pool candidates (same local candidate index) into the
+// duplicate's slots.  One block per (duplicate probe, task).
+__global__ void __launch_bounds__(256) k_s1_expand(const __grid_constant__ S1Args a,
+                                                   const int* rep, int n_s1) {
+  const int d = n_s1 + blockIdx.x / a.T, t = blockIdx.x % a.T;
+  const int u = rep[d];
+  const int jd = d * a.T + t, ju = u * a.T + t;
+  const int W = a.W;
+  const int np = a.pool_n[ju];
+  if (threadIdx.x == 0) {
+    a.pool_n[jd] = np;
+    a.pool_trunc[jd] = a.pool_trunc[ju];
+    a.pool_min_lat2[jd] = a.pool_min_lat2[ju];
+    a.pool_min_sl[jd] = a.pool_min_sl[ju];
+    a.pool_acc_ub[jd] = a.pool_acc_ub[ju];
+    a.cnt[jd] = a.cnt[ju];
+    a.fcnt[jd] = a.fcnt[ju];
+  }
+  const long long bd = job_base(a, d, t), bu = job_base(a, u, t);
+  for (int k = threadIdx.x; k < np; k += blockDim.x) {
+    const long long qd = (long long)jd * W + k, qu = (long long)ju * W + k;
+    const int c = a.pool_cand[qu];
+    a.pool_cand[qd] = c;
+    a.p_sl[qd] = a.p_sl[qu];
+    a.p_cap[qd] = a.p_cap[qu];
+    a.p_acc[qd] = a.p_acc[qu];
+    a.p_lat[qd] = a.p_lat[qu];
+    for (int e = 0; e < a.maxout; ++e) a.p_fan[qd * a.maxout + e] = a.p_fan[qu * a.maxout + e];
+    const int ni = a.nitems[bu + c];
+    a.nitems[bd + c] = ni;
+    for (int m = 0; m < ni; ++m) a.items[(bd + c) * a.maxi + m] = a.items[(bu + c) * a.maxi + m];
+  }
+}
+
+int launch_stage1_expand(const S1Args& a, const int* rep, int n_s1, int n, cudaStream_t st) {
+  if (n <= n_s1) return 0;
+  k_s1_expand<<<(unsigned)((n - n_s1) * a.T), 256, 0, st>>>(a, rep, n_s1);
+  return 1;
+}
+
 // ------------------------------------------------------------------ launchers
 
 static int pick_D(int D) {
