@@ -1423,7 +1423,7 @@ static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active) 
 
 // plan() for a batch of probes sharing one request
 static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, const jsv_probe* in,
-                               jsv_plan_out* out, bool want_config) {
+                               jsv_plan_out* out, bool want_config, bool feas_only = false) {
   jsv_context& c = *p.ctx;
   cudaStream_t st = c.st;
   if (rq.pareto_width < 1 || rq.pareto_width > 32766) return fail(JSV_ERR_ARG, "pareto_width");
@@ -1516,6 +1516,28 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     if (any) {
       rc = run_stage2(p, bs, true, want_config, redo, nullptr);
       if (rc) return rc;
+    }
+    if (feas_only && !want_config) {
+      // max_demand probes need only the verdict: a feasible leaf was found
+      // (every found leaf passed derive/validate), no derivation of outputs
+      CK(cudaEventRecord(c.ev[2], st));
+      CK(cudaEventRecord(c.ev[3], st));
+      CK(cudaEventSynchronize(c.ev[3]));
+      for (int k = 0; k < n; ++k) {
+        jsv_plan_out& o = out_caller[perm[k]];
+        memset(&o, 0, sizeof(o));
+        o.feasible = (!bs.dead[k] && best[k].has) ? 1 : 0;
+        o.dead = bs.dead[k];
+      }
+      collect_prof(c);
+      float ms1 = 0, ms2 = 0, mst = 0;
+      cudaEventElapsedTime(&ms1, c.ev[0], c.ev[1]);
+      cudaEventElapsedTime(&ms2, c.ev[1], c.ev[2]);
+      cudaEventElapsedTime(&mst, c.ev[0], c.ev[3]);
+      c.stats.ms_stage1 += ms1;
+      c.stats.ms_stage2 += ms2;
+      c.stats.ms_total += mst;
+      return JSV_OK;
     }
   }
   JSV_T("stage2 done");
@@ -1625,7 +1647,7 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
       fprintf(stderr, "[jsv dup] probes %zu distinct demands %zu\n", work.size(), distinct);
     }
     std::vector<jsv_plan_out> res(work.size());
-    int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.data(), false);
+    int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.data(), false, true);
     if (rc) return rc;
     feas.resize(work.size());
     for (size_t k = 0; k < work.size(); ++k) feas[k] = res[k].feasible;
