@@ -364,10 +364,18 @@ def main() -> None:
     import torch
     import torch.distributed as dist
 
+    # JSV_BENCH_ONE_GPU=1 (tests only): every rank on GPU 0 with gloo plumbing, to
+    # exercise the multi-rank path on a one-GPU box; real runs: one GPU per rank, NCCL
+    one_gpu = os.environ.get("JSV_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     os.environ["JSV_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2603_08797_b200 import _native as N
     from paper_2603_08797_b200 import planner as P
@@ -481,11 +489,13 @@ def main() -> None:
             extras["placement"] = place_plans(app, table, reqs)
 
     t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1]],
-                     dtype=torch.float64, device="cuda")
+                     dtype=torch.float64, device="cpu" if one_gpu else "cuda")
+    tc = torch.tensor([float(tot["exh_candidates"])], dtype=torch.float64, device=t.device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(tc, op=dist.ReduceOp.SUM)  # every rank's own demand points
     dev_ms_max, e2e_ms_max, sweep_ms_max = t.tolist()
-    total_cand = cand_step * args.steps * world
+    total_cand = int(tc.item())
     value = total_cand / (dev_ms_max / 1e3)
     e2e_value = total_cand / (e2e_ms_max / 1e3)
     h2d = args.batch * ctypes.sizeof(N.Probe) + ctypes.sizeof(N.Request)

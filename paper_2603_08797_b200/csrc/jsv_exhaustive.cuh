@@ -44,11 +44,19 @@
 // lexicographic comparison (ties on m resolved by the canonical item lists).
 
 __device__ __forceinline__ void x_digits(const XProbe& xp, int T, long long idx, uint16_t* ch) {
+  unsigned long long v = (unsigned long long)idx;
   for (int k = T - 1; k >= 0; --k) {
-    const long long r = xp.radix[k];
-    const int d = (int)(idx % r);
-    idx /= r;
-    ch[k] = (d == xp.pn[k]) ? (uint16_t)NONE16 : (uint16_t)d;
+    const unsigned r = (unsigned)xp.radix[k];
+    unsigned d;
+    if (v < 0x100000000ull) {  // 32-bit division once the remaining index fits
+      const unsigned v32 = (unsigned)v;
+      d = v32 % r;
+      v = v32 / r;
+    } else {
+      d = (unsigned)(v % r);
+      v /= r;
+    }
+    ch[k] = (d == (unsigned)xp.pn[k]) ? (uint16_t)NONE16 : (uint16_t)d;
   }
 }
 
