@@ -93,6 +93,20 @@ struct jsv_context {
   int strategy = JSV_STRATEGY_AUTO;
   long long exh_limit = 1LL << 31;
   int shard_rank = 0, shard_world = 1;
+  // pinned host staging for per-solve tables (one async copy instead of several
+  // pageable ones); reused call to call -- every call synchronises before returning
+  void* hpin = nullptr;
+  size_t hpin_cap = 0;
+  void* pinned(size_t bytes) {
+    if (bytes > hpin_cap) {
+      if (hpin) cudaFreeHost(hpin);
+      hpin = nullptr;
+      hpin_cap = 0;
+      if (cudaHostAlloc(&hpin, bytes * 2, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+      hpin_cap = bytes * 2;
+    }
+    return hpin;
+  }
 };
 
 thread_local Prof* g_prof = nullptr;
@@ -219,6 +233,7 @@ extern "C" void jsv_context_destroy(jsv_context* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->st) cudaStreamDestroy(ctx->st);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
   delete ctx;
 }
 
@@ -1163,6 +1178,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     ++nx;
   }
   if (nx == 0) return JSV_OK;
+  JSV_T("exh: probes planned");
   // warp-rounds (x_slots(P) prefixes each) of every probe, concatenated
   const int n_slots = x_slots(p.P);
   std::vector<long long> roff(n + 1, 0), poff(2 * (n + 1), 0);
@@ -1185,6 +1201,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   if (getenv("JSV_NO_RPL")) reg = 0;
   for (int i = 0; i < n; ++i)
     if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
+  JSV_T("exh: before xprobe copy");
   CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
   CK(cudaMemcpyAsync(B[B_XPROBE].p, xp.data(), sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
   CK(B[B_ACTIVE].ensure(sizeof(int) * n));
@@ -1222,6 +1239,10 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   }
   if (getenv("JSV_NO_FAST")) a.fast = 0;
   if (getenv("JSV_NO_TMA")) a.tma = 0;
+  // the sink-pool rank tables only need the probes: sort them while the host
+  // plans the chunk schedule
+  c.stats.kernel_launches += launch_x_rank(a, st);
+  JSV_T("exh: before chunk plan");
   // persistent blocks take chunks -- contiguous warp-round ranges of the
   // concatenation -- from a counter; chunk sizes are guided (a fraction of the
   // remaining modelled cost: prefix derivation + a sweep proportional to the sink
@@ -1262,6 +1283,8 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     }
   }
   const long long n_chunks = (long long)cstart.size() - 1;
+  if (timing_on()) fprintf(stderr, "[jsv t] exh: %lld chunks over %lld rounds, grid %lld\n", n_chunks, n_rounds, G);
+  JSV_T("exh: chunks planned");
   for (int i = 0; i < n; ++i) {
     const long long r0 = roff[i], r1 = roff[i + 1];
     if (r0 == r1) continue;
@@ -1273,15 +1296,18 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   }
   CK(B[B_XBOFF].ensure(sizeof(long long) * (3 * (n + 1) + n_chunks + 2)));
   CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)(n_chunks + n)));
-  CK(cudaMemcpyAsync(B[B_XBOFF].p, poff.data(), sizeof(long long) * 2 * (n + 1),
-                     cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(B[B_XBOFF].as<long long>() + 2 * (n + 1), roff.data(),
-                     sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(B[B_XBOFF].as<long long>() + 3 * (n + 1), cstart.data(),
-                     sizeof(long long) * (n_chunks + 1), cudaMemcpyHostToDevice, st));
-  // the chunk counter (zeroed per launch) follows the chunk starts
-  CK(cudaMemsetAsync(B[B_XBOFF].as<long long>() + 3 * (n + 1) + n_chunks + 1, 0,
-                     sizeof(long long), st));
+  {
+    // part-slot ranges, round offsets, chunk starts and the zeroed chunk counter:
+    // one copy from pinned staging
+    const size_t words = 3 * (size_t)(n + 1) + (size_t)n_chunks + 2;
+    long long* h = static_cast<long long*>(c.pinned(sizeof(long long) * words));
+    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    memcpy(h, poff.data(), sizeof(long long) * 2 * (n + 1));
+    memcpy(h + 2 * (n + 1), roff.data(), sizeof(long long) * (n + 1));
+    memcpy(h + 3 * (n + 1), cstart.data(), sizeof(long long) * (n_chunks + 1));
+    h[words - 1] = 0;
+    CK(cudaMemcpyAsync(B[B_XBOFF].p, h, sizeof(long long) * words, cudaMemcpyHostToDevice, st));
+  }
   a.boff = B[B_XBOFF].as<long long>();
   a.roff = B[B_XBOFF].as<long long>() + 2 * (n + 1);
   a.cstart = B[B_XBOFF].as<long long>() + 3 * (n + 1);
@@ -1290,7 +1316,8 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
                                                  n_chunks + 1);
   const long long grid = std::min(G, n_chunks);
   a.part = B[B_XPART].as<XPart>();
-  c.stats.kernel_launches += launch_stage2_exhaustive(a, grid, p.P, smem, st);
+  JSV_T("exh: before launch");
+  c.stats.kernel_launches += launch_stage2_exhaustive(a, grid, p.P, smem, st, true);
   CK(cudaGetLastError());
   bool any_trunc = false;
   for (int i = 0; i < n; ++i) any_trunc = any_trunc || truncated[i];
@@ -1482,9 +1509,11 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   if (informed) {
     rc = stage2_prep(p, bs);
     if (rc) return rc;
+    JSV_T("s2 prep issued");
     std::vector<int> active(n, 1);
     rc = run_exhaustive(p, bs, want_config, active);
     if (rc) return rc;
+    JSV_T("exhaustive issued");
     rc = run_fanout(p, bs, active);
     if (rc) return rc;
     long long nn = 0;
@@ -1495,11 +1524,13 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
       if (rc) return rc;
     }
     c.stats.nodes += nn;
+    JSV_T("search issued");
     // infeasible full plans: diagnostic re-run for the binding constraint
     std::vector<BestRec> best(n);
     CK(cudaMemcpyAsync(best.data(), c.buf[B_BEST].p, sizeof(BestRec) * n, cudaMemcpyDeviceToHost,
                        st));
     CK(cudaStreamSynchronize(st));
+    JSV_T("stage2 synced");
     std::vector<int> redo(n, 0);
     bool any = false;
     if (getenv("JSV_DEBUG"))

@@ -1,3 +1,4 @@
+#include <map>
 // jsv_exhaustive.cuh -- exhaustive Stage 2: every allocation of the Stage-1
 // cross-product is derived, validated and folded into the argmax (included by
 // jsv_stage2.cu).
@@ -1070,21 +1071,52 @@ size_t x_smem_bytes(int max_pn_last, int P, bool rank) {
                            (int)smem);                                                        \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_s2_exh<PMV, F, RP>, XBLOCK, smem); \
   } while (0)
-#define JSV_XLAUNCH(PMV, F, RP) k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a)
+#define JSV_XLAUNCH(PMV, F, RP)                                                                \
+  do {                                                                                        \
+    if (smem > 40 * 1024)                                                                     \
+      cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                           (int)smem);                                                        \
+    k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a);                            \
+  } while (0)
 
 long long x_resident_blocks(const XArgs& a, int P, size_t smem) {
   int dev = 0, n_sm = 148, per_sm = 1;
   cudaGetDevice(&dev);
+  // the occupancy query costs tens of microseconds of host time on every solve:
+  // memoise it per (device, kernel instance, shared memory)
+  const int inst = (P <= 1 ? 0 : P <= 2 ? 1 : P <= 4 ? 2 : P <= 8 ? 3 : P <= 16 ? 4 : 5) * 8 +
+                   (a.fast ? 4 : 0) + (a.rpl ? 2 : 0);
+  const long long key = ((long long)dev << 48) ^ ((long long)inst << 32) ^ (long long)smem;
+  static thread_local std::map<long long, long long> memo;
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
   JSV_XDISPATCH(JSV_XOCC);
-  return (long long)(per_sm > 0 ? per_sm : 1) * n_sm;
+  const long long r = (long long)(per_sm > 0 ? per_sm : 1) * n_sm;
+  memo[key] = r;
+  return r;
+}
+
+// rank tables of the sink pools (rank-space probes); issued before the host
+// plans the chunk schedule so the two overlap
+int launch_x_rank(const XArgs& a, cudaStream_t st) {
+  if (!a.fast) return 0;
+  int n2 = 1;
+  while (n2 < a.max_pn_last) n2 <<= 1;
+  const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;
+  if (sm2 > 40 * 1024)
+    cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  PROF_BEGIN(K_S2_XSORT);
+  k_x_rank<<<a.s.n_probes, 512, sm2, st>>>(a, n2);
+  PROF_END();
+  return 1;
 }
 
 int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
-                             cudaStream_t st) {
+                             cudaStream_t st, bool rank_done) {
   if (grid <= 0) return 0;
   int launches = 0;
-  if (a.fast) {
+  if (a.fast && !rank_done) {
     int n2 = 1;
     while (n2 < a.max_pn_last) n2 <<= 1;
     const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;

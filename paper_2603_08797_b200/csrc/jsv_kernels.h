@@ -237,8 +237,9 @@ __host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <=
 __host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) & ~127; }
 size_t x_smem_bytes(int max_pn_last, int P, bool rank);
 long long x_resident_blocks(const XArgs& a, int P, size_t smem);
+int launch_x_rank(const XArgs& a, cudaStream_t st);
 int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
-                             cudaStream_t st);
+                             cudaStream_t st, bool rank_done = false);
 
 // fan-out graphs (jsv_fanout.cuh)
 #define FO_DELTA_W 1e-9   // slack on real-valued accuracy sums (>> float error)
