@@ -63,3 +63,21 @@ def test_c3_grid_sharded_points(grid):
         out[lo:hi] = P.max_demand_grid(apps[lo:hi], table, 28, SearchSpace(True, True, True))
     for d, r in zip(docs, out):
         assert r.demand_rps == d["demand"], d["name"]
+
+
+@pytest.mark.parametrize("env", [{"JSV_FEAS_BUDGET": "1"}, {"JSV_FEAS_BUDGET": str(1 << 40)},
+                                 {"JSV_NO_FEAS_SWEEP": "1"}, {"JSV_NO_S1DEDUP": "1"}])
+def test_c3_grid_probe_paths_agree(grid, env, monkeypatch):
+    """The feasibility pre-sweep (every probe undecided -> search; every probe
+    decided by the sweep; off) and the per-demand Stage-1 dedupe (off) are pure
+    performance paths: the sweep's demands and probe counts stay the reference's."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    docs, apps, table = grid
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    res = P.max_demand_grid(apps[::4], table, 28, SearchSpace(True, True, True), 0.05, None, 1e-3)
+    for d, r in zip(docs[::4], res):
+        assert (r.demand_rps, r.probes) == (d["demand"], d["probes"]), d["name"]
+        assert result_dict(r.plan) == d["plan"], d["name"]
