@@ -59,3 +59,38 @@ def test_max_demand_matches_reference(P, doc):
     assert r.demand_rps == doc["demand"]
     assert r.probes == doc["probes"]
     assert result_dict(r.plan) == doc["plan"]
+
+
+def test_bench_batch_strategies_agree_at_full_size():
+    """The bench workload itself (64 XR solves at 240..712 rps, ~1.9e9
+    allocations per batch): the exhaustive sweep, the branch-and-bound and the
+    one-at-a-time plan() calls return identical results -- three independent
+    traversals of the same space (size-independent parity check at full size),
+    and the sweep really evaluated every allocation of every cross-product."""
+    import bench
+    from paper_2603_08797_b200 import planner
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace, plan_result_to_dict
+
+    app, table = bench.xr_inputs()
+    reqs = [PlanRequest(d, 28, SearchSpace(True, True, True)) for d in bench.demand_points(64, 0, 1)]
+
+    def strip(r):
+        d = plan_result_to_dict(r)
+        d["stats"].pop("nodes")
+        d["stats"].pop("wall_ms", None)
+        return d
+
+    try:
+        planner.set_strategy("exhaustive", 1 << 40)
+        exh = planner.plan_batch(app, table, reqs)
+        st = planner.last_stats()
+        covered = sum(bench.covered(app, r, q.demand_rps) for r, q in zip(exh, reqs))
+        assert st["exh_candidates"] == covered and st["leaves"] == covered
+        planner.set_strategy("search")
+        srch = planner.plan_batch(app, table, reqs)
+    finally:
+        planner.set_strategy("auto")
+    one = [planner.plan(app, table, q) for q in reqs[::8]]
+    assert all(r.feasible for r in exh)
+    assert [strip(r) for r in exh] == [strip(r) for r in srch]
+    assert [strip(r) for r in exh[::8]] == [strip(r) for r in one]
