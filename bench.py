@@ -239,6 +239,23 @@ def cpu_sample(args) -> dict:
             "solve_ms": wall * 1e3 * cores / n, "evaluated": sum(o[1] for o in outs)}
 
 
+def cpu_sweep_sample(app) -> dict:
+    """configs[2] on the host: the oracle port's max_demand for two of the 64 grid
+    points (one core), next to the GPU sweep's points/s."""
+    from oracle import planner_oracle as O
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    _app, table = xr_inputs()
+    pts = c3_apps(app)[::37]
+    t0 = time.perf_counter()
+    for a in pts:
+        O.max_demand(a, table, SLICE_BUDGET, SearchSpace(True, True, True))
+    wall = time.perf_counter() - t0
+    return {"value": len(pts) / wall, "unit": "points/s", "cores": 1, "kind": "port",
+            "sample": f"{len(pts)} grid points (max_demand, rel_tol 1e-3) by oracle/planner_oracle.py "
+                      f"in {wall:.1f}s"}
+
+
 _POOL = None
 _INPUTS = None
 
@@ -549,6 +566,8 @@ def main() -> None:
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_sample(args).items()
                                 if k in ("value", "unit", "cores", "kind", "sample")}
+        if "sweep" in line:
+            line["sweep"]["cpu_baseline"] = cpu_sweep_sample(app)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
