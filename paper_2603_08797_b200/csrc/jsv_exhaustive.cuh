@@ -573,12 +573,15 @@ __device__ __forceinline__ void x_sweep_k(const XCtx<PM>& cx, const uint2* __res
   uint2 rec[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) rec[k] = pack[lane + 32 * k];
-  while (vmask) {
-    const int j0 = __ffs(vmask) - 1;
-    vmask &= vmask - 1;
-    const int j1 = vmask ? __ffs(vmask) - 1 : j0;
-    vmask &= vmask - 1;
-    const uint2 b0 = ws.sw[j0], b1 = ws.sw[j1];
+  // fixed slot pairs (2j, 2j+1): a slot that is not a swept leaf prefix holds
+  // subtrahends no record passes, so only pairs with no swept slot are skipped
+  static_assert(NS % 2 == 0, "slot pairs");
+#pragma unroll 1
+  for (int j0 = 0; j0 < NS; j0 += 2) {
+    if (!((vmask >> j0) & 3u)) continue;  // warp-uniform
+    const int j1 = j0 + 1;
+    const uint4 bb = *reinterpret_cast<const uint4*>(&ws.sw[j0]);
+    const uint2 b0 = make_uint2(bb.x, bb.y), b1 = make_uint2(bb.z, bb.w);
     unsigned m0 = 0u, m1 = 0u;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
@@ -591,7 +594,7 @@ __device__ __forceinline__ void x_sweep_k(const XCtx<PM>& cx, const uint2* __res
       for (int k = 0; k < K; ++k) mask |= (X_V(rec[k], b0) == X_H ? 1u : 0u) << k;
       x_slow_reg<PM, NS>(cx, ws, j0, mask, best);
     }
-    if (m1 == X_H && j1 != j0) {
+    if (m1 == X_H) {
       unsigned mask = 0;
 #pragma unroll
       for (int k = 0; k < K; ++k) mask |= (X_V(rec[k], b1) == X_H ? 1u : 0u) << k;
