@@ -837,7 +837,10 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
       DISPATCH_D(a.D, k_pairs_l, gl, a, 0);
     }
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
-    if (tiled) {
+    // survivors pass: few candidates per job with long j ranges -- the tiled
+    // kernel's (i tile, j chunk) work items spread them over the SMs better than
+    // one thread per candidate (ncu: 61 vs 85 us per 64-probe batch)
+    if (tiled || !getenv("JSV_PAIRS_L1")) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
     } else {
       DISPATCH_D(a.D, k_pairs_l, gl, a, 1);
