@@ -72,7 +72,7 @@ struct DevBuf {
 enum BufId {
   B_REQ, B_PROBES, B_DESC, B_WAYS, B_TILE_TASK, B_TILE_START, B_ITEMS, B_NITEMS, B_ARR, B_SL, B_FLAG,
   B_CNT, B_FRONT, B_FCNT, B_FPOS, B_FCR, B_SORTED, B_SCR, B_POOLC, B_POOLN, B_POOLT, B_PSL,
-  B_PCAP, B_PACC, B_PLAT, B_PFAN, B_RANKP, B_RANKM, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
+  B_PCAP, B_PACC, B_PLAT, B_PFAN, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
   B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
@@ -717,8 +717,6 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_PACC].ensure(sizeof(double) * jobs * W));
   CK(B[B_PLAT].ensure(sizeof(double) * jobs * W));
   CK(B[B_PFAN].ensure(sizeof(double) * jobs * W * p.maxout));
-  CK(B[B_RANKP].ensure(sizeof(uint16_t) * jobs * (W + 1)));
-  CK(B[B_RANKM].ensure(sizeof(uint16_t) * jobs * (W + 1)));
   CK(B[B_S1LAT2].ensure(sizeof(double) * jobs));
   CK(B[B_S1SL].ensure(sizeof(int) * jobs));
   CK(B[B_S1ACC].ensure(sizeof(double) * jobs));
@@ -766,8 +764,6 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.p_acc = B[B_PACC].as<double>();
   a.p_lat = B[B_PLAT].as<double>();
   a.p_fan = B[B_PFAN].as<double>();
-  a.rank_p = B[B_RANKP].as<uint16_t>();
-  a.rank_m = B[B_RANKM].as<uint16_t>();
   a.pool_min_lat2 = B[B_S1LAT2].as<double>();
   a.pool_min_sl = B[B_S1SL].as<int>();
   a.pool_acc_ub = B[B_S1ACC].as<double>();
@@ -857,8 +853,6 @@ static void s2_base(jsv_problem& p, BatchState& bs, S2Args& a) {
   a.p_acc = bs.s1.p_acc;
   a.p_lat = bs.s1.p_lat;
   a.p_fan = bs.s1.p_fan;
-  a.rank_p = bs.s1.rank_p;
-  a.rank_m = bs.s1.rank_m;
   a.items = bs.s1.items;
   a.nitems = bs.s1.nitems;
   a.pool_cand = bs.s1.pool_cand;

@@ -77,8 +77,6 @@ struct S1Args {
   double* p_acc;
   double* p_lat;
   double* p_fan;
-  uint16_t* rank_p;
-  uint16_t* rank_m;
   double* pool_min_lat2;
   int* pool_min_sl;
   double* pool_acc_ub;
@@ -123,8 +121,6 @@ struct S2Args {
   const double* p_acc;
   const double* p_lat;
   const double* p_fan;
-  const uint16_t* rank_p;
-  const uint16_t* rank_m;
   // candidate items, for the m tie-break (planner.py:852)
   const uint32_t* items;
   const int* nitems;

@@ -10,6 +10,9 @@
 //                2-variant mixes are decoded from the unit index.
 //   k_stats      one thread per candidate: latency / capacity / slices /
 //                weighted accuracy + fan-out (all-equal short circuit).
+//   k_pairs_l    same-slices pass of the skyline, one thread per candidate over
+//                list-ordered coordinates (k_pairs_a: tiled form, used for the
+//                survivors pass and for wide rows):
 //   k_pairs_a    tiled all-pairs skyline: candidate i dies if another
 //                candidate weakly dominates it with a different row, or has an
 //                identical row and smaller items (the reference's dedup).  By
@@ -20,8 +23,7 @@
 //                rank (-cap, slices, items) by counting.
 //   k_truncate   frontier order, pareto_width truncation (planner.py:574-583),
 //                pool SoA + per-pool bounds for Stage 2.
-//   k_mrank      per-pool ranks of the item lists with end = -inf / +inf; the
-//                Stage-2 tie-break on m compares these.
+//   (ties on m are resolved in Stage 2 directly on the bundles' item lists)
 #include <algorithm>
 #include <cstdlib>
 #include <cub/block/block_scan.cuh>
@@ -697,41 +699,6 @@ __global__ void __launch_bounds__(1024) k_truncate(const __grid_constant__ S1Arg
   }
 }
 
-// Rank of (items, end-sign) among the 2*(P+1) elements of one pool (+ empty).
-__device__ __forceinline__ uint32_t item_word(const S1Args& a, long long c, int n, int k, int sign) {
-  if (k < n) return a.items[c * a.maxi + k];
-  return sign ? 0xFFFFFFFFu : 0u;
-}
-
-__global__ void k_mrank(const __grid_constant__ S1Args a) {
-  const int job = blockIdx.x;
-  const int probe = job / a.T, t = job % a.T;
-  const int P = a.pool_n[job];
-  const int E = 2 * (P + 1);
-  const int e = blockIdx.y * blockDim.x + threadIdx.x;
-  if (e >= E) return;
-  const long long base = job_base(a, probe, t);
-  const int* pool = a.pool_cand + (long long)job * a.W;
-  const int ke = e >> 1, se = e & 1;
-  const long long ce = ke < P ? base + pool[ke] : -1;
-  const int ne = ke < P ? a.nitems[ce] : 0;
-  int rank = 0;
-  for (int f = 0; f < E; ++f) {
-    const int kf = f >> 1, sf = f & 1;
-    const long long cf = kf < P ? base + pool[kf] : -1;
-    const int nf = kf < P ? a.nitems[cf] : 0;
-    int r = 0;
-    for (int k = 0; k <= MAXI && r == 0; ++k) {
-      uint32_t x = item_word(a, cf, nf, k, sf), y = item_word(a, ce, ne, k, se);
-      if (x != y) r = x < y ? -1 : 1;
-      if (k >= nf && k >= ne) break;
-    }
-    rank += r < 0;
-  }
-  const long long q = (long long)job * (a.W + 1) + ke;
-  if (se) a.rank_p[q] = (uint16_t)rank;
-  else a.rank_m[q] = (uint16_t)rank;
-}
 
 // Duplicate probes (identical Stage-1 inputs, see plan_batch_internal): copy the
 // representative's pools -- every per-job array Stage 2 and finalize read -- and

@@ -53,21 +53,6 @@ __device__ __forceinline__ void pack16(unsigned long long* w, int k, unsigned v)
   w[k >> 2] |= (unsigned long long)(v & 0xFFFFu) << ((3 - (k & 3)) * 16);
 }
 
-// m-rank tie key of one leaf (task-id order)
-__device__ inline void tie_key(const S2Args& a, int probe, const uint16_t* cb,
-                               unsigned long long* w) {
-  w[0] = w[1] = w[2] = w[3] = 0ull;
-  bool later = false;
-  for (int u = a.T - 1; u >= 0; --u) {
-    const int job = probe * a.T + u;
-    const int c = cb[u];
-    const int idx = (c == NONE16) ? a.pool_n[job] : c;
-    const long long q = (long long)job * (a.W + 1) + idx;
-    const unsigned rk = later ? a.rank_p[q] : a.rank_m[q];
-    pack16(w, u, rk);
-    if (c != NONE16) later = true;
-  }
-}
 
 __device__ inline void leaf_key(int T, const uint16_t* ch_topo, unsigned long long* w) {
   w[0] = w[1] = w[2] = w[3] = 0ull;
