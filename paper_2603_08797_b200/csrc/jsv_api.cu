@@ -1100,8 +1100,17 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
   }
   c.stats.kernel_launches += launch_finalize(f, st);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(out, f.out, sizeof(jsv_plan_out) * n, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  // results through the pinned staging buffer (a pageable copy of the ~5 KB
+  // records is staged by the driver at a fraction of the link rate)
+  jsv_plan_out* h = static_cast<jsv_plan_out*>(c.pinned(sizeof(jsv_plan_out) * n));
+  if (h) {
+    CK(cudaMemcpyAsync(h, f.out, sizeof(jsv_plan_out) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    memcpy(out, h, sizeof(jsv_plan_out) * n);
+  } else {
+    CK(cudaMemcpyAsync(out, f.out, sizeof(jsv_plan_out) * n, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
   if (nodes)
     for (int i = 0; i < n; ++i) out[i].nodes = (*nodes)[i];
   return JSV_OK;
