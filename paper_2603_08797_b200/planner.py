@@ -169,6 +169,7 @@ def _verdicts_from(out: N.PlanOut, app, lw: LW.Lowered) -> tuple[ConstraintVerdi
 
 
 _PLAN_DTYPE = None
+_PROBE_DTYPE = None
 _new = object.__new__
 
 
@@ -369,20 +370,33 @@ def plan_batch(
     options = options or PlannerOptions()
     if not requests:
         return []
+    same_app = apps is None
     apps = list(apps) if apps is not None else [app] * len(requests)
     r0 = requests[0]
+    ov0 = dict(r0.factor_overrides or {})
     for r in requests[1:]:
-        if (r.slice_budget, r.space, r.slack, dict(r.factor_overrides or {})) != (
-                r0.slice_budget, r0.space, r0.slack, dict(r0.factor_overrides or {})):
+        if (r.slice_budget != r0.slice_budget or r.space != r0.space or r.slack != r0.slack
+                or (r.factor_overrides is not r0.factor_overrides
+                    and dict(r.factor_overrides or {}) != ov0)):
             raise ConfigError("plan_batch requests must share budget, space, slack and overrides")
     t0 = time.perf_counter()
     lw, _ = _prepare(app, profile, r0, options, device)
     probes = (N.Probe * len(requests))()
-    for i, (a, r) in enumerate(zip(apps, requests)):
-        if a.graph is not app.graph and a.graph != app.graph:
-            raise ConfigError("plan_batch apps must share one task graph")
-        st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
-        probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
+    if same_app and r0.space.task_graph_informed:
+        # one app: the probes differ only in demand (a numpy view fills them)
+        global _PROBE_DTYPE
+        if _PROBE_DTYPE is None:
+            _PROBE_DTYPE = np.dtype(N.Probe)
+        proto = LW.probe_struct(app, lw, 0.0, None)
+        view = np.frombuffer(probes, dtype=_PROBE_DTYPE)
+        view[:] = np.frombuffer(proto, dtype=_PROBE_DTYPE)[0]
+        view["demand"] = [float(r.demand_rps) for r in requests]
+    else:
+        for i, (a, r) in enumerate(zip(apps, requests)):
+            if a.graph is not app.graph and a.graph != app.graph:
+                raise ConfigError("plan_batch apps must share one task graph")
+            st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
+            probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
     req, keep = LW.request_struct(lw, r0, options)
     outs = (N.PlanOut * len(requests))()
     N.check(N.load_library().jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests),
