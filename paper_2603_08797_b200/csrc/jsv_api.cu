@@ -1717,7 +1717,10 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
   // speculation depth: a round costs ~F of latency (launches, host round trips)
   // plus ~c per probe; a depth-d bisection subtree resolves d levels with
   // 2^d - 1 probes, so pick d minimising (F + active (2^d - 1) c) / d
-  const double round_ms = 1.0, probe_ms = 0.01;
+  double round_ms = 1.0, probe_ms = 0.01;
+  if (const char* e = getenv("JSV_SPEC_ROUND_MS")) round_ms = atof(e);
+  if (const char* e = getenv("JSV_SPEC_PROBE_MS")) probe_ms = atof(e);
+  const int force_depth = getenv("JSV_SPEC_DEPTH") ? atoi(getenv("JSV_SPEC_DEPTH")) : 0;
   while (true) {
     int active = 0;
     for (auto& s : ps) active += (s.phase == 1 || s.phase == 2);
@@ -1731,6 +1734,7 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
         depth = d;
       }
     }
+    if (force_depth > 0) depth = force_depth;
     std::vector<std::pair<int, double>> w;
     std::vector<std::vector<double>> tree(n);
     for (int i = 0; i < n; ++i) {
