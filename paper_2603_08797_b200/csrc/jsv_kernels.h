@@ -89,6 +89,7 @@ struct S1Args {
   int* sbst;      // [jobs * (S+2)] survivor bucket starts
   int* scnt;      // [jobs] survivors
   double* arrl;   // [D * Ctot] coordinates in list order (slices order, then survivor order)
+  int* fsorted;   // [jobs] 1: k_front_sort computed the job's frontier ranks
   int4* wl[3];    // pair-pass work lists {job, i0, j0}: same-bucket, survivors, frontier
   int* wn;        // [3] their lengths (zeroed per batch)
 };

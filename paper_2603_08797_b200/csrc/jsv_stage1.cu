@@ -538,10 +538,116 @@ __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args
   }
 }
 
+// Frontier order and capacity ranks by sorting instead of counting (jobs whose
+// frontier has at most FSORT_MAX bundles and finite coordinates; the others keep
+// k_pairs_b's pair counts).  One block per job, bitonic sort of frontier
+// indices in shared memory: (1) by the row, lexicographically -- rows are
+// distinct here, so a bundle's sorted rank is the number of rows below it, the
+// position k_pairs_b counts (planner.py:556-559); (2) when the frontier will be
+// truncated, by (-capacity, slices, items) (planner.py:576), distinct keys too.
+#define FSORT_MAX 2048
+template <int D>
+__global__ void __launch_bounds__(512) k_front_sort(const __grid_constant__ S1Args a) {
+  extern __shared__ __align__(16) unsigned char fs_smem[];
+  __shared__ int s_ok;
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const int F = a.fcnt[job];
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  if (F > FSORT_MAX || F == 0) {
+    if (threadIdx.x == 0) a.fsorted[job] = 0;
+    return;
+  }
+  int F2 = 1;
+  while (F2 < F) F2 <<= 1;
+  double* key = reinterpret_cast<double*>(fs_smem);  // [D][F2]
+  int* ix = reinterpret_cast<int*>(key + D * F2);
+  if (threadIdx.x == 0) s_ok = 1;
+  __syncthreads();
+  for (int k = threadIdx.x; k < F2; k += blockDim.x) {
+    ix[k] = k;
+    if (k < F) {
+      const int c = a.front[base + k];
+      for (int d = 0; d < D; ++d) {
+        const double v = a.arr[d * tot + base + c];
+        if (!isfinite(v)) s_ok = 0;
+        key[d * F2 + k] = v;
+      }
+    } else {
+      for (int d = 0; d < D; ++d) key[d * F2 + k] = INFINITY;
+    }
+  }
+  __syncthreads();
+  if (!s_ok) {
+    if (threadIdx.x == 0) a.fsorted[job] = 0;
+    return;
+  }
+  // sort 1: rows, lexicographic (padding rows +inf, ties by index)
+  for (int kk = 2; kk <= F2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < F2; i += blockDim.x) {
+        const int l = i ^ j;
+        if (l > i) {
+          const int x = ix[i], y = ix[l];
+          int c = 0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            if (c == 0) {
+              const double u = key[d * F2 + x], v = key[d * F2 + y];
+              c = u < v ? -1 : (u > v ? 1 : 0);
+            }
+          }
+          if (c == 0) c = x < y ? -1 : 1;
+          const bool up = (i & kk) == 0;
+          if ((c > 0) == up) {
+            ix[i] = y;
+            ix[l] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = threadIdx.x; r < F; r += blockDim.x) a.fpos[base + ix[r]] = r;
+  if (F > a.W) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < F2; k += blockDim.x) ix[k] = k;
+    __syncthreads();
+    // sort 2: (-capacity, slices, items); padding -capacity = +inf
+    for (int kk = 2; kk <= F2; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < F2; i += blockDim.x) {
+          const int l = i ^ j;
+          if (l > i) {
+            const int x = ix[i], y = ix[l];
+            const double cx = key[1 * F2 + x], cy = key[1 * F2 + y];
+            int c;
+            if (cx != cy) c = cx < cy ? -1 : 1;
+            else if (x >= F || y >= F) c = x < y ? -1 : 1;
+            else if (key[x] != key[y]) c = key[x] < key[y] ? -1 : 1;
+            else c = cmp_items(a, base + a.front[base + x], base + a.front[base + y]);
+            if (c == 0) c = x < y ? -1 : 1;
+            const bool up = (i & kk) == 0;
+            if ((c > 0) == up) {
+              ix[i] = y;
+              ix[l] = x;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int r = threadIdx.x; r < F; r += blockDim.x) a.fcr[base + ix[r]] = r;
+  }
+  if (threadIdx.x == 0) a.fsorted[job] = 1;
+}
+
 template <int D>
 __device__ __forceinline__ void pairs_b_tile(const S1Args& a, int job, int i0, int j0, int jchunk,
                                              double* sh, int* shc) {
   const int probe = job / a.T, t = job % a.T;
+  if (a.fsorted[job]) return;  // ranks already computed by k_front_sort
   const int F = a.fcnt[job];
   if (i0 >= F || j0 >= F) return;  // (block-uniform)
   const int j1 = min(F, j0 + jchunk);
@@ -822,6 +928,26 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   if (L.tiles_pp > 0) {
     const unsigned gb = (unsigned)std::max<long long>(1, std::min<long long>(L.max_items, L.grid));
     PROF_BEGIN(K_PAIRS_B);
+    if (a.D <= 8 && !getenv("JSV_NO_FSORT")) {
+      int F2 = 1;
+      while (F2 < FSORT_MAX) F2 <<= 1;
+      const size_t fsm = (size_t)F2 * (a.D * sizeof(double) + sizeof(int));
+#define JSV_FS(DV)                                                                               \
+  do {                                                                                           \
+    cudaFuncSetAttribute(k_front_sort<DV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm); \
+    k_front_sort<DV><<<a.n_probes * a.T, 512, fsm, st>>>(a);                                      \
+  } while (0)
+      switch (a.D) {
+        case 4: JSV_FS(4); break;
+        case 5: JSV_FS(5); break;
+        case 6: JSV_FS(6); break;
+        default: JSV_FS(8); break;
+      }
+#undef JSV_FS
+      ++launches;
+    } else {
+      cudaMemsetAsync(a.fsorted, 0, sizeof(int) * a.n_probes * a.T, st);
+    }
     DISPATCH_D(a.D, k_pairs_b, gb, a, a.wl[2], a.wn + 2, 1024);
     PROF_END();
     ++launches;
