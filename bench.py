@@ -281,6 +281,8 @@ def _cpu_one(demand):
 def run_reference(args, rank, world) -> None:
     if rank != 0:
         return
+    for _ in range(args.warmup):  # untimed, like the GPU arm's warm-up steps
+        cpu_sample(args)
     vals = []
     for _ in range(args.steps):
         vals.append(cpu_sample(args))
