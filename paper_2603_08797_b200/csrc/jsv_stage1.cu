@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256) k_pairs_a(const __grid_constant__ S1Args 
 // coordinates (arrl, L1-resident).  Lanes of a warp hold neighbouring list
 // positions -- the same or adjacent slices buckets -- so they read the same j
 // in step (broadcast loads) and each leaves its loop at its first dominator.
-template <int D>
+template <int D, bool SKIP0>
 __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args a, int mode) {
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long gid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -443,8 +443,9 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
   unsigned fl = 0;
   for (int j = lo; j < hi; ++j) {
     bool le = true, eq = true;
+    // (SKIP0: a same-slices bucket -- coordinate 0 is equal for every j)
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
+    for (int d = SKIP0 ? 1 : 0; d < D; ++d) {
       const double xj = xl[d * tot + j];
       le = le && (xj <= xi[d]);
       eq = eq && (xj == xi[d]);
@@ -873,6 +874,17 @@ int stage1_padded_dims(int D) { return pick_D(D); }
     default: KERNEL<MAXD><<<GRID, 256, 0, st>>>(__VA_ARGS__); break; \
   }
 
+#define DISPATCH_D2(D, KERNEL, B, GRID, ...)                             \
+  switch (D) {                                                            \
+    case 4: KERNEL<4, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;         \
+    case 5: KERNEL<5, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;         \
+    case 6: KERNEL<6, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;         \
+    case 8: KERNEL<8, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;         \
+    case 12: KERNEL<12, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;       \
+    case 16: KERNEL<16, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;       \
+    default: KERNEL<MAXD, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;     \
+  }
+
 int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
   int launches = 0;
   long long gen = (long long)a.n_probes * a.U;
@@ -907,7 +919,12 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     if (tiled) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1 << 30, 0);
     } else {
-      DISPATCH_D(a.D, k_pairs_l, gl, a, 0);
+      // bucketed same-slices pass: skip the slices coordinate
+      if (a.S + 2 <= BUCKET_SMEM_MAX) {
+        DISPATCH_D2(a.D, k_pairs_l, true, gl, a, 0);
+      } else {
+        DISPATCH_D2(a.D, k_pairs_l, false, gl, a, 0);
+      }
     }
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
     // survivors pass: few candidates per job with long j ranges -- the tiled
@@ -916,7 +933,7 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     if (tiled || !getenv("JSV_PAIRS_L1")) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
     } else {
-      DISPATCH_D(a.D, k_pairs_l, gl, a, 1);
+      DISPATCH_D2(a.D, k_pairs_l, false, gl, a, 1);
     }
     PROF_END();
     launches += 3;
