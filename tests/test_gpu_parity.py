@@ -94,3 +94,23 @@ def test_bench_batch_strategies_agree_at_full_size():
     assert all(r.feasible for r in exh)
     assert [strip(r) for r in exh] == [strip(r) for r in srch]
     assert [strip(r) for r in exh[::8]] == [strip(r) for r in one]
+
+
+@pytest.mark.parametrize("env", [{"JSV_NO_FSORT": "1"}, {"JSV_PAIRS_TILED": "1"},
+                                 {"JSV_PAIRS_L1": "1"}, {"JSV_NO_RPL": "1"}, {"JSV_NO_TMA": "1"}])
+def test_alternative_kernel_paths_match_reference(env, monkeypatch):
+    """Every kernel variant the library can pick (frontier ranks by counting vs by
+    sorting, tiled vs barrier-free skyline passes, register vs looped sweep, TMA
+    vs plain staging) reproduces the reference goldens."""
+    from paper_2603_08797_b200 import planner
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    docs = load("plans_bundled.json")
+    planner.set_strategy("exhaustive", EXH_LIMIT)
+    try:
+        for doc in docs[::5]:
+            app, table, req, opt = case_inputs(doc)
+            assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]
+    finally:
+        planner.set_strategy("auto")
