@@ -277,7 +277,8 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) push_items(a.wl[0], a.wn + 0, job, n, 1 << 30, false);
+  // same-bucket pass items: j chunks of 1024 (a tile's bucket range can be long)
+  if (threadIdx.x == 0) push_items(a.wl[0], a.wn + 0, job, n, 1024, false);
   // hist[s] is now the start of bucket s; scatter (order inside a bucket is irrelevant)
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int s = (int)a.arr[base + i];
@@ -917,7 +918,7 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     // wide rows (many out-edges) stage j tiles in shared memory instead
     const bool tiled = a.D > 8 || getenv("JSV_PAIRS_TILED") != nullptr;
     if (tiled) {
-      DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1 << 30, 0);
+      DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1024, 0);
     } else {
       // bucketed same-slices pass: skip the slices coordinate
       if (a.S + 2 <= BUCKET_SMEM_MAX) {
