@@ -78,7 +78,7 @@ enum BufId {
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
-  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_COUNT
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_ARRF, B_COUNT
 };
 
 struct jsv_context {
@@ -795,6 +795,8 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.arrl = B[B_ARRL].as<double>();
   CK(B[B_FSORT].ensure(sizeof(int) * jobs));
   a.fsorted = B[B_FSORT].as<int>();
+  CK(B[B_ARRF].ensure(sizeof(float4) * C1));
+  a.arrf = B[B_ARRF].as<float4>();
   S1Launch L{};
   L.max_items = max_items;
   {

@@ -285,6 +285,10 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
     const int pos = atomicAdd(&hist[s], 1);
     a.order[base + pos] = i;
     for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
+    // float shadow of coordinates 1..4 (the same-slices pass's quick reject)
+    if (a.D == 5)
+      a.arrf[base + pos] = make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
+                                       (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
   }
 }
 
@@ -441,8 +445,18 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
     hi = a.sbst[(long long)job * (a.S + 2) + si];
   }
   const int* list = (mode == 0 ? a.order : a.surv) + base;
+  // quick reject on the float shadow: rounding to float is monotone, so
+  // float(x_j) > float(x_i) in any coordinate proves x_j > x_i there (j cannot
+  // dominate i); otherwise the exact double test below decides
+  constexpr bool FQ = SKIP0 && D == 5;
+  float4 fi = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (FQ) fi = a.arrf[base + p];
   unsigned fl = 0;
   for (int j = lo; j < hi; ++j) {
+    if (FQ) {
+      const float4 fj = a.arrf[base + j];
+      if ((fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w)) continue;
+    }
     bool le = true, eq = true;
     // (SKIP0: a same-slices bucket -- coordinate 0 is equal for every j)
 #pragma unroll
