@@ -452,11 +452,8 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
   float4 fi = make_float4(0.f, 0.f, 0.f, 0.f);
   if (FQ) fi = a.arrf[base + p];
   unsigned fl = 0;
-  for (int j = lo; j < hi; ++j) {
-    if (FQ) {
-      const float4 fj = a.arrf[base + j];
-      if ((fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w)) continue;
-    }
+  // exact weak-dominance / dedup test of j against i; true when i dies
+  auto exact = [&](int j) -> bool {
     bool le = true, eq = true;
     // (SKIP0: a same-slices bucket -- coordinate 0 is equal for every j)
 #pragma unroll
@@ -465,20 +462,44 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
       le = le && (xj <= xi[d]);
       eq = eq && (xj == xi[d]);
     }
-    if (le) {
-      if (!eq) {
-        fl = 1u;
-        break;
-      }
-      if (j != p) {
-        const int ci = list[p], cj = list[j];
-        const int c = cmp_items(a, base + cj, base + ci);
-        if (c < 0 || (c == 0 && cj < ci)) {
-          fl = 2u;
-          break;
-        }
+    if (!le) return false;
+    if (!eq) {
+      fl = 1u;
+      return true;
+    }
+    if (j != p) {
+      const int ci = list[p], cj = list[j];
+      const int c = cmp_items(a, base + cj, base + ci);
+      if (c < 0 || (c == 0 && cj < ci)) {
+        fl = 2u;
+        return true;
       }
     }
+    return false;
+  };
+  if (FQ) {
+    // four shadow loads in flight per step; the j's that survive the quick
+    // reject get the exact test, in j order
+    bool dead = false;
+    for (int j = lo; j < hi && !dead; j += 4) {
+      unsigned keep = 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (j + u < hi) {
+          const float4 fj = a.arrf[base + j + u];
+          const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
+          keep |= (rej ? 0u : 1u) << u;
+        }
+      }
+      while (keep && !dead) {
+        const int u = __ffs(keep) - 1;
+        keep &= keep - 1;
+        dead = exact(j + u);
+      }
+    }
+  } else {
+    for (int j = lo; j < hi; ++j)
+      if (exact(j)) break;
   }
   if (fl) atomicOr(&a.flag[base + list[p]], fl);
 }
