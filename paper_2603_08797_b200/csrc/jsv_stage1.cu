@@ -477,14 +477,15 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
     }
     return false;
   };
+  constexpr int XJ = 8;
   if (FQ) {
-    // four shadow loads in flight per step; the j's that survive the quick
+    // XJ shadow loads in flight per step; the j's that survive the quick
     // reject get the exact test, in j order
     bool dead = false;
-    for (int j = lo; j < hi && !dead; j += 4) {
+    for (int j = lo; j < hi && !dead; j += XJ) {
       unsigned keep = 0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < XJ; ++u) {
         if (j + u < hi) {
           const float4 fj = a.arrf[base + j + u];
           const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
