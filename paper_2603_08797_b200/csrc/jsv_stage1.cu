@@ -463,7 +463,8 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
       eq = eq && (xj == xi[d]);
     }
     if (!le) return false;
-    if (!eq) {
+    // (survivors pass: j has fewer slices, so its row differs from i's)
+    if (!eq || (SKIP0 && mode != 0)) {
       fl = 1u;
       return true;
     }
@@ -529,6 +530,10 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
     if (alive) {
       a.surv[base + carry + off] = i;
       for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + carry + off] = a.arr[d * tot + base + i];
+      if (a.D == 5)
+        a.arrf[base + carry + off] =
+            make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
+                        (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
     }
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
@@ -964,11 +969,12 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
       }
     }
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
-    // survivors pass: few candidates per job with long j ranges -- the tiled
-    // kernel's (i tile, j chunk) work items spread them over the SMs better than
-    // one thread per candidate (ncu: 61 vs 85 us per 64-probe batch)
-    if (tiled || !getenv("JSV_PAIRS_L1")) {
+    // survivors pass: the same barrier-free kernel (float-shadow quick reject in
+    // survivor order, built by k_surv); JSV_PAIRS_A1 selects the tiled kernel
+    if (tiled || getenv("JSV_PAIRS_A1")) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
+    } else if (a.S + 2 <= BUCKET_SMEM_MAX) {
+      DISPATCH_D2(a.D, k_pairs_l, true, gl, a, 1);
     } else {
       DISPATCH_D2(a.D, k_pairs_l, false, gl, a, 1);
     }
