@@ -231,14 +231,35 @@ __global__ void k_stats(const __grid_constant__ S1Args a) {
   a.flag[c] = 0u;
 }
 
-// append the work items of one job: i tiles of 256, j chunks of jchunk over [0, jend(i0))
-__device__ __forceinline__ void push_items(int4* list, int* count, int job, int n, int jchunk,
-                                           bool triangular) {
-  for (int i0 = 0; i0 < n; i0 += 256) {
-    const int jend = triangular ? min(n, i0 + 256) : n;
-    const int nj = max(1, (jend + jchunk - 1) / jchunk);
-    const int at = atomicAdd(count, nj);
-    for (int c = 0; c < nj; ++c) list[at + c] = make_int4(job, i0, c * jchunk, 0);
+// Append the work items of one job: i tiles of 256, j chunks of jchunk over
+// [0, jend(i0)).  Called by every thread of the block: one atomicAdd reserves
+// the job's whole range, the threads write it tile by tile.  Lists the launch
+// will not consume (wl_mask) are skipped.
+__device__ __forceinline__ int items_of_tile(int tl, int n, int jchunk, bool triangular) {
+  const int jend = triangular ? min(n, tl * 256 + 256) : n;
+  return max(1, (jend + jchunk - 1) / jchunk);
+}
+__device__ void push_items(const S1Args& a, int k, int job, int n, int jchunk, bool triangular) {
+  __shared__ int s_at;
+  if (!((a.wl_mask >> k) & 1)) return;  // (block-uniform)
+  const int tiles = (n + 255) / 256;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int tot = 0;
+    for (int tl = 0; tl < tiles; ++tl) tot += items_of_tile(tl, n, jchunk, triangular);
+    s_at = tot ? atomicAdd(a.wn + k, tot) : 0;
+  }
+  __syncthreads();
+  const int at = s_at;
+  for (int tl = threadIdx.x; tl < tiles; tl += blockDim.x) {
+    int off = 0;
+    if (triangular) {
+      for (int u = 0; u < tl; ++u) off += items_of_tile(u, n, jchunk, true);
+    } else {
+      off = tl * items_of_tile(0, n, jchunk, false);
+    }
+    const int nj = items_of_tile(tl, n, jchunk, triangular);
+    for (int c = 0; c < nj; ++c) a.wl[k][at + off + c] = make_int4(job, tl * 256, c * jchunk, 0);
   }
 }
 
@@ -256,6 +277,7 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
   int* bst = a.bstart + (long long)job * NB;
   if (NB > BUCKET_SMEM_MAX) {
     // huge budgets: identity order, every candidate scanned
+    push_items(a, 0, job, n, 1024, false);
     for (int s = threadIdx.x; s < NB; s += blockDim.x) bst[s] = (s == 0) ? 0 : n;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       a.order[base + i] = i;
@@ -276,9 +298,9 @@ __global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args 
       bst[s] = acc;
     }
   }
-  __syncthreads();
   // same-bucket pass items: j chunks of 1024 (a tile's bucket range can be long)
-  if (threadIdx.x == 0) push_items(a.wl[0], a.wn + 0, job, n, 1024, false);
+  push_items(a, 0, job, n, 1024, false);
+  __syncthreads();
   // hist[s] is now the start of bucket s; scatter (order inside a bucket is irrelevant)
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
     const int s = (int)a.arr[base + i];
@@ -544,11 +566,9 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
   const int* bst = a.bstart + (long long)job * NB;
   int* sb = a.sbst + (long long)job * NB;
   for (int s = threadIdx.x; s < NB; s += blockDim.x) sb[s] = bst[s] >= n ? total : a.pcnt[base + bst[s]];
-  if (threadIdx.x == 0) {
-    a.scnt[job] = total;
-    // survivors with fewer slices precede i in the list: j < i0 + 256
-    push_items(a.wl[1], a.wn + 1, job, total, 1024, true);
-  }
+  if (threadIdx.x == 0) a.scnt[job] = total;
+  // survivors with fewer slices precede i in the list: j < i0 + 256
+  push_items(a, 1, job, total, 1024, true);
 }
 
 __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args a) {
@@ -575,10 +595,8 @@ __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
-  if (threadIdx.x == 0) {
-    a.fcnt[job] = carry;
-    push_items(a.wl[2], a.wn + 2, job, carry, 1024, false);
-  }
+  if (threadIdx.x == 0) a.fcnt[job] = carry;
+  push_items(a, 2, job, carry, 1024, false);
 }
 
 // Frontier order and capacity ranks by sorting instead of counting (jobs whose
@@ -927,8 +945,13 @@ int stage1_padded_dims(int D) { return pick_D(D); }
     default: KERNEL<MAXD, B><<<GRID, 256, 0, st>>>(__VA_ARGS__); break;     \
   }
 
-int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
+int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
   int launches = 0;
+  // the tiled pair kernels read device work lists; the barrier-free ones do not
+  const bool tiled = a0.D > 8 || getenv("JSV_PAIRS_TILED") != nullptr;
+  const bool tiled1 = tiled || getenv("JSV_PAIRS_A1") != nullptr;
+  S1Args a = a0;
+  a.wl_mask = (tiled ? 1 : 0) | (tiled1 ? 2 : 0) | 4;
   long long gen = (long long)a.n_probes * a.U;
   if (gen > 0) {
     PROF_BEGIN(K_GENERATE);
@@ -957,7 +980,6 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     PROF_BEGIN(K_PAIRS_A);
     const unsigned gl = (unsigned)((tot + 255) / 256);
     // wide rows (many out-edges) stage j tiles in shared memory instead
-    const bool tiled = a.D > 8 || getenv("JSV_PAIRS_TILED") != nullptr;
     if (tiled) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[0], a.wn + 0, 1024, 0);
     } else {
@@ -971,7 +993,7 @@ int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st) {
     k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
     // survivors pass: the same barrier-free kernel (float-shadow quick reject in
     // survivor order, built by k_surv); JSV_PAIRS_A1 selects the tiled kernel
-    if (tiled || getenv("JSV_PAIRS_A1")) {
+    if (tiled1) {
       DISPATCH_D(a.D, k_pairs_a, ga, a, a.wl[1], a.wn + 1, 1024, 1);
     } else if (a.S + 2 <= BUCKET_SMEM_MAX) {
       DISPATCH_D2(a.D, k_pairs_l, true, gl, a, 1);
