@@ -530,37 +530,84 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
 
 // Survivors of the same-bucket pass, in slices order, and their bucket starts
 // sbst[s] = #survivors with fewer than s slices.
+#define SURV_KC 12
+__device__ __forceinline__ void surv_write(const S1Args& a, long long base, long long tot, int pos, int i) {
+  a.surv[base + pos] = i;
+  for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
+  if (a.D == 5)
+    a.arrf[base + pos] = make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
+                                     (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
+}
+
 __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
+  __shared__ int woff[SURV_KC * 32];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
   const long long base = job_base(a, probe, t);
   const long long tot = (long long)a.n_probes * a.C_probe;
   const int* order = a.order + base;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int s0 = 0; s0 < n; s0 += 1024) {
-    const int p = s0 + threadIdx.x;
-    const int i = p < n ? order[p] : 0;
-    const int alive = (p < n && a.flag[base + i] == 0u) ? 1 : 0;
-    int off, total;
-    Scan(tmp).ExclusiveSum(alive, off, total);
-    if (p < n) a.pcnt[base + p] = carry + off;
-    if (alive) {
-      a.surv[base + carry + off] = i;
-      for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + carry + off] = a.arr[d * tot + base + i];
-      if (a.D == 5)
-        a.arrf[base + carry + off] =
-            make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
-                        (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (n <= SURV_KC * 1024) {
+    // every chunk's list entries and flags loaded up front (no load latency
+    // between chunks), survivor offsets from per-(chunk, warp) ballot counts
+    // and ONE block scan over them
+    int iv[SURV_KC];
+    unsigned bal[SURV_KC];
+#pragma unroll
+    for (int c = 0; c < SURV_KC; ++c) {
+      const int p = c * 1024 + threadIdx.x;
+      iv[c] = p < n ? order[p] : 0;
+    }
+#pragma unroll
+    for (int c = 0; c < SURV_KC; ++c) {
+      const int p = c * 1024 + threadIdx.x;
+      const bool alive = p < n && a.flag[base + iv[c]] == 0u;
+      bal[c] = __ballot_sync(0xffffffffu, alive);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < SURV_KC; ++c) woff[c * 32 + warp] = __popc(bal[c]);
     }
     __syncthreads();
-    if (threadIdx.x == 0) carry += total;
+    // (c, warp) slots in list order: chunk-major, warp-minor
+    const int x = threadIdx.x < SURV_KC * 32 ? woff[threadIdx.x] : 0;
+    int xo, total;
+    Scan(tmp).ExclusiveSum(x, xo, total);
     __syncthreads();
+    if (threadIdx.x < SURV_KC * 32) woff[threadIdx.x] = xo;
+    if (threadIdx.x == 0) carry = total;
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+    for (int c = 0; c < SURV_KC; ++c) {
+      const int p = c * 1024 + threadIdx.x;
+      if (p < n) {
+        const int pos = woff[c * 32 + warp] + __popc(bal[c] & below);
+        a.pcnt[base + p] = pos;
+        if ((bal[c] >> lane) & 1u) surv_write(a, base, tot, pos, iv[c]);
+      }
+    }
+  } else {
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < n; s0 += 1024) {
+      const int p = s0 + threadIdx.x;
+      const int i = p < n ? order[p] : 0;
+      const int alive = (p < n && a.flag[base + i] == 0u) ? 1 : 0;
+      int off, total;
+      Scan(tmp).ExclusiveSum(alive, off, total);
+      if (p < n) a.pcnt[base + p] = carry + off;
+      if (alive) surv_write(a, base, tot, carry + off, i);
+      __syncthreads();
+      if (threadIdx.x == 0) carry += total;
+      __syncthreads();
+    }
   }
+  __syncthreads();
   const int total = carry;
   const int NB = a.S + 2;
   const int* bst = a.bstart + (long long)job * NB;
