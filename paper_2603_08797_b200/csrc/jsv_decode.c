@@ -100,7 +100,8 @@ static PyObject* verdict(PyObject* cls, PyObject* name, PyObject* subject, int p
 /* decode(buf, n, layout, meta, demands, wall_ms) -> list[PlanResult]
  * meta = (ids, keys_full, topo_t, topo_i, task_t, task_i, edge_names, edge_idx,
  *         paths, path_names, a_max, binding_names,
- *         PlanResult, Configuration, ConstraintVerdict, SolverStats) */
+ *         PlanResult, Configuration, ConstraintVerdict, SolverStats, key_hashes)
+ * key_hashes[ti][k] = hash(keys_full[ti][k]), computed once per lowering */
 static PyObject* decode(PyObject* self, PyObject* args) {
   (void)self;
   Py_buffer view;
@@ -131,13 +132,20 @@ static PyObject* decode(PyObject* self, PyObject* args) {
     PyBuffer_Release(&view);
     return NULL;
   }
-  if (PyTuple_GET_SIZE(meta) != 16 || view.len < n * L.size || PyList_GET_SIZE(demands) < n) {
+  if (PyTuple_GET_SIZE(meta) != 17 || view.len < n * L.size || PyList_GET_SIZE(demands) < n) {
     PyBuffer_Release(&view);
     PyErr_SetString(PyExc_ValueError, "decode: bad arguments");
     return NULL;
   }
   PyObject* ids = PyTuple_GET_ITEM(meta, 0);
   PyObject* keys_full = PyTuple_GET_ITEM(meta, 1);
+  PyObject* key_hashes = PyTuple_GET_ITEM(meta, 16);
+  if (!PyTuple_Check(key_hashes) || !PyTuple_Check(keys_full) ||
+      PyTuple_GET_SIZE(key_hashes) != PyTuple_GET_SIZE(keys_full)) {
+    PyBuffer_Release(&view);
+    PyErr_SetString(PyExc_ValueError, "decode: bad key hashes");
+    return NULL;
+  }
   PyObject* topo_t = PyTuple_GET_ITEM(meta, 2);
   PyObject* topo_i = PyTuple_GET_ITEM(meta, 3);
   PyObject* task_t = PyTuple_GET_ITEM(meta, 4);
@@ -223,12 +231,14 @@ static PyObject* decode(PyObject* self, PyObject* args) {
     for (Py_ssize_t k = 0; k < NT; ++k) {
       const long ti = ti_topo[k];
       PyObject* kt = PyTuple_GET_ITEM(keys_full, ti);
+      PyObject* kh = PyTuple_GET_ITEM(key_hashes, ti);
       const int ni = rd_i32(b, L.n_items, ti);
       for (int j = 0; j < ni; ++j) {
         const uint32_t w = rd_u32(b, L.items, ti * L.max_items + j);
+        const Py_hash_t h = (Py_hash_t)PyLong_AsSsize_t(PyTuple_GET_ITEM(kh, w >> 16));
         PyObject* v = pfloat(rd_f64(b, L.hput, ti * L.max_items + j));
         NN(v);
-        int rc = PyDict_SetItem(hput, PyTuple_GET_ITEM(kt, w >> 16), v);
+        int rc = _PyDict_SetItem_KnownHash(hput, PyTuple_GET_ITEM(kt, w >> 16), v, h);
         Py_DECREF(v);
         CHK(rc);
       }

@@ -207,7 +207,9 @@ def _dec_meta(app, lw: LW.Lowered) -> tuple:
             tuple(idx[t] for t in task_t), tuple(e for e, _ in edges), tuple(k for _, k in edges),
             tuple(lw.paths), tuple("->".join(p) for p in lw.paths), float(lw.a_max),
             tuple(N.BINDING_NAMES[k] for k in range(len(N.BINDING_NAMES))),
-            PlanResult, Configuration, ConstraintVerdict, SolverStats)
+            PlanResult, Configuration, ConstraintVerdict, SolverStats,
+            # the keys' hashes (hput dict inserts skip the dataclass __hash__)
+            tuple(tuple(hash(k) for k in ks) for ks in keys_full))
     lw.arrays["_dec_meta"] = (g, meta)
     return meta
 
@@ -374,8 +376,14 @@ def plan_batch(
     apps = list(apps) if apps is not None else [app] * len(requests)
     r0 = requests[0]
     ov0 = dict(r0.factor_overrides or {})
+    sp0 = r0.space
     for r in requests[1:]:
-        if (r.slice_budget != r0.slice_budget or r.space != r0.space or r.slack != r0.slack
+        sp = r.space
+        if (r.slice_budget != r0.slice_budget or r.slack != r0.slack
+                or (sp is not sp0 and (sp.__class__ is not sp0.__class__
+                                       or sp.accuracy_scaling != sp0.accuracy_scaling
+                                       or sp.spatial_partitioning != sp0.spatial_partitioning
+                                       or sp.task_graph_informed != sp0.task_graph_informed))
                 or (r.factor_overrides is not r0.factor_overrides
                     and dict(r.factor_overrides or {}) != ov0)):
             raise ConfigError("plan_batch requests must share budget, space, slack and overrides")
