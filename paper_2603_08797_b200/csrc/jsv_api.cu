@@ -1258,13 +1258,16 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   // chunks' probe ranges are ordered); probe i folds slots [poff[i], poff[n + 1 + i])
   const size_t smem = x_smem_bytes(max_pn_last, p.P, a.fast != 0);
   const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
-  std::vector<double> wr(n, 0.0), wc(n + 1, 0.0);
+  std::vector<double> wr(n, 0.0), iwr(n, 0.0), wc(n + 1, 0.0);
   for (int i = 0; i < n; ++i) {
     const int pn = xp[i].pn[T - 1];
     wr[i] = a.rpl ? 1000.0 + 112.0 * ((pn + 31) / 32) : 1000.0 + 4.0 * pn;
+    iwr[i] = 1.0 / wr[i];
     wc[i + 1] = wc[i] + wr[i] * (double)(roff[i + 1] - roff[i]);
   }
   std::vector<long long> cstart(1, 0);
+  cstart.reserve(4096);
+  const double inv2g = 1.0 / (2.0 * (double)G);
   {
     const long long min_rounds = 4 * (XBLOCK / 32);
     long long r = 0;
@@ -1272,7 +1275,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     while (r < n_rounds) {
       while (pi < n - 1 && roff[pi + 1] <= r) ++pi;
       const double done = wc[pi] + wr[pi] * (double)(r - roff[pi]);
-      const double target = std::max(0.0, (wc[n] - done) / (2.0 * (double)G));
+      const double target = std::max(0.0, (wc[n] - done) * inv2g);
       // advance by `target` cost from round r
       long long e = r;
       double left = target;
@@ -1280,7 +1283,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
       while (e < n_rounds && left > 0) {
         while (pj < n - 1 && roff[pj + 1] <= e) ++pj;
         const long long avail = roff[pj + 1] - e;
-        const long long take = std::min<long long>(avail, (long long)std::ceil(left / wr[pj]));
+        const long long take = std::min<long long>(avail, (long long)std::ceil(left * iwr[pj]));
         e += take;
         left -= (double)take * wr[pj];
       }
