@@ -85,6 +85,20 @@ static PyObject* pbool(int x) { return Py_NewRef(x ? Py_True : Py_False); }
     if (!(x)) goto fail; \
   } while (0)
 
+/* The cyclic GC only needs to see objects that can be part of a reference
+ * cycle.  Immutable objects built here whose referents are all untracked
+ * (strings, numbers, or objects untracked by this rule) cannot be, so they are
+ * untracked as soon as they are complete -- the rule CPython applies to tuples
+ * lazily during a collection, applied eagerly (and to the frozen dataclasses
+ * filled here) so that the ~20 short-lived objects per result stay out of
+ * every gen-0 traversal and never get promoted. */
+static void untrack_tuple(PyObject* t) {
+  for (Py_ssize_t k = 0; k < PyTuple_GET_SIZE(t); ++k)
+    if (PyObject_GC_IsTracked(PyTuple_GET_ITEM(t, k))) return;
+  PyObject_GC_UnTrack(t);
+}
+
+/* ConstraintVerdict(name: str, subject: str, passed: bool, margin: float) */
 static PyObject* verdict(PyObject* cls, PyObject* name, PyObject* subject, int passed,
                          double margin) {
   PyObject* o = new_of(cls);
@@ -94,6 +108,7 @@ static PyObject* verdict(PyObject* cls, PyObject* name, PyObject* subject, int p
     Py_DECREF(o);
     return NULL;
   }
+  if (!PyObject_GC_IsTracked(name) && !PyObject_GC_IsTracked(subject)) PyObject_GC_UnTrack(o);
   return o;
 }
 
@@ -196,8 +211,16 @@ static PyObject* decode(PyObject* self, PyObject* args) {
     NN(stats = new_of(C_st));
     CHK(put(stats, a_nodes, pint(rd_i64(b, L.nodes))));
     CHK(put(stats, a_wall, pfloat(wall_ms)));
-    CHK(put(stats, a_pool, sizes)); sizes = NULL;
-    CHK(put(stats, a_trunc, PyList_AsTuple(cut)));
+    {
+      /* SolverStats(nodes, wall_ms, pool_sizes: {str: int}, truncated_tasks: (str, ...)) */
+      PyObject* tt = PyList_AsTuple(cut);
+      NN(tt);
+      untrack_tuple(tt);
+      const int leaf = !PyObject_GC_IsTracked(sizes) && !PyObject_GC_IsTracked(tt);
+      CHK(put(stats, a_pool, sizes)); sizes = NULL;
+      CHK(put(stats, a_trunc, tt));
+      if (leaf) PyObject_GC_UnTrack(stats);
+    }
     Py_CLEAR(cut);
     const int code = rd_i32(b, L.binding, 0);
     PyObject* bind = code < 0 ? Py_None : PyTuple_GET_ITEM(bnames, code);
@@ -222,6 +245,7 @@ static PyObject* decode(PyObject* self, PyObject* args) {
         const uint32_t w = rd_u32(b, L.items, ti * L.max_items + k);
         PyObject* e = Py_BuildValue("(On)", PyTuple_GET_ITEM(kt, w >> 16), (Py_ssize_t)(w & 0xFFFFu));
         NN(e);
+        untrack_tuple(e);
         int rc = PyList_Append(m, e);
         Py_DECREF(e);
         CHK(rc);
@@ -256,11 +280,14 @@ static PyObject* decode(PyObject* self, PyObject* args) {
       bad = PyList_AsTuple(bl);
       Py_DECREF(bl);
       NN(bad);
+      untrack_tuple(bad);
     }
     NN(cfg = new_of(C_cfg));
     {
       PyObject* mt = PyList_AsTuple(m);
       Py_CLEAR(m);
+      NN(mt);
+      untrack_tuple(mt);
       CHK(put(cfg, a_m, mt));
     }
     CHK(put(cfg, a_entry, PyNumber_Float(PyList_GET_ITEM(demands, i))));
@@ -328,6 +355,7 @@ static PyObject* decode(PyObject* self, PyObject* args) {
       Py_DECREF(subj);
       if (!v) { Py_DECREF(objv); goto fail; }
       PyTuple_SET_ITEM(vs, q++, v);
+      untrack_tuple(vs);
     }
     {
       const int feas = rd_i32(b, L.feasible, 0) != 0;

@@ -622,26 +622,62 @@ __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
+  __shared__ int woff[SURV_KC * 32];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
   const long long base = job_base(a, probe, t);
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
-  for (int s0 = 0; s0 < n; s0 += 1024) {
-    int i = s0 + threadIdx.x;
-    int alive = (i < n && a.flag[base + i] == 0u) ? 1 : 0;
-    int off, total;
-    Scan(tmp).ExclusiveSum(alive, off, total);
-    if (alive) {
-      a.front[base + carry + off] = i;
-      a.fpos[base + carry + off] = 0;
-      a.fcr[base + carry + off] = 0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (n <= SURV_KC * 1024) {
+    // every chunk's flags loaded up front; offsets from ballot counts and one
+    // block scan (as k_surv)
+    unsigned bal[SURV_KC];
+#pragma unroll
+    for (int c = 0; c < SURV_KC; ++c) {
+      const int i = c * 1024 + threadIdx.x;
+      bal[c] = __ballot_sync(0xffffffffu, i < n && a.flag[base + i] == 0u);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < SURV_KC; ++c) woff[c * 32 + warp] = __popc(bal[c]);
     }
     __syncthreads();
-    if (threadIdx.x == 0) carry += total;
+    const int x = threadIdx.x < SURV_KC * 32 ? woff[threadIdx.x] : 0;
+    int xo, total;
+    Scan(tmp).ExclusiveSum(x, xo, total);
     __syncthreads();
+    if (threadIdx.x < SURV_KC * 32) woff[threadIdx.x] = xo;
+    if (threadIdx.x == 0) carry = total;
+    __syncthreads();
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll
+    for (int c = 0; c < SURV_KC; ++c) {
+      if ((bal[c] >> lane) & 1u) {
+        const int pos = woff[c * 32 + warp] + __popc(bal[c] & below);
+        a.front[base + pos] = c * 1024 + threadIdx.x;
+        a.fpos[base + pos] = 0;
+        a.fcr[base + pos] = 0;
+      }
+    }
+  } else {
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < n; s0 += 1024) {
+      int i = s0 + threadIdx.x;
+      int alive = (i < n && a.flag[base + i] == 0u) ? 1 : 0;
+      int off, total;
+      Scan(tmp).ExclusiveSum(alive, off, total);
+      if (alive) {
+        a.front[base + carry + off] = i;
+        a.fpos[base + carry + off] = 0;
+        a.fcr[base + carry + off] = 0;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) carry += total;
+      __syncthreads();
+    }
   }
+  __syncthreads();
   if (threadIdx.x == 0) a.fcnt[job] = carry;
   push_items(a, 2, job, carry, 1024, false);
 }

@@ -450,3 +450,12 @@ def test_c_decoder_equals_python_decoder(name):
         if w.config is not None:
             assert g.config.m == w.config.m and list(g.config.hput) == list(w.config.hput)
             assert list(g.config.demand_rps) == list(w.config.demand_rps)
+    # leaf objects (verdicts, stats, their tuples) are built untracked by the
+    # cyclic GC; a gc pass finds nothing to collect and the values stay intact
+    import gc
+
+    for g in got:
+        assert all(not gc.is_tracked(v) for v in g.verdicts)
+        assert not gc.is_tracked(g.verdicts) and not gc.is_tracked(g.stats)
+    gc.collect()
+    assert [repr(g) for g in got] == [repr(w) for w in want]

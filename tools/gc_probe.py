@@ -10,13 +10,15 @@ reqs = [PlanRequest(d, 28, SearchSpace(True, True, True)) for d in bench.demand_
 P.set_strategy("exhaustive", 1 << 40, device=0)
 for _ in range(6):
     P.plan_batch(app, table, reqs, device=0)
-for label in ("gc on", "gc off", "gc on", "gc off"):
-    (gc.disable if label == "gc off" else gc.enable)()
+for label in ("gc on", "gc off", "gc on", "gc off", "gc on discard", "gc off discard", "gc on discard", "gc off discard"):
+    (gc.disable if label.startswith("gc off") else gc.enable)()
     keep = []
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(50):
-        keep.append(P.plan_batch(app, table, reqs, device=0))
+        r = P.plan_batch(app, table, reqs, device=0)
+        if "discard" not in label:
+            keep.append(r)
     dt = (time.perf_counter() - t0) / 50 * 1e3
     print(label, round(dt, 4), "ms per batch")
 gc.enable()
