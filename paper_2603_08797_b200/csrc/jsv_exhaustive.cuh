@@ -938,12 +938,56 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(const __grid_constant__ X
   XBest best;
   best.has = 0; best.sl = 0; best.obj = 0.0; best.idx = 0;
   unsigned long long leaves = 0;
-  for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
-    const XPart& p = a.part[i];
-    XBest c;
-    c.has = p.has; c.sl = p.sl; c.obj = p.obj; c.idx = p.idx;
-    if (x_better(a, xp, probe, c, best)) best = c;
-    leaves += p.leaves;
+  // LEAF_FULL: first the best (objective, slices) key over the parts -- no m
+  // comparisons -- then only the parts holding exactly that key are folded by
+  // x_better (m ties).  Usually one part holds it and no m comparison runs.
+  // (A NaN objective keeps the plain fold: x_better's order is not total then.)
+  bool key_pass = a.mode == LEAF_FULL;
+  int kh = 0, ks = 0;
+  double ko = 0.0;
+  if (key_pass) {
+    int nan = 0;
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const XPart& p = a.part[i];
+      leaves += p.leaves;
+      if (!p.has) continue;
+      nan |= p.obj != p.obj;
+      if (!kh || p.obj > ko || (p.obj == ko && p.sl < ks)) { kh = 1; ko = p.obj; ks = p.sl; }
+    }
+    for (int d = 16; d > 0; d >>= 1) {
+      const int oh = __shfl_down_sync(0xffffffffu, kh, d);
+      const double oo = __shfl_down_sync(0xffffffffu, ko, d);
+      const int os = __shfl_down_sync(0xffffffffu, ks, d);
+      if (oh && (!kh || oo > ko || (oo == ko && os < ks))) { kh = 1; ko = oo; ks = os; }
+    }
+    nan = __any_sync(0xffffffffu, nan);
+    if ((threadIdx.x & 31) == 0) {
+      s_warp[threadIdx.x >> 5].has = kh;
+      s_warp[threadIdx.x >> 5].obj = ko;
+      s_warp[threadIdx.x >> 5].sl = ks;
+      s_warp[threadIdx.x >> 5].idx = nan;
+    }
+    __syncthreads();
+    kh = 0;
+    int any_nan = 0;
+    for (int w = 0; w < XBLOCK / 32; ++w) {
+      const XBest& o = s_warp[w];
+      any_nan |= (int)o.idx;
+      if (o.has && (!kh || o.obj > ko || (o.obj == ko && o.sl < ks))) { kh = 1; ko = o.obj; ks = o.sl; }
+    }
+    __syncthreads();
+    key_pass = !any_nan;
+  } else {
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) leaves += a.part[i].leaves;
+  }
+  if (!key_pass || kh) {
+    for (long long i = b0 + threadIdx.x; i < b1; i += blockDim.x) {
+      const XPart& p = a.part[i];
+      if (!p.has || (key_pass && (p.obj != ko || p.sl != ks))) continue;
+      XBest c;
+      c.has = p.has; c.sl = p.sl; c.obj = p.obj; c.idx = p.idx;
+      if (x_better(a, xp, probe, c, best)) best = c;
+    }
   }
   for (int d = 16; d > 0; d >>= 1) {
     const XBest o = x_shfl_down(best, d);
