@@ -213,7 +213,12 @@ __global__ void k_finalize(const __grid_constant__ FinArgs a) {
 
 int launch_finalize(const FinArgs& a, cudaStream_t st) {
   PROF_BEGIN(K_FINALIZE);
-  k_finalize<<<(a.n_probes + 63) / 64, 64, 0, st>>>(a);
+  // one thread per probe, spread over the SMs: each thread writes its ~5 KB
+  // record with scattered stores, so few lanes per SM keep the LSUs from
+  // serialising (64 probes: 64 one-thread blocks)
+  int tpb = 1;
+  while (tpb * 148 < a.n_probes && tpb < 64) tpb <<= 1;
+  k_finalize<<<(a.n_probes + tpb - 1) / tpb, tpb, 0, st>>>(a);
   PROF_END();
   return 1;
 }
