@@ -266,7 +266,10 @@ __device__ void push_items(const S1Args& a, int k, int job, int n, int jchunk, b
 // Counting sort of a job's candidates by slice count: order[] and bucket starts
 // bstart[s] = #candidates with fewer than s slices (s = 0 .. S+1).
 #define BUCKET_SMEM_MAX 12288
-__global__ void __launch_bounds__(1024) k_bucket(const __grid_constant__ S1Args a) {
+// (JOB_BS threads: two job blocks per SM at <= 64 registers, so a batch's
+// jobs run in one wave)
+#define JOB_BS 512
+__global__ void __launch_bounds__(JOB_BS, 2) k_bucket(const __grid_constant__ S1Args a) {
   extern __shared__ int hist[];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
@@ -530,7 +533,8 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
 
 // Survivors of the same-bucket pass, in slices order, and their bucket starts
 // sbst[s] = #survivors with fewer than s slices.
-#define SURV_KC 12
+#define SURV_KC 24
+#define JOB_W (JOB_BS / 32)
 __device__ __forceinline__ void surv_write(const S1Args& a, long long base, long long tot, int pos, int i) {
   a.surv[base + pos] = i;
   for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
@@ -539,11 +543,11 @@ __device__ __forceinline__ void surv_write(const S1Args& a, long long base, long
                                      (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
 }
 
-__global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a) {
-  typedef cub::BlockScan<int, 1024> Scan;
+__global__ void __launch_bounds__(JOB_BS, 2) k_surv(const __grid_constant__ S1Args a) {
+  typedef cub::BlockScan<int, JOB_BS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
-  __shared__ int woff[SURV_KC * 32];
+  __shared__ int woff[SURV_KC * JOB_W];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
@@ -551,50 +555,44 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
   const long long tot = (long long)a.n_probes * a.C_probe;
   const int* order = a.order + base;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (n <= SURV_KC * 1024) {
+  if (n <= SURV_KC * JOB_BS) {
     // every chunk's list entries and flags loaded up front (no load latency
     // between chunks), survivor offsets from per-(chunk, warp) ballot counts
     // and ONE block scan over them
-    int iv[SURV_KC];
     unsigned bal[SURV_KC];
 #pragma unroll
     for (int c = 0; c < SURV_KC; ++c) {
-      const int p = c * 1024 + threadIdx.x;
-      iv[c] = p < n ? order[p] : 0;
-    }
-#pragma unroll
-    for (int c = 0; c < SURV_KC; ++c) {
-      const int p = c * 1024 + threadIdx.x;
-      const bool alive = p < n && a.flag[base + iv[c]] == 0u;
+      const int p = c * JOB_BS + threadIdx.x;
+      const bool alive = p < n && a.flag[base + order[p]] == 0u;
       bal[c] = __ballot_sync(0xffffffffu, alive);
     }
     if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < SURV_KC; ++c) woff[c * 32 + warp] = __popc(bal[c]);
+      for (int c = 0; c < SURV_KC; ++c) woff[c * JOB_W + warp] = __popc(bal[c]);
     }
     __syncthreads();
     // (c, warp) slots in list order: chunk-major, warp-minor
-    const int x = threadIdx.x < SURV_KC * 32 ? woff[threadIdx.x] : 0;
+    const int x = threadIdx.x < SURV_KC * JOB_W ? woff[threadIdx.x] : 0;
     int xo, total;
     Scan(tmp).ExclusiveSum(x, xo, total);
     __syncthreads();
-    if (threadIdx.x < SURV_KC * 32) woff[threadIdx.x] = xo;
+    if (threadIdx.x < SURV_KC * JOB_W) woff[threadIdx.x] = xo;
     if (threadIdx.x == 0) carry = total;
     __syncthreads();
     const unsigned below = (1u << lane) - 1u;
 #pragma unroll
     for (int c = 0; c < SURV_KC; ++c) {
-      const int p = c * 1024 + threadIdx.x;
+      const int p = c * JOB_BS + threadIdx.x;
       if (p < n) {
-        const int pos = woff[c * 32 + warp] + __popc(bal[c] & below);
+        const int pos = woff[c * JOB_W + warp] + __popc(bal[c] & below);
         a.pcnt[base + p] = pos;
-        if ((bal[c] >> lane) & 1u) surv_write(a, base, tot, pos, iv[c]);
+        if ((bal[c] >> lane) & 1u) surv_write(a, base, tot, pos, order[p]);
       }
     }
   } else {
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int s0 = 0; s0 < n; s0 += 1024) {
+    for (int s0 = 0; s0 < n; s0 += JOB_BS) {
       const int p = s0 + threadIdx.x;
       const int i = p < n ? order[p] : 0;
       const int alive = (p < n && a.flag[base + i] == 0u) ? 1 : 0;
@@ -618,43 +616,43 @@ __global__ void __launch_bounds__(1024) k_surv(const __grid_constant__ S1Args a)
   push_items(a, 1, job, total, 1024, true);
 }
 
-__global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args a) {
-  typedef cub::BlockScan<int, 1024> Scan;
+__global__ void __launch_bounds__(JOB_BS, 2) k_compact(const __grid_constant__ S1Args a) {
+  typedef cub::BlockScan<int, JOB_BS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
-  __shared__ int woff[SURV_KC * 32];
+  __shared__ int woff[SURV_KC * JOB_W];
   const int job = blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
   const long long base = job_base(a, probe, t);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (n <= SURV_KC * 1024) {
+  if (n <= SURV_KC * JOB_BS) {
     // every chunk's flags loaded up front; offsets from ballot counts and one
     // block scan (as k_surv)
     unsigned bal[SURV_KC];
 #pragma unroll
     for (int c = 0; c < SURV_KC; ++c) {
-      const int i = c * 1024 + threadIdx.x;
+      const int i = c * JOB_BS + threadIdx.x;
       bal[c] = __ballot_sync(0xffffffffu, i < n && a.flag[base + i] == 0u);
     }
     if (lane == 0) {
 #pragma unroll
-      for (int c = 0; c < SURV_KC; ++c) woff[c * 32 + warp] = __popc(bal[c]);
+      for (int c = 0; c < SURV_KC; ++c) woff[c * JOB_W + warp] = __popc(bal[c]);
     }
     __syncthreads();
-    const int x = threadIdx.x < SURV_KC * 32 ? woff[threadIdx.x] : 0;
+    const int x = threadIdx.x < SURV_KC * JOB_W ? woff[threadIdx.x] : 0;
     int xo, total;
     Scan(tmp).ExclusiveSum(x, xo, total);
     __syncthreads();
-    if (threadIdx.x < SURV_KC * 32) woff[threadIdx.x] = xo;
+    if (threadIdx.x < SURV_KC * JOB_W) woff[threadIdx.x] = xo;
     if (threadIdx.x == 0) carry = total;
     __syncthreads();
     const unsigned below = (1u << lane) - 1u;
 #pragma unroll
     for (int c = 0; c < SURV_KC; ++c) {
       if ((bal[c] >> lane) & 1u) {
-        const int pos = woff[c * 32 + warp] + __popc(bal[c] & below);
-        a.front[base + pos] = c * 1024 + threadIdx.x;
+        const int pos = woff[c * JOB_W + warp] + __popc(bal[c] & below);
+        a.front[base + pos] = c * JOB_BS + threadIdx.x;
         a.fpos[base + pos] = 0;
         a.fcr[base + pos] = 0;
       }
@@ -662,7 +660,7 @@ __global__ void __launch_bounds__(1024) k_compact(const __grid_constant__ S1Args
   } else {
     if (threadIdx.x == 0) carry = 0;
     __syncthreads();
-    for (int s0 = 0; s0 < n; s0 += 1024) {
+    for (int s0 = 0; s0 < n; s0 += JOB_BS) {
       int i = s0 + threadIdx.x;
       int alive = (i < n && a.flag[base + i] == 0u) ? 1 : 0;
       int off, total;
@@ -1053,7 +1051,7 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
     const int NB = a.S + 2;
     const size_t smem = NB <= BUCKET_SMEM_MAX ? sizeof(int) * NB : 0;
     PROF_BEGIN(K_BUCKET);
-    k_bucket<<<a.n_probes * a.T, 1024, smem, st>>>(a);
+    k_bucket<<<a.n_probes * a.T, JOB_BS, smem, st>>>(a);
     PROF_END();
     ++launches;
   }
@@ -1073,7 +1071,7 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
         DISPATCH_D2(a.D, k_pairs_l, false, gl, a, 0);
       }
     }
-    k_surv<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+    k_surv<<<a.n_probes * a.T, JOB_BS, 0, st>>>(a);
     // survivors pass: the same barrier-free kernel (float-shadow quick reject in
     // survivor order, built by k_surv); JSV_PAIRS_A1 selects the tiled kernel
     if (tiled1) {
@@ -1087,7 +1085,7 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
     launches += 3;
   }
   PROF_BEGIN(K_COMPACT);
-  k_compact<<<a.n_probes * a.T, 1024, 0, st>>>(a);
+  k_compact<<<a.n_probes * a.T, JOB_BS, 0, st>>>(a);
   PROF_END();
   ++launches;
   if (L.tiles_pp > 0) {
