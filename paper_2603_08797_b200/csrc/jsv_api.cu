@@ -672,23 +672,32 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   fill_req(p, rq, hreq);
   auto& B = c.buf;
   CK(B[B_REQ].ensure(sizeof(DReq)));
-  CK(cudaMemcpyAsync(B[B_REQ].p, &hreq, sizeof(DReq), cudaMemcpyHostToDevice, st));
   CK(B[B_PROBES].ensure(sizeof(DProbe) * n));
-  CK(cudaMemcpyAsync(B[B_PROBES].p, probes, sizeof(DProbe) * n, cudaMemcpyHostToDevice, st));
   CK(B[B_DESC].ensure(sizeof(GenDesc) * std::max<size_t>(1, pl.desc.size())));
-  if (!pl.desc.empty())
-    CK(cudaMemcpyAsync(B[B_DESC].p, pl.desc.data(), sizeof(GenDesc) * pl.desc.size(),
-                       cudaMemcpyHostToDevice, st));
-  CK(B[B_WAYS].ensure(sizeof(unsigned) * pl.ways.size()));
-  CK(cudaMemcpyAsync(B[B_WAYS].p, pl.ways.data(), sizeof(unsigned) * pl.ways.size(),
-                     cudaMemcpyHostToDevice, st));
+  CK(B[B_WAYS].ensure(sizeof(unsigned) * std::max<size_t>(1, pl.ways.size())));
   CK(B[B_TILE_TASK].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_task.size())));
   CK(B[B_TILE_START].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_start.size())));
-  if (!pl.tile_task.empty()) {
-    CK(cudaMemcpyAsync(B[B_TILE_TASK].p, pl.tile_task.data(), sizeof(int) * pl.tile_task.size(),
-                       cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size(),
-                       cudaMemcpyHostToDevice, st));
+  {
+    // the batch's inputs staged in pinned memory: truly asynchronous copies
+    // (pageable sources would each be a staged, host-blocking transfer)
+    struct Up { void* dst; const void* src; size_t bytes; };
+    const Up ups[] = {{B[B_REQ].p, &hreq, sizeof(DReq)},
+                      {B[B_PROBES].p, probes, sizeof(DProbe) * n},
+                      {B[B_DESC].p, pl.desc.data(), sizeof(GenDesc) * pl.desc.size()},
+                      {B[B_WAYS].p, pl.ways.data(), sizeof(unsigned) * pl.ways.size()},
+                      {B[B_TILE_TASK].p, pl.tile_task.data(), sizeof(int) * pl.tile_task.size()},
+                      {B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size()}};
+    size_t total = 0;
+    for (const Up& u : ups) total += (u.bytes + 15) & ~size_t(15);
+    char* h = static_cast<char*>(c.pinned(total));
+    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    size_t off = 0;
+    for (const Up& u : ups) {
+      if (u.bytes == 0) continue;
+      memcpy(h + off, u.src, u.bytes);
+      CK(cudaMemcpyAsync(u.dst, h + off, u.bytes, cudaMemcpyHostToDevice, st));
+      off += (u.bytes + 15) & ~size_t(15);
+    }
   }
   const size_t C1 = (size_t)std::max<long long>(1, Ctot);
   CK(B[B_ITEMS].ensure(sizeof(uint32_t) * C1 * pl.maxi));
