@@ -260,6 +260,7 @@ static PyObject* decode(PyObject* self, PyObject* args) {
       for (int j = 0; j < ni; ++j) {
         const uint32_t w = rd_u32(b, L.items, ti * L.max_items + j);
         const Py_hash_t h = (Py_hash_t)PyLong_AsSsize_t(PyTuple_GET_ITEM(kh, w >> 16));
+        if (h == -1 && PyErr_Occurred()) goto fail;
         PyObject* v = pfloat(rd_f64(b, L.hput, ti * L.max_items + j));
         NN(v);
         int rc = _PyDict_SetItem_KnownHash(hput, PyTuple_GET_ITEM(kt, w >> 16), v, h);
