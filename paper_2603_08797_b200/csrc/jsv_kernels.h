@@ -90,7 +90,7 @@ struct S1Args {
   int* scnt;      // [jobs] survivors
   double* arrl;   // [D * Ctot] coordinates in list order (slices order, then survivor order)
   int* fsorted;   // [jobs] 1: k_front_sort computed the job's frontier ranks
-  float4* arrf;   // [Ctot] float shadow of coordinates 1..4 in bucket order (D == 5)
+  float4* arrf;   // [Ctot] float shadow of coordinates 1..4 in bucket order (D >= 5)
   int wl_mask;    // bit k: the launch consumes work list k (set by launch_stage1)
   int4* wl[3];    // pair-pass work lists {job, i0, j0}: same-bucket, survivors, frontier
   int* wn;        // [3] their lengths (zeroed per batch)

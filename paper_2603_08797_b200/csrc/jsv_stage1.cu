@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(JOB_BS, 2) k_bucket(const __grid_constant__ S1
     a.order[base + pos] = i;
     for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
     // float shadow of coordinates 1..4 (the same-slices pass's quick reject)
-    if (a.D == 5)
+    if (a.D >= 5)
       a.arrf[base + pos] = make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
                                        (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
   }
@@ -473,7 +473,7 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
   // quick reject on the float shadow: rounding to float is monotone, so
   // float(x_j) > float(x_i) in any coordinate proves x_j > x_i there (j cannot
   // dominate i); otherwise the exact double test below decides
-  constexpr bool FQ = SKIP0 && D == 5;
+  constexpr bool FQ = SKIP0 && D >= 5;
   float4 fi = make_float4(0.f, 0.f, 0.f, 0.f);
   if (FQ) fi = a.arrf[base + p];
   unsigned fl = 0;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256) k_pairs_l(const __grid_constant__ S1Args 
 __device__ __forceinline__ void surv_write(const S1Args& a, long long base, long long tot, int pos, int i) {
   a.surv[base + pos] = i;
   for (int d = 0; d < a.D; ++d) a.arrl[d * tot + base + pos] = a.arr[d * tot + base + i];
-  if (a.D == 5)
+  if (a.D >= 5)
     a.arrf[base + pos] = make_float4((float)a.arr[1 * tot + base + i], (float)a.arr[2 * tot + base + i],
                                      (float)a.arr[3 * tot + base + i], (float)a.arr[4 * tot + base + i]);
 }
@@ -1029,7 +1029,7 @@ int stage1_padded_dims(int D) { return pick_D(D); }
 int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
   int launches = 0;
   // the tiled pair kernels read device work lists; the barrier-free ones do not
-  const bool tiled = a0.D > 8 || getenv("JSV_PAIRS_TILED") != nullptr;
+  const bool tiled = a0.D > 16 || getenv("JSV_PAIRS_TILED") != nullptr;
   const bool tiled1 = tiled || getenv("JSV_PAIRS_A1") != nullptr;
   S1Args a = a0;
   a.wl_mask = (tiled ? 1 : 0) | (tiled1 ? 2 : 0) | 4;
