@@ -10,9 +10,10 @@
 //                2-variant mixes are decoded from the unit index.
 //   k_stats      one thread per candidate: latency / capacity / slices /
 //                weighted accuracy + fan-out (all-equal short circuit).
-//   k_pairs_l    same-slices pass of the skyline, one thread per candidate over
-//                list-ordered coordinates (k_pairs_a: tiled form, used for the
-//                survivors pass and for wide rows):
+//   k_pairs_l    both skyline passes (same slices; survivors with fewer
+//                slices), one thread per candidate over list-ordered
+//                coordinates with a float shadow quick reject (k_pairs_a: tiled
+//                form, for rows of more than 16 coordinates):
 //   k_pairs_a    tiled all-pairs skyline: candidate i dies if another
 //                candidate weakly dominates it with a different row, or has an
 //                identical row and smaller items (the reference's dedup).  By
