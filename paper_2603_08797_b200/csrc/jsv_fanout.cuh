@@ -70,8 +70,11 @@ __device__ __forceinline__ bool fo_leaf_ok(const FoArgs& a, int probe, int b0, i
 __global__ void __launch_bounds__(256) k_fo_prep(const __grid_constant__ FoArgs a) {
   __shared__ double sacc[1024];  // feasible bundles of one leaf as (slices, accuracy) pairs
   __shared__ int ssl[1024];
-  __shared__ int sflag[1024];
-  __shared__ int scount;
+  __shared__ int msl[1024];       // DP classes: per slices value, the largest accuracy
+  __shared__ double mac[1024];
+  __shared__ int scount, smcount;
+  typedef cub::BlockScan<int, 256> FoScan;
+  __shared__ typename FoScan::TempStorage ftmp;
   const S2Args& s = a.s;
   const int probe = blockIdx.x / a.P0max, b0 = blockIdx.x % a.P0max;
   const int T = s.T;
@@ -89,95 +92,108 @@ __global__ void __launch_bounds__(256) k_fo_prep(const __grid_constant__ FoArgs 
   const int s0 = s.p_sl[q0];
   // entry throughput verdict; the budget must leave room for the entry itself
   const bool b0_ok = (s.p_cap[q0] - pr.demand * sf >= 0) && (s0 <= a.SB);
-  for (int j = 0; j < a.k; ++j) {
+  // Leaves in reverse order: each leaf's class list is built (global, for
+  // k_fo_enum) and its suffix-DP step taken at once.  The DP only needs, per
+  // slices value, the class of largest accuracy (w is monotone in it and the
+  // rest term depends on slices alone), so the step runs over <= SB + 1
+  // classes held in shared memory -- the same maxima as over every class.
+  const int SB = a.SB;
+  for (int sv = threadIdx.x; sv <= SB; sv += blockDim.x)
+    a.F[fo_F_base(a, probe, b0, a.k) + sv] = (sv == 0) ? 0.0 : -INFINITY;
+  for (int j = a.k - 1; j >= 0; --j) {
     const int lt = a.leaf[j];
     const int Pl = s.pool_n[probe * T + lt];
     const double r = fo_leaf_demand(a, probe, b0, j);
     const long long cb = fo_cls_base(a, probe, b0, j);
+    __syncthreads();
     if (r == 0.0) {
       // only "no instances" (planner.py:868-875): slices 0, accuracy 1.0
       if (threadIdx.x == 0) {
         a.cls[cb].acc = 1.0; a.cls[cb].s = 0;
         a.ncls[bq * a.k + j] = 1;
+        msl[0] = 0; mac[0] = 1.0;
+        smcount = 1;
       }
-      continue;
-    }
-    const double need = r * sf;
-    int n2 = 1;
-    while (n2 < Pl) n2 <<= 1;
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-      if (i < Pl && fo_leaf_ok(a, probe, b0, j, i, need)) {
-        const long long q = (long long)(probe * T + lt) * s.W + i;
-        ssl[i] = s.p_sl[q];
-        sacc[i] = s.p_acc[q];
-      } else {
-        ssl[i] = 0x7FFFFFFF;
-        sacc[i] = INFINITY;
+    } else {
+      const double need = r * sf;
+      int n2 = 1;
+      while (n2 < Pl) n2 <<= 1;
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        if (i < Pl && fo_leaf_ok(a, probe, b0, j, i, need)) {
+          const long long q = (long long)(probe * T + lt) * s.W + i;
+          ssl[i] = s.p_sl[q];
+          sacc[i] = s.p_acc[q];
+        } else {
+          ssl[i] = 0x7FFFFFFF;
+          sacc[i] = INFINITY;
+        }
       }
-    }
-    __syncthreads();
-    // bitonic sort by (slices, accuracy)
-    for (int kk = 2; kk <= n2; kk <<= 1) {
-      for (int jj = kk >> 1; jj > 0; jj >>= 1) {
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-          const int l = i ^ jj;
-          if (l > i) {
-            const bool up = (i & kk) == 0;
-            const bool gt = ssl[i] > ssl[l] || (ssl[i] == ssl[l] && sacc[i] > sacc[l]);
-            if (gt == up) {
-              const int ts = ssl[i]; ssl[i] = ssl[l]; ssl[l] = ts;
-              const double ta = sacc[i]; sacc[i] = sacc[l]; sacc[l] = ta;
+      __syncthreads();
+      // bitonic sort by (slices, accuracy)
+      for (int kk = 2; kk <= n2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            const int l = i ^ jj;
+            if (l > i) {
+              const bool up = (i & kk) == 0;
+              const bool gt = ssl[i] > ssl[l] || (ssl[i] == ssl[l] && sacc[i] > sacc[l]);
+              if (gt == up) {
+                const int ts = ssl[i]; ssl[i] = ssl[l]; ssl[l] = ts;
+                const double ta = sacc[i]; sacc[i] = sacc[l]; sacc[l] = ta;
+              }
             }
           }
+          __syncthreads();
+        }
+      }
+      // unique -> class list (global), and the last class of each slices value
+      // -> DP classes (shared); block scans over chunks of the sorted list
+      if (threadIdx.x == 0) { scount = 0; smcount = 0; }
+      __syncthreads();
+      for (int i0 = 0; i0 < n2; i0 += blockDim.x) {
+        const int i = i0 + threadIdx.x;
+        const bool valid = i < n2 && ssl[i] != 0x7FFFFFFF;
+        const int fu = valid && (i == 0 || ssl[i] != ssl[i - 1] || !(sacc[i] == sacc[i - 1]));
+        const int fm = valid && (i + 1 == n2 || ssl[i + 1] != ssl[i]);
+        int ou, tu, om, tm;
+        FoScan(ftmp).ExclusiveSum(fu, ou, tu);
+        __syncthreads();
+        FoScan(ftmp).ExclusiveSum(fm, om, tm);
+        if (fu) {
+          a.cls[cb + scount + ou].acc = sacc[i];
+          a.cls[cb + scount + ou].s = ssl[i];
+        }
+        if (fm) {
+          msl[smcount + om] = ssl[i];
+          mac[smcount + om] = sacc[i];
         }
         __syncthreads();
+        if (threadIdx.x == 0) { scount += tu; smcount += tm; }
+        __syncthreads();
       }
-    }
-    // unique -> class list
-    for (int i = threadIdx.x; i < n2; i += blockDim.x)
-      sflag[i] = (ssl[i] != 0x7FFFFFFF) &&
-                 (i == 0 || ssl[i] != ssl[i - 1] || !(sacc[i] == sacc[i - 1]));
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int c = 0;
-      for (int i = 0; i < n2; ++i)
-        if (sflag[i]) {
-          a.cls[cb + c].acc = sacc[i];
-          a.cls[cb + c].s = ssl[i];
-          ++c;
-        }
-      a.ncls[bq * a.k + j] = c;
-      scount = c;
+      if (threadIdx.x == 0) a.ncls[bq * a.k + j] = scount;
     }
     __syncthreads();
-  }
-  __syncthreads();
-  // suffix DP over leaves (real arithmetic: a bound, not a verdict)
-  const int SB = a.SB;
-  for (int sv = threadIdx.x; sv <= SB; sv += blockDim.x)
-    a.F[fo_F_base(a, probe, b0, a.k) + sv] = (sv == 0) ? 0.0 : -INFINITY;
-  __syncthreads();
-  for (int j = a.k - 1; j >= 0; --j) {
-    const long long cb = fo_cls_base(a, probe, b0, j);
-    const int nc = a.ncls[bq * a.k + j];
+    // suffix DP step (real arithmetic: a bound, not a verdict)
+    const int nm = smcount;
     const double frac = g.path_frac[j];
     const double* Fn = a.F + fo_F_base(a, probe, b0, j + 1);
     double* Fj = a.F + fo_F_base(a, probe, b0, j);
     for (int sv = threadIdx.x; sv <= SB; sv += blockDim.x) {
       double best = -INFINITY;
-      for (int c = 0; c < nc; ++c) {
-        const int sc = a.cls[cb + c].s;
+      for (int c = 0; c < nm; ++c) {
+        const int sc = msl[c];
         if (sc > sv) break;  // classes sorted by slices
         const double rest = Fn[sv - sc];
         if (rest == -INFINITY) continue;
-        const double w = frac * ((1.0 * acc0) * a.cls[cb + c].acc);
+        const double w = frac * ((1.0 * acc0) * mac[c]);
         const double v = w + rest;
         best = v > best ? v : best;
       }
       Fj[sv] = best;
     }
-    __syncthreads();
   }
+  __syncthreads();
   if (threadIdx.x == 0) {
     double best = -INFINITY;
     if (b0_ok) {

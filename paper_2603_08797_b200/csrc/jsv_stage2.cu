@@ -17,6 +17,7 @@
 // infeasible plan there is no incumbent, so the set of visited prefixes is
 // order-independent and the diagnostic re-run reproduces the reference's kill
 // counts, deepest blocked level and last failed leaf (H5).
+#include <cub/block/block_scan.cuh>
 #include "jsv_internal.cuh"
 #include "jsv_kernels.h"
 
