@@ -698,7 +698,9 @@ __global__ void __launch_bounds__(512) k_front_sort(const __grid_constant__ S1Ar
   const int F = a.fcnt[job];
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long base = job_base(a, probe, t);
-  if (F > FSORT_MAX || F == 0) {
+  // (rows of 16 coordinates: half the frontier fits the shared-memory keys)
+  constexpr int FMAX = D <= 12 ? FSORT_MAX : FSORT_MAX / 2;
+  if (F > FMAX || F == 0) {
     if (threadIdx.x == 0) a.fsorted[job] = 0;
     return;
   }
@@ -1092,9 +1094,10 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
   if (L.tiles_pp > 0) {
     const unsigned gb = (unsigned)std::max<long long>(1, std::min<long long>(L.max_items, L.grid));
     PROF_BEGIN(K_PAIRS_B);
-    if (a.D <= 8 && !getenv("JSV_NO_FSORT")) {
+    if (a.D <= 16 && !getenv("JSV_NO_FSORT")) {
+      const int fmax = a.D <= 12 ? FSORT_MAX : FSORT_MAX / 2;
       int F2 = 1;
-      while (F2 < FSORT_MAX) F2 <<= 1;
+      while (F2 < fmax) F2 <<= 1;
       const size_t fsm = (size_t)F2 * (a.D * sizeof(double) + sizeof(int));
 #define JSV_FS(DV)                                                                               \
   do {                                                                                           \
@@ -1105,7 +1108,9 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
         case 4: JSV_FS(4); break;
         case 5: JSV_FS(5); break;
         case 6: JSV_FS(6); break;
-        default: JSV_FS(8); break;
+        case 8: JSV_FS(8); break;
+        case 12: JSV_FS(12); break;
+        default: JSV_FS(16); break;
       }
 #undef JSV_FS
       ++launches;
