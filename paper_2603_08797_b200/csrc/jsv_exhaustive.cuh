@@ -1023,10 +1023,16 @@ __global__ void __launch_bounds__(XBLOCK) k_s2_xreduce(const __grid_constant__ X
 // per probe).  For a verdict "x >= v" that holds on an up-set of the sorted
 // values, x passes iff rank(x) >= #{failing values}; for a down-set ("t(x) <=
 // hi"), iff rank(x) < #{passing values}.
+// keys sorted side by side when their tables fit (one barrier per bitonic
+// stage for all three instead of three sorts in a row)
+#define XRANK_PAR_MAX 2048
+__device__ __host__ inline int x_rank_keys_per_pass(int n2) { return n2 <= XRANK_PAR_MAX ? 3 : 1; }
+
 __global__ void __launch_bounds__(512) k_x_rank(const __grid_constant__ XArgs a, int n2) {
   extern __shared__ __align__(16) unsigned char k_smem[];
-  double* v = reinterpret_cast<double*>(k_smem);
-  int* ix = reinterpret_cast<int*>(v + n2);
+  const int nk = x_rank_keys_per_pass(n2);
+  double* v = reinterpret_cast<double*>(k_smem);  // [nk][n2]
+  int* ix = reinterpret_cast<int*>(v + nk * n2);  // [nk][n2]
   const int probe = blockIdx.x;
   const XProbe& xp = a.xp[probe];
   if (xp.rounds == 0) return;  // not an exhaustive probe
@@ -1037,36 +1043,42 @@ __global__ void __launch_bounds__(512) k_x_rank(const __grid_constant__ XArgs a,
   const long long q = (long long)(probe * T + tl) * s.W;
   const long long o = (long long)probe * s.W;
   unsigned* rk = reinterpret_cast<unsigned*>(a.xrank + o);
-  for (int key = 0; key < 3; ++key) {
-    for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+  const int m = nk * n2;
+  for (int key0 = 0; key0 < 3; key0 += nk) {
+    for (int t = threadIdx.x; t < m; t += blockDim.x) {
+      const int key = key0 + t / n2, i = t % n2;
       double x = INFINITY;
       if (i < n) x = key == 0 ? s.p_cap[q + i] : key == 1 ? s.p_acc[q + i] : 2.0 * s.p_lat[q + i];
-      v[i] = x;
-      ix[i] = i;
+      v[t] = x;
+      ix[t] = i;
     }
     __syncthreads();
     for (int k = 2; k <= n2; k <<= 1) {
       for (int j = k >> 1; j > 0; j >>= 1) {
-        for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        for (int t = threadIdx.x; t < m; t += blockDim.x) {
+          const int i = t & (n2 - 1);  // (n2 is a power of two)
           const int l = i ^ j;
           if (l > i) {
+            const int tl2 = t - i + l;
             const bool up = (i & k) == 0;
-            const double x = v[i], y = v[l];
+            const double x = v[t], y = v[tl2];
             if ((x > y) == up) {
-              v[i] = y; v[l] = x;
-              const int t = ix[i]; ix[i] = ix[l]; ix[l] = t;
+              v[t] = y; v[tl2] = x;
+              const int tt = ix[t]; ix[t] = ix[tl2]; ix[tl2] = tt;
             }
           }
         }
         __syncthreads();
       }
     }
-    double* out = key == 0 ? a.scap : key == 1 ? a.sacc : a.slat2;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      out[o + i] = v[i];
-      const double x = v[i];
-      const int r = x_first(n, [&](int k) { return v[k] >= x; });  // #{values < x}
-      rk[4 * ix[i] + key] = (unsigned)r;
+    for (int t = threadIdx.x; t < nk * n; t += blockDim.x) {
+      const int kk = t / n, i = t % n, key = key0 + kk;
+      const double* vk = v + kk * n2;
+      double* out = key == 0 ? a.scap : key == 1 ? a.sacc : a.slat2;
+      const double x = vk[i];
+      out[o + i] = x;
+      const int r = x_first(n, [&](int k) { return vk[k] >= x; });  // #{values < x}
+      rk[4 * ix[kk * n2 + i] + key] = (unsigned)r;
     }
     __syncthreads();
   }
@@ -1150,9 +1162,8 @@ int launch_x_rank(const XArgs& a, cudaStream_t st) {
   if (!a.fast) return 0;
   int n2 = 1;
   while (n2 < a.max_pn_last) n2 <<= 1;
-  const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;
-  if (sm2 > 40 * 1024)
-    cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  const size_t sm2 = (sizeof(double) + sizeof(int)) * n2 * x_rank_keys_per_pass(n2);
+  cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
   PROF_BEGIN(K_S2_XSORT);
   k_x_rank<<<a.s.n_probes, 512, sm2, st>>>(a, n2);
   PROF_END();
@@ -1166,9 +1177,8 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
   if (a.fast && !rank_done) {
     int n2 = 1;
     while (n2 < a.max_pn_last) n2 <<= 1;
-    const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;
-    if (sm2 > 40 * 1024)
-      cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+    const size_t sm2 = (sizeof(double) + sizeof(int)) * n2 * x_rank_keys_per_pass(n2);
+    cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
     PROF_BEGIN(K_S2_XSORT);
     k_x_rank<<<a.s.n_probes, 512, sm2, st>>>(a, n2);
     PROF_END();
