@@ -12,6 +12,7 @@
 #include <memory>
 #include <string>
 #include <tuple>
+#include <unordered_map>
 #include <vector>
 #include <algorithm>
 
@@ -32,9 +33,20 @@ static bool timing_on() {
   static const bool on = getenv("JSV_TIMING") != nullptr;
   return on;
 }
-#define JSV_T(label)                                                              \
-  do {                                                                            \
-    if (timing_on()) fprintf(stderr, "[jsv t] %10.3f %s\n", host_ms(), label); \
+// (timestamps are buffered and printed when the batch ends, so the printing
+// does not stretch the gaps it measures)
+struct TMark { double t; const char* label; };
+static thread_local std::vector<TMark> g_tmarks;
+static void jsv_t(const char* label) {
+  g_tmarks.push_back({host_ms(), label});
+  if (strcmp(label, "finalize done") == 0 || g_tmarks.size() > 4096) {
+    for (const TMark& m : g_tmarks) fprintf(stderr, "[jsv t] %10.3f %s\n", m.t, m.label);
+    g_tmarks.clear();
+  }
+}
+#define JSV_T(label)                 \
+  do {                               \
+    if (timing_on()) jsv_t(label);   \
   } while (0)
 
 static int fail(int code, const std::string& msg) {
@@ -1481,19 +1493,23 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   // points, coinciding bisection brackets) get one Stage-1 computation.  The
   // batch is permuted so the distinct probes come first; outputs are permuted
   // back at the end.
+  JSV_T("batch entry");
   std::vector<DProbe> fp(n);
   for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i]);
+  JSV_T("probes filled");
   std::vector<int> perm;  // batch slot -> caller index
   std::vector<int> rep;   // batch slot -> slot whose Stage-1 pools it shares
   int n_s1 = n;
   {
-    std::map<std::string, int> seen;
+    std::unordered_map<std::string, int> seen;
+    seen.reserve(2 * (size_t)n);
+    const bool no_dedup = getenv("JSV_NO_S1DEDUP") != nullptr;
     std::vector<int> first, dups, dup_rep;
     for (int i = 0; i < n; ++i) {
       std::string key(reinterpret_cast<const char*>(fp[i].r_upper[0]), sizeof(double) * p.T);
       key.append(reinterpret_cast<const char*>(fp[i].r_upper[1]), sizeof(double) * p.T);
       auto it = seen.find(key);
-      if (it == seen.end() || getenv("JSV_NO_S1DEDUP")) {
+      if (it == seen.end() || no_dedup) {
         seen.emplace(key, (int)first.size());
         first.push_back(i);
       } else {
@@ -1508,8 +1524,12 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     for (int k = 0; k < n_s1; ++k) rep[k] = k;
     for (size_t k = 0; k < dups.size(); ++k) rep[n_s1 + k] = dup_rep[k];
   }
-  bs.probes.resize(n);
-  for (int k = 0; k < n; ++k) bs.probes[k] = fp[perm[k]];
+  if (n_s1 == n) {
+    bs.probes.swap(fp);  // (perm is the identity)
+  } else {
+    bs.probes.resize(n);
+    for (int k = 0; k < n; ++k) bs.probes[k] = fp[perm[k]];
+  }
   std::vector<jsv_plan_out> pout;
   jsv_plan_out* out_caller = out;
   if (n_s1 < n) {
