@@ -107,17 +107,19 @@ struct jsv_context {
   int shard_rank = 0, shard_world = 1;
   // pinned host staging for per-solve tables (one async copy instead of several
   // pageable ones); reused call to call -- every call synchronises before returning
-  void* hpin = nullptr;
-  size_t hpin_cap = 0;
-  void* pinned(size_t bytes) {
-    if (bytes > hpin_cap) {
-      if (hpin) cudaFreeHost(hpin);
-      hpin = nullptr;
-      hpin_cap = 0;
-      if (cudaHostAlloc(&hpin, bytes * 2, cudaHostAllocDefault) != cudaSuccess) return nullptr;
-      hpin_cap = bytes * 2;
+  // (slot 1: the exhaustive probes' records, in flight together with slot 0's
+  // chunk tables)
+  void* hpin[2] = {nullptr, nullptr};
+  size_t hpin_cap[2] = {0, 0};
+  void* pinned(size_t bytes, int slot = 0) {
+    if (bytes > hpin_cap[slot]) {
+      if (hpin[slot]) cudaFreeHost(hpin[slot]);
+      hpin[slot] = nullptr;
+      hpin_cap[slot] = 0;
+      if (cudaHostAlloc(&hpin[slot], bytes * 2, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+      hpin_cap[slot] = bytes * 2;
     }
-    return hpin;
+    return hpin[slot];
   }
 };
 
@@ -245,7 +247,8 @@ extern "C" void jsv_context_destroy(jsv_context* ctx) {
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
   if (ctx->st) cudaStreamDestroy(ctx->st);
-  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  for (void* h : ctx->hpin)
+    if (h) cudaFreeHost(h);
   delete ctx;
 }
 
@@ -1231,7 +1234,12 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
   JSV_T("exh: before xprobe copy");
   CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
-  CK(cudaMemcpyAsync(B[B_XPROBE].p, xp.data(), sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
+  {
+    void* h = c.pinned(sizeof(XProbe) * n, 1);
+    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    memcpy(h, xp.data(), sizeof(XProbe) * n);
+    CK(cudaMemcpyAsync(B[B_XPROBE].p, h, sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
+  }
   CK(B[B_ACTIVE].ensure(sizeof(int) * n));
   CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
   XArgs a;
