@@ -90,8 +90,12 @@ __global__ void k_generate(const __grid_constant__ S1Args a) {
   const bool in = gtid < (long long)a.n_probes * a.U;
   const int probe = in ? (int)(gtid / a.U) : 0;
   const int u = in ? (int)(gtid % a.U) : 0;
-  int d = 0;
-  while (d + 1 < a.n_desc && a.desc[d + 1].unit_off <= u) ++d;
+  // the last descriptor whose first unit is <= u (unit_off is non-decreasing):
+  // binary search instead of a scan of dependent loads
+  int d = 0, step = 1;
+  while (step * 2 < a.n_desc) step <<= 1;
+  for (; step > 0; step >>= 1)
+    if (d + step < a.n_desc && a.desc[d + step].unit_off <= u) d += step;
   const GenDesc D = a.desc[d];
   const int lu = u - D.unit_off;
   const DGraph& g = *a.g;
