@@ -57,13 +57,9 @@ NOMINAL_DEMAND = 480.0
 
 
 def xr_inputs():
-    from paper_2603_08797_b200.model import app_from_dict
-    from paper_2603_08797_b200.profiles import knobs_from_dict, synth_profile
+    from paper_2603_08797_b200 import workloads
 
-    with open(os.path.join(ROOT, "tests", "golden", "apps.json")) as fh:
-        doc = json.load(fh)["ar-assistant"]
-    app = app_from_dict(doc["app"])
-    return app, synth_profile(app.graph, knobs_from_dict(doc["knobs"]))
+    return workloads.xr()
 
 
 def demand_points(batch: int, rank: int, world: int) -> list[float]:

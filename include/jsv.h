@@ -13,6 +13,7 @@
  *   jsv_derive            <- derive_configuration() planner.py:243-315
  *                            + validate_configuration() planner.py:329-361
  *   jsv_validate          <- validate_configuration() on a caller-built Configuration
+ *   jsv_brute_force       <- brute_force_plan()    planner.py:1191-1272
  *   jsv_pool_dump         <- _Search.pools (Stage 1, _candidate_pool 586-635) for parity tests
  *   jsv_pack              <- placement.pack()      placement.py:163-216 (+ _exact_pack 219-266)
  *   jsv_min_gpus          <- placement.min_gpus()  placement.py:269-290
@@ -23,6 +24,11 @@
  * the planner entry points refuse to run without a CUDA device (there is no CPU
  * fallback).  The placement entry points (jsv_pack, jsv_min_gpus) are host
  * code: sequential bitmask tree walks over a plan's few MIG instances.
+ *
+ * Threading: a context serialises its calls (each entry point taking a
+ * jsv_context holds the context's mutex for the whole call), so several host
+ * threads may share one; contexts are independent of each other.  A problem
+ * belongs to the context it was created on.
  */
 #ifndef JSV_H
 #define JSV_H
@@ -214,6 +220,18 @@ int jsv_derive(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req
                const jsv_probe* probe, const int32_t* n_items, const uint32_t* items,
                jsv_plan_out* out);
 
+/* brute_force_plan() (planner.py:1191-1272) over the request space's profile keys:
+ * every instance-count map with counts 0..min(max_count, left / cost) and total
+ * slices <= budget, each derived + validated on the GPU; argmax (objective,
+ * -total_slices), ties on the smaller canonical m.  *assignments = number of maps
+ * (SolverStats.nodes); more than max_assignments -> JSV_ERR_CONFIG "oracle refuses:
+ * assignment cap exceeded".  *found = 0: no feasible map (out is then unused);
+ * else out = derive + validate of the winner.  The task/variant/segment/batch caps
+ * of OracleCaps are checked by the caller (planner.py:1205-1227). */
+int jsv_brute_force(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                    const jsv_probe* probe, int32_t max_count, int64_t max_assignments,
+                    int64_t* assignments, int32_t* found, jsv_plan_out* out);
+
 /* validate_configuration on caller-supplied derived fields (per task index). */
 int jsv_validate(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
                  const jsv_probe* probe, const double* latency, const double* capacity,
@@ -254,6 +272,12 @@ int jsv_set_strategy(jsv_context* ctx, int strategy, int64_t max_candidates);
  * replicated on every rank.
  */
 int jsv_set_shard(jsv_context* ctx, int rank, int world);
+
+/* jsv_plan_batch with shard (rank, world) for this call only (the context's
+ * own shard setting is untouched, so concurrent callers do not see it). */
+int jsv_plan_batch_shard(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                         int32_t n, const jsv_probe* probes, int32_t rank, int32_t world,
+                         jsv_plan_out* out);
 
 /* Per-kernel CUDA-event timing on the library stream (bench roofline).
  * jsv_profile(on) resets the accumulators; jsv_kernel_times fills ms[k] /

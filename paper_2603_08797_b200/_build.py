@@ -10,8 +10,10 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libjsv.so")
-SOURCES = ["jsv_api.cu", "jsv_stage1.cu", "jsv_stage2.cu", "jsv_place.cu"]
-HEADERS = ["jsv_internal.cuh", "jsv_kernels.h", "jsv_search.cuh", "jsv_exhaustive.cuh", "jsv_fanout.cuh", os.path.join("..", "..", "include", "jsv.h")]
+SOURCES = ["jsv_api.cu", "jsv_stage1.cu", "jsv_stage2.cu", "jsv_exh.cu", "jsv_fo.cu", "jsv_brute.cu", "jsv_place.cu"]
+HEADERS = ["jsv_internal.cuh", "jsv_kernels.h", "jsv_s2common.cuh", "jsv_search.cuh", "jsv_exhaustive.cuh",
+           "jsv_fanout.cuh", os.path.join("..", "..", "include", "jsv.h")]
+OBJDIR = os.path.join(HERE, "build")
 
 NVCC_FLAGS = [
     "-O3",
@@ -24,7 +26,6 @@ NVCC_FLAGS = [
     "-prec-sqrt=true",
     # ... and on the host side of the runtime
     "-Xcompiler", "-fPIC,-ffp-contract=off,-O2",
-    "-shared",
 ]
 
 
@@ -62,9 +63,28 @@ def build_decoder(verbose: bool = False) -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """One nvcc per translation unit (in parallel), then one shared-library link."""
     if not force and not _stale():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES]]
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs = [os.path.join(OBJDIR, s.replace(".cu", ".o")) for s in SOURCES]
+
+    def compile_one(src_obj):
+        src, obj = src_obj
+        cmd = [nvcc(), *NVCC_FLAGS, "-c", "-o", obj, os.path.join(CSRC, src)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        return subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        runs = list(ex.map(compile_one, zip(SOURCES, objs)))
+    for r in runs:
+        if r.stderr:
+            print(r.stderr, file=sys.stderr, end="")
+        r.check_returncode()
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB + ".tmp", *objs]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -102,6 +102,8 @@ EXPORTS = {
     "jsv_problem_destroy": (None, [C.c_void_p]),
     "jsv_plan_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.c_int32,
                                  C.POINTER(Probe), C.POINTER(PlanOut)]),
+    "jsv_plan_batch_shard": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.c_int32,
+                                       C.POINTER(Probe), C.c_int32, C.c_int32, C.POINTER(PlanOut)]),
     "jsv_max_demand_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.c_int32,
                                        C.POINTER(Probe), C.c_double, C.POINTER(DemandOut),
                                        C.POINTER(PlanOut)]),
@@ -110,6 +112,9 @@ EXPORTS = {
     "jsv_validate": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.POINTER(Probe),
                                _F64P, _F64P, _F64P, C.c_int32, C.c_double, C.c_uint32,
                                C.POINTER(PlanOut)]),
+    "jsv_brute_force": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.POINTER(Probe),
+                                  C.c_int32, C.c_int64, C.POINTER(C.c_int64), _I32P,
+                                  C.POINTER(PlanOut)]),
     "jsv_pool_dump": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.POINTER(Probe),
                                 C.c_int32, C.c_int32, _I32P, _I32P, _U32P, _F64P, _I32P]),
     "jsv_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <string>
 #include <tuple>
@@ -90,10 +91,14 @@ enum BufId {
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
-  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_ARRF, B_COUNT
+  B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_ARRF,
+  B_BFKEY, B_BFWAYS, B_BFPART, B_BFOUT, B_COUNT
 };
 
 struct jsv_context {
+  // one call at a time per context: entry points lock it (ctypes releases the GIL,
+  // and every call reuses the context's device scratch, pinned staging and stats)
+  std::recursive_mutex mu;
   int device = 0;
   cudaStream_t st = nullptr;
   cudaEvent_t ev[4] = {};
@@ -149,6 +154,7 @@ struct ProfScope {
 
 extern "C" int jsv_profile(jsv_context* ctx, int on) {
   if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   ctx->prof.on = on != 0;
   ctx->prof.st = ctx->st;
   for (int k = 0; k < K_COUNT_; ++k) {
@@ -160,6 +166,7 @@ extern "C" int jsv_profile(jsv_context* ctx, int on) {
 
 extern "C" int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count) {
   if (!ctx || !ms || !count) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   for (int k = 0; k < n && k < K_COUNT_; ++k) {
     ms[k] = ctx->kms[k];
     count[k] = ctx->kcnt[k];
@@ -256,6 +263,7 @@ extern "C" void jsv_context_destroy(jsv_context* ctx) {
 
 extern "C" int jsv_problem_create(jsv_context* ctx, const jsv_problem_desc* d, jsv_problem** out) {
   if (!ctx || !d || !out) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   const int T = d->n_tasks, E = d->n_edges, P = d->n_paths;
   if (T < 1 || T > MAXT) return fail(JSV_ERR_ARG, "task count outside [1, 16]");
   if (E < 0 || E > MAXE) return fail(JSV_ERR_ARG, "edge count outside [0, 32]");
@@ -1654,6 +1662,7 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
 extern "C" int jsv_plan_batch(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
                               int32_t n, const jsv_probe* probes, jsv_plan_out* out) {
   if (!ctx || !prob || !req || !probes || !out || n < 0) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   if (n == 0) return JSV_OK;
   CK(cudaSetDevice(ctx->device));
   memset(&ctx->stats, 0, sizeof(ctx->stats));
@@ -1661,8 +1670,24 @@ extern "C" int jsv_plan_batch(jsv_context* ctx, const jsv_problem* prob, const j
   return plan_batch_internal(*const_cast<jsv_problem*>(prob), *req, n, probes, out, true);
 }
 
+extern "C" int jsv_plan_batch_shard(jsv_context* ctx, const jsv_problem* prob,
+                                    const jsv_request* req, int32_t n, const jsv_probe* probes,
+                                    int32_t rank, int32_t world, jsv_plan_out* out) {
+  if (!ctx || !prob || !req || !probes || !out || n < 0) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+  if (world < 1 || rank < 0 || rank >= world) return fail(JSV_ERR_ARG, "bad shard rank/world");
+  const int r0 = ctx->shard_rank, w0 = ctx->shard_world;
+  ctx->shard_rank = rank;
+  ctx->shard_world = world;
+  const int rc = jsv_plan_batch(ctx, prob, req, n, probes, out);
+  ctx->shard_rank = r0;
+  ctx->shard_world = w0;
+  return rc;
+}
+
 extern "C" int jsv_set_strategy(jsv_context* ctx, int strategy, int64_t max_candidates) {
   if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   if (strategy < JSV_STRATEGY_SEARCH || strategy > JSV_STRATEGY_AUTO)
     return fail(JSV_ERR_ARG, "unknown strategy");
   if (max_candidates < 1) return fail(JSV_ERR_ARG, "max_candidates must be positive");
@@ -1673,6 +1698,7 @@ extern "C" int jsv_set_strategy(jsv_context* ctx, int strategy, int64_t max_cand
 
 extern "C" int jsv_set_shard(jsv_context* ctx, int rank, int world) {
   if (!ctx) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   if (world < 1 || rank < 0 || rank >= world) return fail(JSV_ERR_ARG, "bad shard rank/world");
   ctx->shard_rank = rank;
   ctx->shard_world = world;
@@ -1681,6 +1707,7 @@ extern "C" int jsv_set_shard(jsv_context* ctx, int rank, int world) {
 
 extern "C" int jsv_last_stats(jsv_context* ctx, jsv_stats* out) {
   if (!ctx || !out) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   *out = ctx->stats;
   return JSV_OK;
 }
@@ -1698,6 +1725,7 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
                                     const jsv_request* req, int32_t n, const jsv_probe* points,
                                     double rel_tol, jsv_demand_out* out, jsv_plan_out* plans) {
   if (!ctx || !prob || !req || !points || !out || n < 0) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   if (req->budget <= 0) return fail(JSV_ERR_CONFIG, "slice budget must be positive");
   if (n == 0) return JSV_OK;
   CK(cudaSetDevice(ctx->device));
@@ -1906,6 +1934,7 @@ extern "C" int jsv_derive(jsv_context* ctx, const jsv_problem* prob, const jsv_r
                           jsv_plan_out* out) {
   if (!ctx || !prob || !req || !probe || !n_items || !items || !out)
     return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   CK(cudaSetDevice(ctx->device));
   jsv_problem& p = *const_cast<jsv_problem*>(prob);
   auto& B = ctx->buf;
@@ -1938,12 +1967,124 @@ extern "C" int jsv_derive(jsv_context* ctx, const jsv_problem* prob, const jsv_r
   return JSV_OK;
 }
 
+// --------------------------------------------------------- brute_force_plan
+
+extern "C" int jsv_brute_force(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
+                               const jsv_probe* probe, int32_t max_count, int64_t max_assignments,
+                               int64_t* assignments, int32_t* found, jsv_plan_out* out) {
+  if (!ctx || !prob || !req || !probe || !assignments || !found || !out)
+    return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+  CK(cudaSetDevice(ctx->device));
+  jsv_problem& p = *const_cast<jsv_problem*>(prob);
+  // the request space's keys in the reference's sorted (task, variant, segment, batch)
+  // order: tasks by id rank, keys of a task in local key order (planner.py:1210-1227)
+  const int sub = ((req->space & JSV_SPACE_A) ? 2 : 0) + ((req->space & JSV_SPACE_S) ? 1 : 0);
+  std::vector<int> kt, kl, kc;
+  for (int t = 0; t < p.T; ++t) {
+    const int lo = p.sub_off[t * 4 + sub], hi = p.sub_off[t * 4 + sub + 1];
+    if (hi - lo > MAXI)
+      return fail(JSV_ERR_CONFIG, "oracle refuses: more than 16 profile keys for one task "
+                                  "(sm_100a brute_force_plan limit)");
+    for (int k = lo; k < hi; ++k) {
+      const int loc = p.sub_key[k];
+      kt.push_back(t);
+      kl.push_back(loc);
+      kc.push_back(p.key_cost[p.key_off[t] + loc]);
+      if (kc.back() < 1) return fail(JSV_ERR_ARG, "slice cost < 1");
+    }
+  }
+  const int K = (int)kt.size(), S = req->budget;
+  if (K > BF_MAXK)
+    return fail(JSV_ERR_CONFIG, "oracle refuses: more than 64 profile keys "
+                                "(sm_100a brute_force_plan limit)");
+  if (S < 0) return fail(JSV_ERR_ARG, "negative slice budget");
+  if (max_count < 0 || max_count > 0xFFFF) return fail(JSV_ERR_ARG, "max_count outside [0, 65535]");
+  // ways[i][left]: suffix counts, saturated above the assignment cap
+  const long long SAT = (long long)max_assignments + 1;
+  std::vector<long long> ways((size_t)(K + 1) * (S + 1), 1);
+  for (int i = K - 1; i >= 0; --i)
+    for (int left = 0; left <= S; ++left) {
+      long long n = 0;
+      const int cap = std::min<int>(max_count, left / kc[i]);
+      for (int c = 0; c <= cap && n < SAT; ++c) n += ways[(size_t)(i + 1) * (S + 1) + left - c * kc[i]];
+      ways[(size_t)i * (S + 1) + left] = std::min(n, SAT);
+    }
+  const long long total = ways[S];
+  *assignments = total;
+  if (total > max_assignments) return fail(JSV_ERR_CONFIG, "oracle refuses: assignment cap exceeded");
+  auto& B = ctx->buf;
+  cudaStream_t st = ctx->st;
+  DReq hreq;
+  fill_req(p, *req, hreq);
+  DProbe hp;
+  fill_probe(p, *req, *probe, hp);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+  const int blocks = (int)std::max(1LL, std::min<long long>((total + 255) / 256, (long long)sms * 8));
+  CK(B[B_REQ].ensure(sizeof(DReq)));
+  CK(B[B_PROBES].ensure(sizeof(DProbe)));
+  CK(B[B_BFKEY].ensure(sizeof(int) * 3 * (K + 1)));
+  CK(B[B_BFWAYS].ensure(sizeof(long long) * ways.size()));
+  CK(B[B_BFPART].ensure(sizeof(BruteBest) * blocks));
+  CK(B[B_BFOUT].ensure(64));
+  CK(B[B_DN].ensure(sizeof(int) * MAXT));
+  CK(B[B_DITEMS].ensure(sizeof(uint32_t) * MAXT * MAXI));
+  CK(B[B_OUT].ensure(sizeof(jsv_plan_out)));
+  std::vector<int> keys(3 * (K + 1), 0);
+  std::copy(kt.begin(), kt.end(), keys.begin());
+  std::copy(kl.begin(), kl.end(), keys.begin() + (K + 1));
+  std::copy(kc.begin(), kc.end(), keys.begin() + 2 * (K + 1));
+  CK(cudaMemcpyAsync(B[B_REQ].p, &hreq, sizeof(DReq), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_PROBES].p, &hp, sizeof(DProbe), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_BFKEY].p, keys.data(), sizeof(int) * keys.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_BFWAYS].p, ways.data(), sizeof(long long) * ways.size(),
+                     cudaMemcpyHostToDevice, st));
+  BruteArgs a{};
+  a.g = p.dgraph.as<DGraph>();
+  a.tb = p.dt;
+  a.rq = B[B_REQ].as<DReq>();
+  a.probe = B[B_PROBES].as<DProbe>();
+  a.K = K;
+  a.S = S;
+  a.maxc = max_count;
+  a.key_task = B[B_BFKEY].as<int>();
+  a.key_local = B[B_BFKEY].as<int>() + (K + 1);
+  a.key_cost = B[B_BFKEY].as<int>() + 2 * (K + 1);
+  a.ways = B[B_BFWAYS].as<long long>();
+  a.total = total;
+  a.part = B[B_BFPART].as<BruteBest>();
+  a.found = B[B_BFOUT].as<int>();
+  a.win = reinterpret_cast<long long*>(B[B_BFOUT].as<char>() + 8);
+  a.n_items = B[B_DN].as<int>();
+  a.items = B[B_DITEMS].as<uint32_t>();
+  int launches = launch_brute(a, blocks, st);
+  DeriveArgs d{};
+  d.g = a.g;
+  d.tb = p.dt;
+  d.rq = a.rq;
+  d.probe = a.probe;
+  d.n_items = a.n_items;
+  d.items = a.items;
+  d.out = B[B_OUT].as<jsv_plan_out>();
+  launches += launch_derive(d, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d.out, sizeof(jsv_plan_out), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(found, a.found, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  ctx->stats = jsv_stats{};
+  ctx->stats.leaves = total;
+  ctx->stats.kernel_launches = launches;
+  return JSV_OK;
+}
+
 extern "C" int jsv_validate(jsv_context* ctx, const jsv_problem* prob, const jsv_request* req,
                             const jsv_probe* probe, const double* latency, const double* capacity,
                             const double* demand, int32_t total_slices, double a_obj,
                             uint32_t uncovered_mask, jsv_plan_out* out) {
   if (!ctx || !prob || !req || !probe || !latency || !capacity || !demand || !out)
     return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   CK(cudaSetDevice(ctx->device));
   jsv_problem& p = *const_cast<jsv_problem*>(prob);
   auto& B = ctx->buf;
@@ -1987,6 +2128,7 @@ extern "C" int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const js
                              const jsv_probe* probe, int32_t task, int32_t cap, int32_t* n_out,
                              int32_t* n_items, uint32_t* items, double* stats, int32_t* truncated) {
   if (!ctx || !prob || !req || !probe || !n_out) return fail(JSV_ERR_ARG, "null argument");
+  std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
   CK(cudaSetDevice(ctx->device));
   jsv_problem& p = *const_cast<jsv_problem*>(prob);
   if (task < 0 || task >= p.T) return fail(JSV_ERR_ARG, "task index");

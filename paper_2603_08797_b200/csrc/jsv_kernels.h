@@ -342,3 +342,29 @@ struct ValidateArgs {
   jsv_plan_out* out;
 };
 int launch_validate(const ValidateArgs& a, cudaStream_t st);
+
+// brute_force_plan (jsv_brute.cu): ranked enumeration of instance-count maps
+#define BF_MAXK 64
+struct BruteBest {
+  int has, sl;
+  double obj;
+  long long idx;
+};
+struct BruteArgs {
+  const DGraph* g;
+  DTables tb;
+  const DReq* rq;
+  const DProbe* probe;
+  int K, S, maxc;
+  const int* key_task;    // [K] task index, ascending
+  const int* key_local;   // [K] local key index within the task
+  const int* key_cost;    // [K] slice cost
+  const long long* ways;  // [(K+1) x (S+1)] count suffixes of keys i.. within `left` slices
+  long long total;        // ways[0][S] = maps to evaluate
+  BruteBest* part;        // [blocks]
+  int* found;
+  long long* win;
+  int* n_items;           // [T]   winner, for k_derive
+  uint32_t* items;        // [T*MAXI]
+};
+int launch_brute(const BruteArgs& a, int blocks, cudaStream_t st);

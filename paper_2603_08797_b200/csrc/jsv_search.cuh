@@ -31,16 +31,6 @@ __device__ __forceinline__ double bits_obj(unsigned long long b) {
   return __longlong_as_double((long long)b);
 }
 
-__device__ __forceinline__ int find_probe(const long long* off, int n, long long x) {
-  int lo = 0, hi = n - 1;
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (off[mid] <= x) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
 // largest slot s in [lo, hi) with pfx[s] <= w
 __device__ __forceinline__ long long find_slot(const long long* pfx, long long lo, long long hi,
                                                long long w) {
@@ -269,38 +259,6 @@ __device__ inline int cmp_leaf(const S2Args& a, long long c1, long long c2) {
   }
   return 0;
 }
-
-// Cursor over the canonical m of one leaf: ((task, variant, segment, batch), count)
-// tuples in task-id order (planner.py:262), each encoded as task << 32 | key << 16 | count.
-struct MCursor {
-  const S2Args* a;
-  int probe;
-  const uint16_t* ch;  // choices by topo position
-  int u, k, n;
-  long long base;
-  __device__ void open_task() {
-    while (u < a->T) {
-      const int c = ch[a->g->pos_of[u]];
-      if (c != NONE16) {
-        const long long q = (long long)(probe * a->T + u) * a->W + c;
-        base = (long long)probe * a->C_probe + a->task_base[u] + a->pool_cand[q];
-        n = a->nitems[base];
-        if (n > 0) return;
-      }
-      ++u;
-    }
-  }
-  __device__ bool next(unsigned long long& e) {
-    if (u >= a->T) return false;
-    e = ((unsigned long long)u << 32) | a->items[base * a->maxi + k];
-    if (++k >= n) {
-      ++u;
-      k = 0;
-      open_task();
-    }
-    return true;
-  }
-};
 
 // m(leaf c1) vs m(leaf c2) as Python tuple comparison (planner.py:852)
 __device__ inline int cmp_tie(const S2Args& a, int probe, long long c1, long long c2) {

@@ -50,39 +50,9 @@ __global__ void k_s2_prep(const __grid_constant__ S2Args a, double* min_lat2, in
   B->leaves = 0;
 }
 
-__device__ __forceinline__ void pack16(unsigned long long* w, int k, unsigned v) {
-  w[k >> 2] |= (unsigned long long)(v & 0xFFFFu) << ((3 - (k & 3)) * 16);
-}
-
-
-__device__ inline void leaf_key(int T, const uint16_t* ch_topo, unsigned long long* w) {
-  w[0] = w[1] = w[2] = w[3] = 0ull;
-  for (int k = 0; k < T; ++k) pack16(w, k, ch_topo[k] == NONE16 ? 0u : ch_topo[k]);
-}
-
-__device__ inline void load_leaf(const S2Args& a, int probe, const uint16_t* ch_topo, double* lat,
-                                 double* cap, double* acc, int* sl, double* fan, uint32_t& present) {
-  const DGraph& g = *a.g;
-  present = 0;
-  for (int u = 0; u < a.T; ++u) {
-    const int c = ch_topo[g.pos_of[u]];
-    const int job = probe * a.T + u;
-    const int outd = g.succ_off[u + 1] - g.succ_off[u];
-    if (c == NONE16) {
-      lat[u] = 0.0; cap[u] = 0.0; acc[u] = 1.0; sl[u] = 0;
-      for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = 0.0;
-    } else {
-      const long long q = (long long)job * a.W + c;
-      lat[u] = a.p_lat[q]; cap[u] = a.p_cap[q]; acc[u] = a.p_acc[q]; sl[u] = a.p_sl[q];
-      for (int j = 0; j < outd; ++j) fan[g.succ_off[u] + j] = a.p_fan[q * a.maxout + j];
-      present |= 1u << u;
-    }
-  }
-}
+#include "jsv_s2common.cuh"
 
 #include "jsv_search.cuh"
-#include "jsv_exhaustive.cuh"
-#include "jsv_fanout.cuh"
 
 
 __device__ void write_config(const FinArgs& a, int probe, const uint16_t* cb_task,

@@ -60,6 +60,7 @@ __all__ = [
     "max_demand",
     "max_demand_grid",
     "OracleCaps",
+    "brute_force_plan",
     "plan_result_to_dict",
     "last_stats",
     "set_strategy",
@@ -369,9 +370,22 @@ def plan_batch(
     (and, through ``apps``, the SLO/objective scalars) may differ per probe.
     Results equal ``[plan(a, profile, r, options) for a, r in ...]``.
     """
-    options = options or PlannerOptions()
     if not requests:
         return []
+    t0 = time.perf_counter()
+    outs, lw, apps = solve_records(app, profile, requests, options, apps, device)
+    wall = (time.perf_counter() - t0) * 1000.0
+    return _results_from(outs, apps, lw, requests, wall)
+
+
+def solve_records(app, profile, requests: Sequence[PlanRequest], options=None, apps=None,
+                  device=None, shard: tuple[int, int] | None = None):
+    """plan_batch without the decode: (jsv_plan_out array, lowering, apps).
+
+    ``shard=(rank, world)`` sweeps only that block of every exhaustive
+    candidate space (jsv_plan_batch_shard; shard.plan_sharded combines).
+    """
+    options = options or PlannerOptions()
     same_app = apps is None
     apps = list(apps) if apps is not None else [app] * len(requests)
     r0 = requests[0]
@@ -387,7 +401,6 @@ def plan_batch(
                 or (r.factor_overrides is not r0.factor_overrides
                     and dict(r.factor_overrides or {}) != ov0)):
             raise ConfigError("plan_batch requests must share budget, space, slack and overrides")
-    t0 = time.perf_counter()
     lw, _ = _prepare(app, profile, r0, options, device)
     probes = (N.Probe * len(requests))()
     if same_app and r0.space.task_graph_informed:
@@ -407,10 +420,32 @@ def plan_batch(
             probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
     req, keep = LW.request_struct(lw, r0, options)
     outs = (N.PlanOut * len(requests))()
-    N.check(N.load_library().jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests),
-                                            probes, outs))
-    wall = (time.perf_counter() - t0) * 1000.0
-    return _results_from(outs, apps, lw, requests, wall)
+    lib = N.load_library()
+    if shard is None:
+        N.check(lib.jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests), probes, outs))
+    else:
+        N.check(lib.jsv_plan_batch_shard(lw.ctx, lw.handle, C.byref(req), len(requests), probes,
+                                         int(shard[0]), int(shard[1]), outs))
+    return outs, lw, apps
+
+
+def derive_record(app, profile, lw: LW.Lowered, request: PlanRequest, n_items, items) -> N.PlanOut:
+    """derive + validate of one assignment given as per-task packed items (jsv_derive)."""
+    ni = np.ascontiguousarray(n_items, dtype=np.int32)
+    it = np.ascontiguousarray(items, dtype=np.uint32)
+    req, keep = LW.request_struct(lw, request, PlannerOptions())
+    probe = LW.probe_struct(app, lw, float(request.demand_rps))
+    out = N.PlanOut()
+    N.check(N.load_library().jsv_derive(
+        lw.ctx, lw.handle, C.byref(req), C.byref(probe),
+        ni.ctypes.data_as(C.POINTER(C.c_int32)), it.ctypes.data_as(C.POINTER(C.c_uint32)),
+        C.byref(out)))
+    return out
+
+
+def decode_records(outs, app, lw: LW.Lowered, requests, wall_ms: float = 0.0) -> list[PlanResult]:
+    """jsv_plan_out records -> PlanResults (the decoder plan_batch uses)."""
+    return _results_from(outs, [app] * len(requests), lw, requests, wall_ms)
 
 
 def plan(
@@ -560,6 +595,42 @@ def validate_configuration(config: Configuration, app, profile, request: PlanReq
     vs.append(ConstraintVerdict("coverage", ",".join(bad), not bad,
                                 0.0 if not bad else -float(len(bad))))
     return tuple(vs)
+
+
+def brute_force_plan(app, profile, request: PlanRequest, caps: OracleCaps = OracleCaps()) -> PlanResult:
+    """Exhaustive solver for tiny instances, on the GPU (reference planner.py:1191-1272).
+
+    Every instance-count map over the request space's profile keys (counts up to
+    ``caps.max_count``, within the slice budget) is derived and validated by
+    ``jsv_brute_force``; the argmax uses plan()'s tie-break.  The caps and the
+    refusal messages are the reference's; the map count is ``stats.nodes``.
+    """
+    t0 = time.perf_counter()
+    graph = app.graph
+    if len(graph.task_ids) > caps.max_tasks:
+        raise ConfigError(f"oracle refuses: {len(graph.task_ids)} tasks > cap {caps.max_tasks}")
+    lw = _problem(app, profile)
+    sub = 2 * int(bool(request.space.accuracy_scaling)) + int(bool(request.space.spatial_partitioning))
+    for t in graph.task_ids:
+        ti = lw.index[t]
+        rows = [lw.keys[ti][k] for k in lw.sub_tuples[ti][sub]]
+        if (len({r[0] for r in rows}) > caps.max_variants or len({r[1] for r in rows}) > caps.max_segments
+                or len({r[2] for r in rows}) > caps.max_batches):
+            raise ConfigError(f"oracle refuses: task {t!r} exceeds variant/segment/batch caps")
+    req, keep = LW.request_struct(lw, request, PlannerOptions())
+    probe = LW.probe_struct(app, lw, float(request.demand_rps))
+    n = C.c_int64()
+    found = np.zeros(1, dtype=np.int32)
+    out = N.PlanOut()
+    N.check(N.load_library().jsv_brute_force(
+        lw.ctx, lw.handle, C.byref(req), C.byref(probe), int(caps.max_count),
+        int(caps.max_assignments), C.byref(n), found.ctypes.data_as(C.POINTER(C.c_int32)),
+        C.byref(out)))
+    stats = SolverStats(nodes=int(n.value), wall_ms=(time.perf_counter() - t0) * 1000.0)
+    if not found[0]:
+        return PlanResult(False, None, None, lw.a_max, None, (), stats)
+    cfg = _config_from(out, app, lw, request.demand_rps)
+    return PlanResult(True, cfg, cfg.objective, lw.a_max, None, _verdicts_from(out, app, lw), stats)
 
 
 def pool_dump(app, profile, request: PlanRequest, options: PlannerOptions | None = None,

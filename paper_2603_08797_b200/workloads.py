@@ -19,8 +19,9 @@ import os
 from .model import AppSpec, ModelVariant, Task, TaskGraph, app_from_dict
 from .profiles import SegmentType, SynthKnobs, knobs_from_dict, synth_profile
 
-_APPS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
-                     "apps.json")
+# the reference's three bundled apps and their generator knobs (reference
+# pkg/src/sliceserve/apps/*.json), shipped with the package
+_APPS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "bundled_apps.json")
 
 C3_LATENCY_SLOS_MS = (800.0, 1000.0, 1200.0, 1400.0, 1550.0, 1800.0, 2000.0, 2500.0)
 C3_ACCURACY_SLOS = (0.80, 0.825, 0.85, 0.875, 0.90, 0.925, 0.95, 0.975)

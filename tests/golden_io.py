@@ -3,6 +3,7 @@
 from __future__ import annotations
 
 import functools
+import gzip
 import json
 import os
 
@@ -15,7 +16,8 @@ GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 @functools.lru_cache(maxsize=None)
 def load(name: str):
-    with open(os.path.join(GOLDEN, name)) as fh:
+    path = os.path.join(GOLDEN, name)
+    with (gzip.open(path, "rt") if name.endswith(".gz") else open(path)) as fh:
         return json.load(fh)
 
 

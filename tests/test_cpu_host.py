@@ -165,6 +165,18 @@ def test_uninformed_statics_match_the_oracle():
 
 # ------------------------------------------------------------ multi-process
 
+def _record(feasible, obj, sl, items_per_task):
+    out = N.PlanOut()
+    out.feasible = out.has_config = int(feasible)
+    out.objective = obj
+    out.total_slices = sl
+    for t, items in enumerate(items_per_task):
+        out.n_items[t] = len(items)
+        for k, w in enumerate(items):
+            out.items[t][k] = w
+    return out
+
+
 def _gloo_worker(rank, world, port, q):
     import torch.distributed as dist
 
@@ -172,24 +184,20 @@ def _gloo_worker(rank, world, port, q):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    rng = random.Random(1234 + rank)
-    recs = [(1, round(rng.uniform(0.3, 0.5), 2), rng.randint(5, 9),
-             tuple(rng.randrange(1 << 64) for _ in range(4))) for _ in range(5)]
-    if rank == 1:
-        recs.append((0, 9.0, 0, (0, 0, 0, 0)))  # an infeasible shard never wins
-    local = recs[shard.combine_best(recs)]
-    gathered = shard.all_gather_best(local)
-    win = gathered[shard.combine_best(gathered)]
+    # rank 0: (0.5, 7 slices, m = ((0,k1,2),)); rank 1: same objective and slices,
+    # m = ((0,k1,1),(1,k0,1)) -> smaller m wins the tie (reference planner.py:850-854)
+    mine = [_record(1, 0.5, 7, [[(1 << 16) | 2], []]),
+            _record(1, 0.5, 7, [[(1 << 16) | 1], [1]])][rank]
+    gathered = shard.all_gather_records(shard.plan_record(mine, 2))
     items = list(range(11))
     mapped = shard.sharded_map(items, lambda xs: [x * x for x in xs])
-    q.put((rank, win, gathered, mapped))
+    q.put((rank, gathered, shard.pick_record(gathered, 2), shard.pick_record(gathered, 2, True),
+           mapped))
     dist.destroy_process_group()
 
 
-def test_gloo_two_rank_best_record_combine_and_sharded_map():
+def test_gloo_two_rank_record_combine_and_sharded_map():
     import torch.multiprocessing as mp
-
-    from paper_2603_08797_b200 import shard
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -201,13 +209,30 @@ def test_gloo_two_rank_best_record_combine_and_sharded_map():
     for p in procs:
         p.join(timeout=60)
     outs.sort()
-    (_, w0, g0, m0), (_, w1, g1, m1) = outs
-    assert w0 == w1 and g0 == g1
-    assert g0[shard.combine_best(g0)] == w0
+    (_, g0, w0, f0, m0), (_, g1, w1, f1, m1) = outs
+    assert g0 == g1 and len(g0) == 2 and len(g0[0]) == 3 + 2 * 17
+    assert w0 == w1 == 1          # the tie goes to the smaller m
+    assert f0 == f1 == 0          # feasible_only: the lowest feasible rank (first DFS leaf)
     assert m0 == m1 == [x * x for x in range(11)]
-    # round trip of the wire format keeps every bit
-    for rec in g0:
-        assert shard.unpack_record(shard.pack_record(rec)) == rec
+
+
+def test_pick_record_reference_tie_break():
+    from paper_2603_08797_b200 import shard
+
+    rec = lambda *a: shard.plan_record(_record(*a), 2)  # noqa: E731
+    infeasible = rec(0, 9.0, 1, [[(3 << 16) | 1], []])
+    a = rec(1, 0.4, 9, [[(1 << 16) | 1], [(2 << 16) | 1]])
+    b = rec(1, 0.4, 8, [[(1 << 16) | 1], [(2 << 16) | 3]])   # fewer slices wins
+    c = rec(1, 0.41, 12, [[(5 << 16) | 1], []])              # higher objective wins
+    pre = rec(1, 0.4, 8, [[(1 << 16) | 1], []])               # strict prefix of b's m
+    assert shard.pick_record([infeasible, infeasible], 2) is None
+    assert shard.pick_record([infeasible, a, b], 2) == 2
+    assert shard.pick_record([a, c, b], 2) == 1
+    assert shard.pick_record([b, pre], 2) == 1
+    assert shard.pick_record([infeasible, a, c], 2, feasible_only=True) == 1
+    # every bit of the objective survives the wire format
+    words = rec(1, -0.1234567890123, 3, [[7], [8]])
+    assert shard._record_key(words, 2)[0] == -0.1234567890123
 
 
 def test_block_range_partitions_exactly():
@@ -246,43 +271,53 @@ def test_workloads_c3_grid_matches_golden_slos():
         [(d["app"]["slo"]["latency_ms"], d["app"]["slo"]["accuracy_frac"]) for d in docs]
 
 
-def _fake_result(feasible, objective, slices, m):
-    from paper_2603_08797_b200.plan_types import Configuration, PlanResult, SolverStats
-
-    cfg = None
-    if feasible:
-        cfg = Configuration(m, 1.0, {}, {}, {}, {}, {}, {}, {}, {}, slices, 1.0, 1.0, objective, ())
-    return PlanResult(feasible, cfg, objective if feasible else None, 1.0,
-                      None if feasible else "throughput", (), SolverStats(0, 0.0))
-
-
 def _gloo_plan_sharded_worker(rank, world, port, q):
+    """plan_sharded's host pipeline on 4 gloo ranks with the GPU calls faked:
+    solve_records (the shard's jsv_plan_batch_shard), derive_record (jsv_derive of
+    the winner) and decode_records (the result decoder) are recorded, so the test
+    sees exactly which shard record every rank adopts."""
+    import types
+
     import torch.distributed as dist
 
-    from paper_2603_08797_b200 import _native as N
     from paper_2603_08797_b200 import planner, shard
+    from paper_2603_08797_b200.plan_types import PlannerOptions
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    # rank 0 and 2 tie on (objective, slices) and differ in m (rank 2's is smaller);
+    # rank 1 has fewer slices at a lower objective; rank 3's shard is infeasible
+    local = {0: _record(1, 0.5, 7, [[(4 << 16) | 2], []]),
+             1: _record(1, 0.4, 3, [[(0 << 16) | 1], []]),
+             2: _record(1, 0.5, 7, [[(1 << 16) | 2], []]),
+             3: _record(0, 0.0, 0, [[], []])}[rank]
+    local.pool_size[0] = 100 + rank
     seen = {}
-    # the GPU solve of one shard, faked per rank: rank 0 and 2 tie on (objective,
-    # slices) and differ in m; rank 1 has fewer slices at a lower objective;
-    # rank 3's shard is infeasible
-    local = {0: _fake_result(True, 0.5, 7, ((("t", "v1", "1g", 4), 2),)),
-             1: _fake_result(True, 0.4, 3, ((("t", "v0", "1g", 1), 1),)),
-             2: _fake_result(True, 0.5, 7, ((("t", "v0", "2g", 4), 2),)),
-             3: _fake_result(False, 0.0, 0, ())}[rank]
-    N.context = lambda device=None: "ctx"
-    N.set_shard = lambda ctx, r, w: seen.setdefault("shards", []).append((r, w))
-    planner.plan_batch = lambda app, prof, reqs, opt=None, device=None: [local]
+    lw = types.SimpleNamespace(ids=["a", "b"])
+
+    def solve_records(app, prof, reqs, opt=None, apps=None, device=None, shard=None):
+        seen["shard"] = shard
+        return [local], lw, None
+
+    def derive_record(app, prof, lw_, req, n_items, items):
+        seen["derived"] = (list(n_items[:2]), [list(items[0][:1]), list(items[1][:1])])
+        return _record(1, 0.5, 7, [[items[0][0]], []])
+
+    planner.solve_records = solve_records
+    planner.derive_record = derive_record
+    planner.decode_records = lambda outs, app, lw_, reqs, wall=0.0: [
+        (outs[0].objective, outs[0].total_slices, outs[0].items[0][0], outs[0].pool_size[0])]
     res = shard.plan_sharded(None, None, None)
-    q.put((rank, seen["shards"], res.objective, res.config.total_slices, res.config.m))
+    derived = seen.pop("derived", None)
+    res_first = shard.plan_sharded(None, None, None, PlannerOptions(feasible_only=True))
+    q.put((rank, seen["shard"], derived, res, res_first))
     dist.destroy_process_group()
 
 
 def test_gloo_four_rank_plan_sharded_combine():
-    """plan_sharded: each rank sweeps its shard, one all-gather, the reference
-    tie-break (objective, slices, m) on every rank; an infeasible shard never wins."""
+    """plan_sharded: each rank sweeps its shard, ONE all-gather of the fixed-size
+    records, the reference tie-break (objective, slices, m) on every rank, the
+    winner re-derived where it is not local; an infeasible shard never wins."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
@@ -294,10 +329,14 @@ def test_gloo_four_rank_plan_sharded_combine():
     outs = sorted(q.get(timeout=180) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    for rank, shards, obj, sl, m in outs:
-        assert shards == [(rank, 4), (0, 1)]  # set for the solve, reset afterwards
-        assert (obj, sl) == (0.5, 7)
-        assert m == ((("t", "v0", "2g", 4), 2),)  # the smaller m of the two ties
+    for rank, sh, derived, res, res_first in outs:
+        assert sh == (rank, 4)
+        # the winner is rank 2's record: objective 0.5, 7 slices, item (1 << 16) | 2;
+        # Stage-1 statistics (pool sizes) stay the local rank's
+        assert res == (0.5, 7, (1 << 16) | 2, 100 + rank)
+        assert (derived is None) == (rank == 2)
+        # feasible_only: the lowest feasible rank (0) holds the first DFS leaf
+        assert res_first[:3] == (0.5, 7, (4 << 16) | 2)
 
 
 def test_profile_csv_byte_identical_to_reference(tmp_path):

@@ -97,20 +97,83 @@ def test_bench_batch_strategies_agree_at_full_size():
 
 
 @pytest.mark.parametrize("env", [{"JSV_NO_FSORT": "1"}, {"JSV_PAIRS_TILED": "1"},
-                                 {"JSV_PAIRS_A1": "1"}, {"JSV_NO_RPL": "1"}, {"JSV_NO_TMA": "1"}])
+                                 {"JSV_PAIRS_A1": "1"}, {"JSV_NO_RPL": "1"}, {"JSV_NO_TMA": "1"},
+                                 {"JSV_NO_FAST": "1"}, {"JSV_NO_FAST": "1", "JSV_NO_RPL": "1"},
+                                 {"JSV_NO_FEAS_SWEEP": "1"}, {"JSV_NO_S1DEDUP": "1"}])
 def test_alternative_kernel_paths_match_reference(env, monkeypatch):
     """Every kernel variant the library can pick (frontier ranks by counting vs by
     sorting, tiled vs barrier-free skyline passes, register vs looped sweep, TMA
-    vs plain staging) reproduces the reference goldens."""
-    from paper_2603_08797_b200 import planner
+    vs plain staging, the float evaluator instead of the rank-space fast path --
+    the only path for profiles outside `lat_fast`) reproduces the reference
+    goldens, on bundled plans, the bench's demands and max_demand points."""
+    from paper_2603_08797_b200 import planner, workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
 
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     docs = load("plans_bundled.json")
     planner.set_strategy("exhaustive", EXH_LIMIT)
     try:
-        for doc in docs[::5]:
+        for doc in docs[::5] + load("plans_mixed.json")[::10]:
             app, table, req, opt = case_inputs(doc)
             assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]
+        app, table = workloads.xr()
+        rows = load("bench_xr64.json")["solves"][::4]
+        reqs = [PlanRequest(r["demand"], 28, SearchSpace(True, True, True)) for r in rows]
+        for r, res in zip(rows, planner.plan_batch(app, table, reqs)):
+            assert result_dict(res) == r["result"], r["demand"]
+        for doc in load("max_demand_c3.json")[::9]:
+            _check_md(planner, doc)
     finally:
         planner.set_strategy("auto")
+
+
+def _check_md(P, doc):
+    from paper_2603_08797_b200.model import app_from_dict
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    r = P.max_demand(app_from_dict(doc["app"]), profile_of(doc), doc["budget"],
+                     SearchSpace.from_label(doc["space"]), doc["slack"], None, doc["rel_tol"])
+    assert (r.demand_rps, r.probes) == (doc["demand"], doc["probes"]), doc["name"]
+    assert result_dict(r.plan) == doc["plan"], doc["name"]
+
+
+def test_bench_workload_matches_reference(P):
+    """The bench step itself: the 64 XR solves (240..712.5 rps) against the reference's
+    own results (tests/golden/bench_xr64.json), batched as bench.py runs them and one
+    at a time."""
+    import bench
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    gold = load("bench_xr64.json")
+    assert [r["demand"] for r in gold["solves"]] == bench.demand_points(64, 0, 1)
+    app, table = workloads.xr()
+    reqs = [PlanRequest(r["demand"], 28, SearchSpace(True, True, True)) for r in gold["solves"]]
+    got = P.plan_batch(app, table, reqs)
+    for r, res in zip(gold["solves"], got):
+        assert result_dict(res) == r["result"], r["demand"]
+    for r in gold["solves"][::16]:
+        res = P.plan(app, table, PlanRequest(r["demand"], 28, SearchSpace(True, True, True)))
+        assert result_dict(res) == r["result"], r["demand"]
+
+
+@pytest.mark.parametrize("doc", load("max_demand_840.json"), ids=_ids)
+def test_max_demand_840_slices_matches_reference(doc):
+    """configs[4](i): max_demand of traffic-analysis at 840 slices in all 8 spaces."""
+    from paper_2603_08797_b200 import planner
+
+    _check_md(planner, doc)
+
+
+def test_star_through_generic_strategies_matches_reference(monkeypatch):
+    """JSV_NO_FANOUT: the star ladder solved by the generic strategies instead of
+    the fan-out solver (3-5 tasks: the sizes they finish quickly)."""
+    from paper_2603_08797_b200 import planner
+
+    monkeypatch.setenv("JSV_NO_FANOUT", "1")
+    for doc in (load("plans_star.json") + load("plans_star_ladder.json")):
+        app, table, req, opt = case_inputs(doc)
+        if len(app.graph.task_ids) > 5:
+            continue
+        assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]

@@ -1,17 +1,30 @@
-"""One solve split across shards: every shard sweeps a
-disjoint block of the mixed-radix candidate space (jsv_set_shard) and the
-local results are combined with the reference tie-break (shard.pick_sharded).
-The shards run one after another on one GPU here -- the combine is exactly
-what plan_sharded does after its all-gather -- and the combined result must be
-the golden one for every shard count."""
+"""One solve split across shards.
+
+Every shard sweeps a disjoint block of the mixed-radix candidate space
+(jsv_plan_batch_shard) and the fixed-size local records are combined with the
+reference tie-break (shard.pick_record) and the winner re-derived
+(shard.combine_sharded) -- exactly what plan_sharded does after its one
+all-gather.  Here the shards run one after another on one GPU and the combine
+is applied as every rank would apply it; the result must be the golden one for
+every shard count and on every rank.  The last tests launch real
+multi-process runs (torchrun x2, both ranks on GPU 0 over gloo: the driver's
+boxes have one GPU) of plan_sharded and of the point-sharded sweep."""
 
 from __future__ import annotations
 
+import json
+import os
+import random
+import subprocess
+import sys
+
 import pytest
 
-from golden_io import all_plan_cases, case_inputs, result_dict
+from golden_io import all_plan_cases, case_inputs, load, result_dict
 
 pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 # T-informed solves (the uninformed planner has no Stage-2 search to shard)
 CASES = [d for d in all_plan_cases() if "T" in d["request"]["space"].split("+")]
@@ -19,26 +32,67 @@ CASES = [d for d in all_plan_cases() if "T" in d["request"]["space"].split("+")]
 
 @pytest.fixture(scope="module")
 def env():
-    from paper_2603_08797_b200 import _native as N
     from paper_2603_08797_b200 import planner, shard
 
     planner.set_strategy("exhaustive", 1 << 32)
-    yield planner, shard, N
-    N.set_shard(N.context(), 0, 1)
+    yield planner, shard
     planner.set_strategy("auto")
 
 
+def _sharded(planner, shard, app, table, req, opt, world):
+    outs = []
+    for r in range(world):
+        o, lw, _ = planner.solve_records(app, table, [req], opt, shard=(r, world))
+        outs.append(o[0])
+    records = [shard.plan_record(o, len(lw.ids)) for o in outs]
+    return [shard.combine_sharded(app, table, req, lw, outs[r], records, bool(opt.feasible_only))
+            for r in range(world)]
+
+
 @pytest.mark.parametrize("world", [2, 3, 8])
-@pytest.mark.parametrize("doc", CASES[::3], ids=lambda d: d["name"])
+@pytest.mark.parametrize("doc", CASES[::3] + [d for d in CASES if "feasible_only" in d["name"]],
+                         ids=lambda d: d["name"])
 def test_sharded_solve_matches_reference(env, doc, world):
-    planner, shard, N = env
+    planner, shard = env
     app, table, req, opt = case_inputs(doc)
-    ctx = N.context()
-    parts = []
-    try:
-        for r in range(world):
-            N.set_shard(ctx, r, world)
-            parts.append(planner.plan(app, table, req, opt))
-    finally:
-        N.set_shard(ctx, 0, 1)
-    assert result_dict(shard.pick_sharded(parts)) == doc["result"]
+    for res in _sharded(planner, shard, app, table, req, opt, world):
+        assert result_dict(res) == doc["result"]
+
+
+def test_sharded_bench_workload_every_rank_agrees(env):
+    """The bench's 64 XR solves (reference goldens, tests/golden/bench_xr64.json) split 4 ways."""
+    planner, shard = env
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlannerOptions, PlanRequest, SearchSpace
+
+    gold = load("bench_xr64.json")
+    app, table = workloads.xr()
+    for row in gold["solves"][::7]:
+        req = PlanRequest(row["demand"], 28, SearchSpace(True, True, True))
+        for res in _sharded(planner, shard, app, table, req, PlannerOptions(), 4):
+            assert result_dict(res) == row["result"], row["demand"]
+
+
+def _torchrun(args: list[str], timeout: int = 600) -> list[dict]:
+    port = 20000 + random.Random().randrange(20000)
+    env = dict(os.environ, JSV_BENCH_ONE_GPU="1", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.join(ROOT, "tests", "mp_shard_worker.py"), *args]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    return [json.loads(line) for line in p.stdout.splitlines() if line.startswith("{")]
+
+
+def test_torchrun_two_ranks_plan_sharded():
+    lines = _torchrun(["plan"])
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    for x in lines:
+        assert x["mismatches"] == [], x
+
+
+def test_torchrun_two_ranks_sharded_sweep():
+    lines = _torchrun(["sweep"])
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    for x in lines:
+        assert x["mismatches"] == [], x

@@ -1,8 +1,9 @@
 """configs[4] traces and the batched analytical day plan (paper_2603_08797_b200.workload)
-against tests/golden/day_traffic_840.json, written by the reference
-(tools/make_golden_day.py): the 288-bin trace, the predictor's demands, and
+against tests/golden/day_traffic_840_full.json.gz, written by the reference
+(tools/make_golden_full.py day): the 288-bin trace, the predictor's demands, and
 run_day's planning decisions (plan at the prediction, memoised max_demand
-fallback) for A+S+T and the three ablations."""
+fallback) for EVERY bin in A+S+T and the three ablations -- the 1,152 plans the
+bench's configs[4] extra times."""
 
 from __future__ import annotations
 
@@ -13,7 +14,7 @@ from golden_io import load, result_dict
 
 @pytest.fixture(scope="module")
 def gold():
-    return load("day_traffic_840.json")
+    return load("day_traffic_840_full.json.gz")
 
 
 def test_gen_trace_bit_identical(gold):
@@ -50,6 +51,7 @@ def test_plan_day_matches_reference(gold, space):
     app, table = workloads.traffic()
     tr = W.DemandTrace(tuple(enumerate(gold["demands"])))
     day = W.plan_day(app, table, tr, gold["budget"], SearchSpace.from_label(space), gold["slack"])
+    assert len(gold["plans"][space]) == len(day) == 288
     for row in gold["plans"][space]:
         d = day[row["bin"]]
         assert d.predicted_rps == gold["predicted"][row["bin"]]
