@@ -26,11 +26,25 @@ _SAVED: list[tuple[object, str, object]] = []
 _MODS: dict[str, ModuleType | None] = {}
 
 
+def _owned(ref_mod: ModuleType, name: str, val) -> bool:
+    """Is ``name`` the replaced module's own API (not a name it imported from a sibling)?"""
+    home = getattr(val, "__module__", None)
+    if isinstance(val, ModuleType):
+        return False
+    if home is not None and (callable(val) or isinstance(val, type)):
+        return home == ref_mod.__name__
+    return True  # constants (ALL_SPACES, DEFAULT_GEOMETRY, ...)
+
+
 def _rebind(ref_mod: ModuleType, new_mod: ModuleType) -> None:
+    public = set(getattr(new_mod, "__all__", ()))
     ref_ids = {}
     for name, val in vars(ref_mod).items():
-        if not name.startswith("__") and hasattr(new_mod, name):
-            ref_ids[id(val)] = (val, name)
+        if name.startswith("__") or not hasattr(new_mod, name) or not _owned(ref_mod, name, val):
+            continue
+        if not (callable(val) or isinstance(val, type)) and name not in public:
+            continue
+        ref_ids[id(val)] = (val, name)
     for mname, mod in list(sys.modules.items()):
         if mod is None or not (mname == "sliceserve" or mname.startswith("sliceserve.")):
             continue

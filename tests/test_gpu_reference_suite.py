@@ -35,7 +35,7 @@ FILES = ["test_planner.py", "test_model.py", "test_profiles.py", "test_placement
 def _run(files, timeout=3000, extra=()):
     if not os.path.isdir(os.path.join(REF, "sliceserve")) or not os.path.isdir(REF_TESTS):
         pytest.skip("baseline/_ref (the offline reference install) is not in this snapshot")
-    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), REF_TESTS]),
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([os.path.join(ROOT, "tests"), REF_TESTS, REF]),
                PYTHONDONTWRITEBYTECODE="1",
                PATH=os.path.join(REF, "bin") + os.pathsep + os.environ.get("PATH", ""))
     cmd = [sys.executable, "-m", "pytest", "-q", "-p", "ref_swap_plugin", "-p", "no:cacheprovider",
