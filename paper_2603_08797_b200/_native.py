@@ -89,7 +89,8 @@ class Stats(C.Structure):
                 ("candidates_generated", C.c_int64), ("leaves", C.c_int64), ("nodes", C.c_int64),
                 ("kernel_launches", C.c_int32), ("dims", C.c_int32), ("pair_tests_a", C.c_int64),
                 ("pair_tests_b", C.c_int64), ("leaf_work", C.c_int64),
-                ("exh_candidates", C.c_int64), ("exh_probes", C.c_int32), ("exh_pad_", C.c_int32)]
+                ("exh_candidates", C.c_int64), ("exh_probes", C.c_int32), ("exh_pad_", C.c_int32),
+                ("swept", C.c_int64), ("live_prefixes", C.c_int64)]
 
 
 EXPORTS = {
@@ -131,7 +132,7 @@ EXPORTS = {
 KERNEL_NAMES = ("generate", "stats", "pairs_a", "compact", "pairs_b", "truncate", "mrank",
                 "s2_prep", "s2_level", "s2_leaf", "s2_reduce", "finalize", "uninformed", "bucket",
                 "s2_prefix", "s2_exh", "s2_xreduce", "s2_xsort", "fo_prep", "fo_enum",
-                "fo_eval")
+                "fo_eval", "x_live")
 
 STRATEGY_SEARCH, STRATEGY_EXHAUSTIVE, STRATEGY_AUTO = 0, 1, 2
 STRATEGIES = {"search": STRATEGY_SEARCH, "exhaustive": STRATEGY_EXHAUSTIVE, "auto": STRATEGY_AUTO}

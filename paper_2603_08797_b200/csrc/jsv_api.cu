@@ -86,7 +86,7 @@ enum BufId {
   B_REQ, B_PROBES, B_DESC, B_WAYS, B_TILE_TASK, B_TILE_START, B_ITEMS, B_NITEMS, B_ARR, B_SL, B_FLAG,
   B_CNT, B_FRONT, B_FCNT, B_FPOS, B_FCR, B_SORTED, B_SCR, B_POOLC, B_POOLN, B_POOLT, B_PSL,
   B_PCAP, B_PACC, B_PLAT, B_PFAN, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
-  B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
+  B_XLIVE, B_MRANK, B_XRDONE, B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
@@ -101,6 +101,8 @@ struct jsv_context {
   std::recursive_mutex mu;
   int device = 0;
   cudaStream_t st = nullptr;
+  cudaStream_t st2 = nullptr;               // side stream for independent kernels of a call
+  cudaEvent_t fork = nullptr, join = nullptr;  // st -> st2 -> st ordering (no timing)
   cudaEvent_t ev[4] = {};
   DevBuf buf[B_COUNT];
   jsv_stats stats{};
@@ -243,6 +245,9 @@ extern "C" int jsv_context_create(int device, jsv_context** out) {
   auto* c = new jsv_context();
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
   *out = c;
   return JSV_OK;
@@ -253,6 +258,9 @@ extern "C" void jsv_context_destroy(jsv_context* ctx) {
   cudaSetDevice(ctx->device);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
+  if (ctx->fork) cudaEventDestroy(ctx->fork);
+  if (ctx->join) cudaEventDestroy(ctx->join);
+  if (ctx->st2) cudaStreamDestroy(ctx->st2);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   for (void* h : ctx->hpin)
     if (h) cudaFreeHost(h);
@@ -1148,7 +1156,7 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
     CK(cudaStreamSynchronize(st));
   }
   if (nodes)
-    for (int i = 0; i < n; ++i) out[i].nodes = (*nodes)[i];
+    for (int i = 0; i < n; ++i) out[i].nodes += (*nodes)[i];
   return JSV_OK;
 }
 
@@ -1218,25 +1226,27 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   }
   if (nx == 0) return JSV_OK;
   JSV_T("exh: probes planned");
-  // warp-rounds (x_slots(P) prefixes each) of every probe, concatenated
+  // every probe's prefix range, concatenated (k_x_live); live lists at the same offsets
   const int n_slots = x_slots(p.P);
-  std::vector<long long> roff(n + 1, 0), poff(2 * (n + 1), 0);
-  long long n_rounds = 0;
+  // k_x_live's work units: upper prefixes (all prefix digits but the fastest)
+  std::vector<long long> uoff(n + 1, 0);
+  long long n_pref = 0, n_upper = 0, max_rounds = 0;
   for (int i = 0; i < n; ++i) {
-    roff[i] = n_rounds;
-    if (xp[i].rounds) n_rounds += (xp[i].nq + n_slots - 1) / n_slots;
+    uoff[i] = n_upper;
+    xp[i].loff = n_pref;
+    if (xp[i].rounds && xp[i].nq > 0) {
+      n_pref += xp[i].nq;
+      max_rounds += (xp[i].nq + n_slots - 1) / n_slots;
+      const long long Rl = T >= 2 ? xp[i].radix[T - 2] : 1;
+      n_upper += (xp[i].q0 + xp[i].nq - 1) / Rl - xp[i].q0 / Rl + 1;
+    }
   }
-  roff[n] = n_rounds;
+  uoff[n] = n_upper;
   c.stats.exh_candidates += cand;
   c.stats.exh_probes += nx;
-  // register records need whole-warp prefix groups (every sink pool >= 32) and <= 512 bundles;
-  // each probe sweeps ceil(pool / 32) records per lane
+  // register records: <= 512 bundles per sink pool (ceil(pool / 32) records per lane)
   int reg = 0;
-  if (p.P <= 4 && max_pn_last <= 512 && bs.s1.S < 0x7FFF) {
-    reg = 1;
-    for (int i = 0; i < n; ++i)
-      if (xp[i].rounds > 0 && xp[i].glog < 5) reg = 0;
-  }
+  if (p.P <= 4 && max_pn_last <= 512 && bs.s1.S < 0x7FFF) reg = 1;
   if (getenv("JSV_NO_RPL")) reg = 0;
   for (int i = 0; i < n; ++i)
     if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
@@ -1281,90 +1291,58 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
     a.slat2 = B[B_XSLAT].as<double>();
     a.xrank = B[B_XRANK].as<uint4>();
   }
-  if (getenv("JSV_NO_FAST")) a.fast = 0;
-  if (getenv("JSV_NO_TMA")) a.tma = 0;
-  // the sink-pool rank tables only need the probes: sort them while the host
-  // plans the chunk schedule
-  c.stats.kernel_launches += launch_x_rank(a, st);
-  JSV_T("exh: before chunk plan");
-  // persistent blocks take chunks -- contiguous warp-round ranges of the
-  // concatenation -- from a counter; chunk sizes are guided (a fraction of the
-  // remaining modelled cost: prefix derivation + a sweep proportional to the sink
-  // pool), large first and small last, so the blocks finish together.  The
-  // segment of probe i inside chunk o reduces into part slot o + i (unique:
-  // chunks' probe ranges are ordered); probe i folds slots [poff[i], poff[n + 1 + i])
-  const size_t smem = x_smem_bytes(max_pn_last, p.P, a.fast != 0);
-  const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
-  std::vector<double> wr(n, 0.0), iwr(n, 0.0), wc(n + 1, 0.0);
-  for (int i = 0; i < n; ++i) {
-    const int pn = xp[i].pn[T - 1];
-    wr[i] = a.rpl ? 1000.0 + 112.0 * ((pn + 31) / 32) : 1000.0 + 4.0 * pn;
-    iwr[i] = 1.0 / wr[i];
-    wc[i + 1] = wc[i] + wr[i] * (double)(roff[i + 1] - roff[i]);
-  }
-  std::vector<long long> cstart(1, 0);
-  cstart.reserve(4096);
-  const double inv2g = 1.0 / (2.0 * (double)G);
-  {
-    const long long min_rounds = 4 * (XBLOCK / 32);
-    long long r = 0;
-    int pi = 0;
-    while (r < n_rounds) {
-      while (pi < n - 1 && roff[pi + 1] <= r) ++pi;
-      const double done = wc[pi] + wr[pi] * (double)(r - roff[pi]);
-      const double target = std::max(0.0, (wc[n] - done) * inv2g);
-      // advance by `target` cost from round r
-      long long e = r;
-      double left = target;
-      int pj = pi;
-      while (e < n_rounds && left > 0) {
-        while (pj < n - 1 && roff[pj + 1] <= e) ++pj;
-        const long long avail = roff[pj + 1] - e;
-        const long long take = std::min<long long>(avail, (long long)std::ceil(left * iwr[pj]));
-        e += take;
-        left -= (double)take * wr[pj];
-      }
-      e = std::min(n_rounds, std::max(e, r + min_rounds));
-      cstart.push_back(e);
-      r = e;
+  a.prune = getenv("JSV_NO_PRUNE") ? 0 : 1;
+  if (a.mode == LEAF_FULL) {
+    // m tie-breaks: packed keys when T <= 5 and every pool's lists fit k_m_rank's
+    // shared memory (ranks of 2 n + 2 <= 2048 sequences fit 11 bits), else ranks
+    int max_pool = 0;
+    for (int i = 0; i < n; ++i)
+      if (xp[i].rounds)
+        for (int k = 0; k < T; ++k) max_pool = std::max(max_pool, xp[i].pn[k]);
+    a.mkey = (T <= 5 && max_pool <= 1023 && (long long)max_pool * bs.s1.maxi <= 4096 &&
+              !getenv("JSV_NO_MKEY")) ? 1 : 0;
+    if (a.mkey) {
+      CK(B[B_MRANK].ensure(sizeof(uint32_t) * ((size_t)n * T * W + (size_t)n * T)));
+      a.s.mkey = B[B_MRANK].as<uint32_t>();
+      a.s.mnone = B[B_MRANK].as<uint32_t>() + (size_t)n * T * W;
+    } else {
+      CK(B[B_MRANK].ensure(sizeof(uint32_t) * (size_t)n * T * W));
+      a.s.mrank = B[B_MRANK].as<uint32_t>();
     }
   }
-  const long long n_chunks = (long long)cstart.size() - 1;
-  if (timing_on()) fprintf(stderr, "[jsv t] exh: %lld chunks over %lld rounds, grid %lld\n", n_chunks, n_rounds, G);
-  JSV_T("exh: chunks planned");
-  for (int i = 0; i < n; ++i) {
-    const long long r0 = roff[i], r1 = roff[i + 1];
-    if (r0 == r1) continue;
-    // chunks containing rounds r0 and r1 - 1: the last o with cstart[o] <= r
-    const long long o_lo = (long long)(std::upper_bound(cstart.begin(), cstart.end() - 1, r0) - cstart.begin()) - 1;
-    const long long o_hi = (long long)(std::upper_bound(cstart.begin(), cstart.end() - 1, r1 - 1) - cstart.begin()) - 1;
-    poff[i] = o_lo + i;
-    poff[n + 1 + i] = o_hi + i + 1;
-  }
-  CK(B[B_XBOFF].ensure(sizeof(long long) * (3 * (n + 1) + n_chunks + 2)));
-  CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)(n_chunks + n)));
+  if (getenv("JSV_NO_FAST")) a.fast = 0;
+  if (getenv("JSV_NO_TMA")) a.tma = 0;
+  // live lists + their round offsets are built on the device; persistent blocks take
+  // fixed chunks of X_CHUNK rounds; the segment of probe i inside chunk o reduces
+  // into part slot o + i
+  const size_t smem = x_smem_bytes(max_pn_last, p.P, a.fast != 0);
+  const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
+  CK(B[B_XLIVE].ensure(sizeof(unsigned) * (size_t)std::max<long long>(1, n_pref)));
+  CK(B[B_XBOFF].ensure(sizeof(long long) * (2 * (size_t)(n + 1) + 1) + sizeof(int) * (size_t)n));
+  CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)std::max<long long>(1, max_rounds)));
   {
-    // part-slot ranges, round offsets, chunk starts and the zeroed chunk counter:
-    // one copy from pinned staging
-    const size_t words = 3 * (size_t)(n + 1) + (size_t)n_chunks + 2;
-    long long* h = static_cast<long long*>(c.pinned(sizeof(long long) * words));
+    // upper-prefix offsets (pinned upload); round offsets, round counter, live counts zeroed
+    long long* h = static_cast<long long*>(c.pinned(sizeof(long long) * (n + 1)));
     if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
-    memcpy(h, poff.data(), sizeof(long long) * 2 * (n + 1));
-    memcpy(h + 2 * (n + 1), roff.data(), sizeof(long long) * (n + 1));
-    memcpy(h + 3 * (n + 1), cstart.data(), sizeof(long long) * (n_chunks + 1));
-    h[words - 1] = 0;
-    CK(cudaMemcpyAsync(B[B_XBOFF].p, h, sizeof(long long) * words, cudaMemcpyHostToDevice, st));
+    memcpy(h, uoff.data(), sizeof(long long) * (n + 1));
+    CK(cudaMemcpyAsync(B[B_XBOFF].p, h, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(B[B_XBOFF].as<long long>() + (n + 1), 0,
+                       sizeof(long long) * (n + 2) + sizeof(int) * n, st));
   }
-  a.boff = B[B_XBOFF].as<long long>();
-  a.roff = B[B_XBOFF].as<long long>() + 2 * (n + 1);
-  a.cstart = B[B_XBOFF].as<long long>() + 3 * (n + 1);
-  a.n_chunks = n_chunks;
-  a.work = reinterpret_cast<unsigned long long*>(B[B_XBOFF].as<long long>() + 3 * (n + 1) +
-                                                 n_chunks + 1);
-  const long long grid = std::min(G, n_chunks);
+  a.uoff = B[B_XBOFF].as<long long>();
+  a.roff = B[B_XBOFF].as<long long>() + (n + 1);
+  a.roff_w = B[B_XBOFF].as<long long>() + (n + 1);
+  a.work = reinterpret_cast<unsigned long long*>(B[B_XBOFF].as<long long>() + 2 * (n + 1));
+  a.live_cnt = reinterpret_cast<int*>(B[B_XBOFF].as<long long>() + 2 * (n + 1) + 1);
+  a.live = B[B_XLIVE].as<unsigned>();
+  CK(B[B_XRDONE].ensure(sizeof(int) * (size_t)n));
+  a.xr_done = B[B_XRDONE].as<int>();
+  const long long grid = std::min(G, std::max<long long>(1, (max_rounds + 7) / 8));
   a.part = B[B_XPART].as<XPart>();
   JSV_T("exh: before launch");
-  c.stats.kernel_launches += launch_stage2_exhaustive(a, grid, p.P, smem, st, true);
+  c.stats.kernel_launches +=
+      launch_stage2_exhaustive(a, grid, p.P, smem, st, getenv("JSV_NO_SIDE") ? st : c.st2, c.fork,
+                               c.join, n_upper);
   CK(cudaGetLastError());
   bool any_trunc = false;
   for (int i = 0; i < n; ++i) any_trunc = any_trunc || truncated[i];
@@ -1598,6 +1576,8 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
         any = true;
       }
       c.stats.leaves += (long long)best[i].leaves;
+      c.stats.swept += (long long)best[i].nodes;
+      c.stats.live_prefixes += (long long)best[i].live;
     }
     if (any) {
       rc = run_stage2(p, bs, true, want_config, redo, nullptr);

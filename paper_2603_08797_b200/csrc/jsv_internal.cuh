@@ -114,6 +114,7 @@ struct BestRec {
   int deepest;      // deepest blocked level (-1)
   int kills[MAXT][5];
   unsigned long long nodes, leaves;
+  unsigned long long live;  // exhaustive: prefixes derived in full and swept (k_x_live's list)
 };
 
 __device__ __forceinline__ double d_max(double a, double b) {

@@ -6,7 +6,7 @@
 // Per-kernel CUDA-event timing on the launching stream (bench.py roofline).
 enum KernelId {
   K_GENERATE, K_STATS, K_PAIRS_A, K_COMPACT, K_PAIRS_B, K_TRUNCATE, K_MRANK, K_S2_PREP,
-  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_S2_EXH, K_S2_XREDUCE, K_S2_XSORT, K_FO_PREP, K_FO_ENUM, K_FO_EVAL, K_COUNT_
+  K_S2_LEVEL, K_S2_LEAF, K_S2_REDUCE, K_FINALIZE, K_UNINFORMED, K_BUCKET, K_S2_PREFIX, K_S2_EXH, K_S2_XREDUCE, K_S2_XSORT, K_FO_PREP, K_FO_ENUM, K_FO_EVAL, K_X_LIVE, K_COUNT_
 };
 
 struct Prof {
@@ -15,7 +15,11 @@ struct Prof {
   std::vector<cudaEvent_t> ev;
   std::vector<int> ids;
   size_t used = 0;
-  void begin(int id) {
+  void begin(int id) { begin_on(id, st); }
+  void end() { end_on(st); }
+  // events on the kernel's own stream (kernels of a side stream overlap the main one:
+  // their times are their own, not a share of a serial step)
+  void begin_on(int id, cudaStream_t s) {
     if (!on) return;
     if (used + 2 > ev.size()) {
       for (int i = 0; i < 64; ++i) {
@@ -26,11 +30,11 @@ struct Prof {
     }
     ids.resize(ev.size() / 2 + 1);
     ids[used / 2] = id;
-    cudaEventRecord(ev[used], st);
+    cudaEventRecord(ev[used], s);
   }
-  void end() {
+  void end_on(cudaStream_t s) {
     if (!on) return;
-    cudaEventRecord(ev[used + 1], st);
+    cudaEventRecord(ev[used + 1], s);
     used += 2;
   }
 };
@@ -43,6 +47,14 @@ extern thread_local Prof* g_prof;
 #define PROF_END()     \
   do {                 \
     if (g_prof) g_prof->end(); \
+  } while (0)
+#define PROF_BEGIN_ON(id, s) \
+  do {                       \
+    if (g_prof) g_prof->begin_on(id, s); \
+  } while (0)
+#define PROF_END_ON(s)       \
+  do {                       \
+    if (g_prof) g_prof->end_on(s); \
   } while (0)
 
 struct S1Args {
@@ -131,6 +143,15 @@ struct S2Args {
   long long C_probe;
   long long task_base[MAXT + 1];
   int maxi;
+  // m order of the pool bundles (k_m_rank; exhaustive full plans): [job * W + k] =
+  // rank | ext << 16 | empty << 31 -- rank = #bundles of the pool with a smaller item
+  // list, ext = rank + #bundles having this list as a proper prefix
+  const uint32_t* mrank;
+  // packed m keys (XArgs::mkey): [job * W + k] = key0 | key1 << 16 -- the rank of the
+  // bundle's item list among every list and every list followed by a later task's
+  // entry (key1: that continuation); mnone[job]: the same for "no instances"
+  const uint32_t* mkey;
+  const uint32_t* mnone;
   const double* min_lat2;  // [jobs] (0 for could_zero tasks, set by stage2 prep)
   const int* min_sl;
   const double* acc_ub;
@@ -193,6 +214,8 @@ struct XPart {
   double obj;
   long long idx;
   unsigned long long leaves;
+  unsigned long long swept;  // candidates the register sweep compared (live prefixes x pool)
+  unsigned long long mk;     // packed m key of the best (XArgs::mkey)
 };
 
 // per-probe decomposition (host-computed after Stage 1)
@@ -200,6 +223,7 @@ struct XProbe {
   int radix[MAXT];      // digit radix by topo position (pool_n + could_zero)
   int pn[MAXT];         // pool size by topo position ("no instances" digit value)
   long long q0, nq;     // prefix range of this shard
+  long long loff;       // first slot of this probe's live list (prefix sum of nq)
   int glog;             // lanes per prefix group = 1 << glog
   int R;                // radix of the last position
   int rounds;           // 1: exhaustive probe (0: not swept)
@@ -228,7 +252,18 @@ struct XArgs {
   int max_pn_last;        // largest sink pool of the batch
   int rpl;                // rank space: 1 = sink records kept in registers (XProbe::rpl per
                           // lane), 0 = loop over the shared-memory records
+  int prune;              // prefixes failing a prefix task's throughput verdict are decided
+                          // by k_x_live without the full derivation or a sweep
+  const long long* uoff;  // [n_probes + 1] first upper prefix of each probe (k_x_live's
+                          // work units: every prefix digit but the fastest)
+  unsigned* live;         // live prefixes (local index - q0) of probe i at [xp[i].loff, ...)
+  int* live_cnt;          // [n_probes] live prefixes per probe
+  long long* roff_w;      // = roff, written by k_x_sched
+  int mkey;               // full plans, T <= 5: m tie-breaks compare packed 55-bit keys
+  int* xr_done;           // [n_probes] column blocks of k_x_rank finished
 };
+// rounds per chunk of the exhaustive kernel's persistent blocks
+#define X_CHUNK 8
 
 // prefix-state slots per warp of the exhaustive kernel for a graph with P paths
 __host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <= 16 ? 8 : 2); }
@@ -237,8 +272,9 @@ __host__ __device__ constexpr int x_pad(int n) { return ((n > 0 ? n : 1) + 127) 
 size_t x_smem_bytes(int max_pn_last, int P, bool rank);
 long long x_resident_blocks(const XArgs& a, int P, size_t smem);
 int launch_x_rank(const XArgs& a, cudaStream_t st);
-int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
-                             cudaStream_t st, bool rank_done = false);
+int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem, cudaStream_t st,
+                             cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join,
+                             long long n_upper);
 
 // fan-out graphs (jsv_fanout.cuh)
 #define FO_DELTA_W 1e-9   // slack on real-valued accuracy sums (>> float error)

@@ -48,6 +48,7 @@ __global__ void k_s2_prep(const __grid_constant__ S2Args a, double* min_lat2, in
     for (int k = 0; k < 5; ++k) B->kills[i][k] = 0;
   B->nodes = 0;
   B->leaves = 0;
+  B->live = 0;
 }
 
 #include "jsv_s2common.cuh"
@@ -136,7 +137,7 @@ __global__ void k_finalize(const __grid_constant__ FinArgs a) {
     o.pool_present[t] = 1;
   }
   const BestRec& B = a.best[probe];
-  o.nodes = 0;
+  o.nodes = (long long)B.nodes;
   o.leaves = (long long)B.leaves;
   if (a.uninformed) {
     uint16_t cb[MAXT];

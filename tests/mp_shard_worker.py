@@ -64,8 +64,11 @@ def main() -> None:
                     result_dict(r.plan) != doc["plan"]:
                 bad.append(doc["name"])
         n = len(grid)
-    print(json.dumps({"rank": rank, "world": dist.get_world_size(), "mode": mode, "cases": n,
-                      "mismatches": bad}), flush=True)
+    # one write() per line: the ranks share the pipe, and a single write of < PIPE_BUF
+    # bytes is not interleaved with the other rank's (print() may split text and newline)
+    line = json.dumps({"rank": rank, "world": dist.get_world_size(), "mode": mode, "cases": n,
+                       "mismatches": bad}) + "\n"
+    os.write(1, line.encode())
     dist.destroy_process_group()
 
 
