@@ -86,7 +86,7 @@ enum BufId {
   B_REQ, B_PROBES, B_DESC, B_WAYS, B_TILE_TASK, B_TILE_START, B_ITEMS, B_NITEMS, B_ARR, B_SL, B_FLAG,
   B_CNT, B_FRONT, B_FCNT, B_FPOS, B_FCR, B_SORTED, B_SCR, B_POOLC, B_POOLN, B_POOLT, B_PSL,
   B_PCAP, B_PACC, B_PLAT, B_PFAN, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
-  B_XLIVE, B_MRANK, B_XRDONE, B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
+  B_XLIVE, B_MRANK, B_XRDONE, B_STAMPS, B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
@@ -852,7 +852,52 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   L.jchunks_a = (int)std::max<long long>(1, (pl.max_cap + L.jchunk_a - 1) / L.jchunk_a);
   L.jchunk_b = 1024;
   L.jchunks_b = L.jchunks_a;
-  c.stats.kernel_launches += launch_stage1(a, L, st);
+  // fused Stage 1 (one block per job) unless rows are wider than 16 coordinates or
+  // the budget's bucket tables are too large for shared memory
+  {
+    for (int t = 0, d = 0; t <= T; ++t) {
+      while (d < (int)pl.desc.size() && pl.desc[d].task < t) ++d;
+      a.desc_t0[t] = d;
+    }
+  }
+  const int NB = rq.budget + 2;
+  const bool fused = D <= 16 && NB <= 4096 && !getenv("JSV_S1_LEGACY");
+  if (fused) {
+    const size_t smax = 100 * 1024;  // two blocks per SM (with the static shared memory)
+    long long cap = pl.max_cap;
+    if (s1_fused_smem(D, NB, (int)std::min<long long>(cap, 1 << 20)) > smax) {
+      const size_t fixed = ((size_t)2 * NB * sizeof(int) + 15) & ~(size_t)15;
+      cap = (long long)((smax - fixed - 64) / (5 * sizeof(int) + sizeof(float4) + 1));
+    }
+    a.fused_cap = (int)std::max<long long>(0, cap);
+    const size_t smem = s1_fused_smem(D, NB, a.fused_cap);
+    const bool phases = getenv("JSV_S1_PHASES") != nullptr;
+    if (phases) {
+      CK(B[B_STAMPS].ensure(sizeof(unsigned long long) * 10 * (size_t)n_s1 * T));
+      a.stamps = B[B_STAMPS].as<unsigned long long>();
+    }
+    c.stats.kernel_launches += launch_stage1_fused(a, smem, st);
+    if (phases) {
+      // mean phase durations over the jobs (diagnostics on stderr)
+      std::vector<unsigned long long> h(10 * (size_t)n_s1 * T);
+      CK(cudaMemcpyAsync(h.data(), a.stamps, sizeof(unsigned long long) * h.size(),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      double acc[9] = {0};
+      unsigned long long t0 = ~0ull, t1 = 0;
+      for (size_t j = 0; j < (size_t)n_s1 * T; ++j) {
+        for (int k = 0; k < 8; ++k) acc[k] += (double)(h[j * 10 + k + 1] - h[j * 10 + k]);
+        t0 = std::min(t0, h[j * 10]);
+        t1 = std::max(t1, h[j * 10 + 8]);
+      }
+      fprintf(stderr, "[jsv s1] jobs %d span %.1f us; mean us per phase:", n_s1 * T, (t1 - t0) / 1e3);
+      for (int k = 0; k < 8; ++k) fprintf(stderr, " %.1f", acc[k] / (n_s1 * T) / 1e3);
+      fprintf(stderr, "\n");
+      a.stamps = nullptr;
+    }
+  } else {
+    c.stats.kernel_launches += launch_stage1(a, L, st);
+  }
   CK(cudaGetLastError());
   if (n_s1 < n) {
     CK(B[B_REP].ensure(sizeof(int) * n));

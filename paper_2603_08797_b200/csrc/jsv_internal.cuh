@@ -216,6 +216,69 @@ __device__ inline void bundle_stats(const DGraph& g, const DTables& tb, int t, c
   }
 }
 
+// the same with the task's profile-key tables given directly (indexed by local key;
+// the fused Stage-1 kernel stages them in shared memory)
+__device__ inline void bundle_stats_k(const DGraph& g, const DTables& tb, int t, const uint32_t* items,
+                                      int n, Stat& s, const int* key_var, const int* key_cost,
+                                      const double* key_lat, const double* key_thr) {
+  int outd = g.succ_off[t + 1] - g.succ_off[t];
+  if (n == 0) {
+    s.lat = 0.0; s.cap = 0.0; s.acc = 1.0; s.sl = 0;
+    for (int j = 0; j < outd; ++j) s.fan[j] = 0.0;
+    return;
+  }
+  const int vb = g.var_off[t];
+  double lat = 0.0, cap = 0.0;
+  int sl = 0;
+  // weighted means with the all-equal short circuit (planner.py:155-166)
+  int v0 = key_var[(items[0] >> 16)];
+  double a0 = tb.var_acc[vb + v0];
+  bool acc_eq = true;
+  for (int i = 0; i < n; ++i) {
+    int k = (items[i] >> 16);
+    double c = (double)(items[i] & 0xFFFFu);
+    double h = c * key_thr[k];
+    lat = d_max(lat, key_lat[k]);
+    cap += h;
+    sl += (int)(items[i] & 0xFFFFu) * key_cost[k];
+    double a = tb.var_acc[vb + key_var[k]];
+    if (!(a == a0)) acc_eq = false;
+  }
+  s.lat = lat; s.cap = cap; s.sl = sl;
+  if (acc_eq) {
+    s.acc = a0;
+  } else {
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < n; ++i) {
+      int k = (items[i] >> 16);
+      double h = (double)(items[i] & 0xFFFFu) * key_thr[k];
+      num += tb.var_acc[vb + key_var[k]] * h;
+      den += h;
+    }
+    s.acc = num / den;
+  }
+  for (int j = 0; j < outd; ++j) {
+    double f0 = tb.var_fac[tb.var_fac_off[vb + v0] + j];
+    bool eq = true;
+    for (int i = 1; i < n; ++i) {
+      double f = tb.var_fac[tb.var_fac_off[vb + key_var[(items[i] >> 16)]] + j];
+      if (!(f == f0)) { eq = false; break; }
+    }
+    if (eq) {
+      s.fan[j] = f0;
+    } else {
+      double num = 0.0, den = 0.0;
+      for (int i = 0; i < n; ++i) {
+        int k = (items[i] >> 16);
+        double h = (double)(items[i] & 0xFFFFu) * key_thr[k];
+        num += tb.var_fac[tb.var_fac_off[vb + key_var[k]] + j] * h;
+        den += h;
+      }
+      s.fan[j] = num / den;
+    }
+  }
+}
+
 // Fraction-weighted path accuracy (model.py:267-282).
 __device__ inline double weighted_paths(const DGraph& g, const double* acc) {
   double total = 0.0;

@@ -106,6 +106,9 @@ struct S1Args {
   int wl_mask;    // bit k: the launch consumes work list k (set by launch_stage1)
   int4* wl[3];    // pair-pass work lists {job, i0, j0}: same-bucket, survivors, frontier
   int* wn;        // [3] their lengths (zeroed per batch)
+  int desc_t0[MAXT + 1];  // fused Stage 1: first descriptor of each task (descriptors by task)
+  int fused_cap;  // fused Stage 1: candidates whose working lists fit shared memory
+  unsigned long long* stamps;  // JSV_S1_PHASES: [jobs x 10] phase timestamps (else null)
 };
 
 struct S1Launch {
@@ -121,6 +124,8 @@ struct S1Launch {
 int stage1_padded_dims(int D);
 int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st);
 int launch_stage1_expand(const S1Args& a, const int* rep, int n_s1, int n, cudaStream_t st);
+size_t s1_fused_smem(int D, int NB, int cap);
+int launch_stage1_fused(const S1Args& a, size_t smem, cudaStream_t st);
 
 // ------------------------------------------------------------------ stage 2
 

@@ -85,6 +85,111 @@ __device__ __forceinline__ void store_candidate(const S1Args& a, int probe, int 
   for (int k = 0; k < n; ++k) a.items[c * a.maxi + k] = it[k];
 }
 
+// One enumeration unit lu of descriptor D for one probe: either one item list
+// (it[0 .. n), m = 1) or m singletons / homogeneous covers of one key (key1 >= 0,
+// counts[0 .. m)); m = 0: no candidate.
+struct GenOut {
+  uint32_t it[MAXI];
+  int n, m, key1;
+  int counts[N_LEVELS + 1];
+};
+
+__device__ __forceinline__ void gen_unit(const S1Args& a, int probe, const GenDesc& D, int lu,
+                                         GenOut& o, const unsigned* W) {
+  const DGraph& g = *a.g;
+  const DReq& rq = *a.rq;
+  const int t = D.task;
+  const int S = rq.S;
+  const int kb = g.key_off[t];
+  const int* tup = a.tb.sub_key + D.key_base;
+  o.n = 0;
+  o.m = 0;
+  o.key1 = -1;
+  if (D.mode == 0) {
+    // unrank count vector lu+1 (0 is the empty vector) -- _exhaustive_counts
+    unsigned long long idx = (unsigned long long)lu + 1ull;
+    int left = S;
+    bool ok = true;
+    for (int i = 0; i < D.n_tuples && ok; ++i) {
+      const int cost = a.tb.key_cost[kb + tup[i]];
+      int c = 0;
+      while (true) {
+        unsigned long long w = W[(i + 1) * (S + 1) + (left - c * cost)];
+        if (idx < w) break;
+        idx -= w;
+        ++c;
+      }
+      if (c > 0) {
+        if (o.n >= MAXI) { atomicExch(a.err, 2); ok = false; break; }
+        o.it[o.n++] = ((uint32_t)tup[i] << 16) | (uint32_t)c;
+      }
+      left -= c * cost;
+    }
+    o.m = ok ? 1 : 0;
+    return;
+  }
+  const DProbe& pr = a.probes[probe];
+  const double target = pr.r_upper[D.a][t] * (1.0 + rq.slack);
+  const bool has_lv = target > 0;
+  if (lu < D.n_tuple_units) {
+    // singleton + homogeneous covers of one tuple, distinct counts only
+    o.key1 = tup[lu];
+    const int cost = a.tb.key_cost[kb + o.key1];
+    const double h = a.tb.key_thr[kb + o.key1];
+    int cnt[N_LEVELS + 1];
+    int mm = 0;
+    if (cost <= S) cnt[mm++] = 1;
+    if (has_lv) {
+      for (int k = 0; k < N_LEVELS; ++k) {
+        int c = cover_count(target * c_grid[k], h, cost, S);
+        if (c > 0) cnt[mm++] = c;
+      }
+    }
+    for (int x = 0; x < mm; ++x) {
+      bool dup = false;
+      for (int y = 0; y < o.m; ++y) dup |= o.counts[y] == cnt[x];
+      if (!dup) o.counts[o.m++] = cnt[x];
+    }
+  } else if (has_lv) {
+    // two-variant mix unit: (pair, phi, level, rep_a, rep_b)
+    int mu = lu - D.n_tuple_units;
+    const int per_pair = rq.n_mix * N_LEVELS * 4;
+    int pi = mu / per_pair;
+    int rem = mu % per_pair;
+    const int rsel = rem & 3;
+    rem >>= 2;
+    const int lvk = rem % N_LEVELS;
+    const int ph = rem / N_LEVELS;
+    int ga = 0, gb = 1;
+    {
+      // pair index -> (ga < gb) in row-major order
+      int G = D.n_groups;
+      int acc = 0;
+      for (ga = 0; ga < G; ++ga) {
+        int cnt = G - 1 - ga;
+        if (pi < acc + cnt) { gb = ga + 1 + (pi - acc); break; }
+        acc += cnt;
+      }
+    }
+    const int ia = a.tb.grp_rep[2 * (D.grp_base + ga) + (rsel & 1)];
+    const int ib = a.tb.grp_rep[2 * (D.grp_base + gb) + (rsel >> 1)];
+    if (ia >= 0 && ib >= 0) {
+      const double phi = rq.mix[ph];
+      const double lvl = target * c_grid[lvk];
+      const int ka = tup[ia], kbb = tup[ib];
+      const int costa = a.tb.key_cost[kb + ka], costb = a.tb.key_cost[kb + kbb];
+      const int ca = cover_count(phi * lvl, a.tb.key_thr[kb + ka], costa, S);
+      const int cb = cover_count((1.0 - phi) * lvl, a.tb.key_thr[kb + kbb], costb, S);
+      if (ca != 0 && cb != 0 && ca * costa + cb * costb <= S) {
+        o.it[0] = ((uint32_t)ka << 16) | (uint32_t)ca;
+        o.it[1] = ((uint32_t)kbb << 16) | (uint32_t)cb;
+        o.n = 2;
+        o.m = 1;
+      }
+    }
+  }
+}
+
 __global__ void k_generate(const __grid_constant__ S1Args a) {
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const bool in = gtid < (long long)a.n_probes * a.U;
@@ -97,111 +202,21 @@ __global__ void k_generate(const __grid_constant__ S1Args a) {
   for (; step > 0; step >>= 1)
     if (d + step < a.n_desc && a.desc[d + step].unit_off <= u) d += step;
   const GenDesc D = a.desc[d];
-  const int lu = u - D.unit_off;
-  const DGraph& g = *a.g;
-  const DReq& rq = *a.rq;
   const int t = D.task;
-  const int S = rq.S;
-  const int kb = g.key_off[t];
-  const int* tup = a.tb.sub_key + D.key_base;
-  // this unit's candidates: one item list (n items), or m singletons of key `key1`
-  uint32_t it[MAXI];
-  int n = 0, m = 0, key1 = -1;
-  int counts[N_LEVELS + 1];
-  if (in) {
-    if (D.mode == 0) {
-      // unrank count vector lu+1 (0 is the empty vector) -- _exhaustive_counts
-      unsigned long long idx = (unsigned long long)lu + 1ull;
-      int left = S;
-      const unsigned* W = a.ways + D.w_off;
-      bool ok = true;
-      for (int i = 0; i < D.n_tuples && ok; ++i) {
-        const int cost = a.tb.key_cost[kb + tup[i]];
-        int c = 0;
-        while (true) {
-          unsigned long long w = W[(i + 1) * (S + 1) + (left - c * cost)];
-          if (idx < w) break;
-          idx -= w;
-          ++c;
-        }
-        if (c > 0) {
-          if (n >= MAXI) { atomicExch(a.err, 2); ok = false; break; }
-          it[n++] = ((uint32_t)tup[i] << 16) | (uint32_t)c;
-        }
-        left -= c * cost;
-      }
-      m = ok ? 1 : 0;
-    } else {
-      const DProbe& pr = a.probes[probe];
-      const double target = pr.r_upper[D.a][t] * (1.0 + rq.slack);
-      const bool has_lv = target > 0;
-      if (lu < D.n_tuple_units) {
-        // singleton + homogeneous covers of one tuple, distinct counts only
-        key1 = tup[lu];
-        const int cost = a.tb.key_cost[kb + key1];
-        const double h = a.tb.key_thr[kb + key1];
-        int mm = 0;
-        if (cost <= S) counts[mm++] = 1;
-        if (has_lv) {
-          for (int k = 0; k < N_LEVELS; ++k) {
-            int c = cover_count(target * c_grid[k], h, cost, S);
-            if (c > 0) counts[mm++] = c;
-          }
-        }
-        for (int x = 0; x < mm; ++x) {
-          bool dup = false;
-          for (int y = 0; y < m; ++y) dup |= counts[y] == counts[x];
-          if (!dup) counts[m++] = counts[x];
-        }
-      } else if (has_lv) {
-        // two-variant mix unit: (pair, phi, level, rep_a, rep_b)
-        int mu = lu - D.n_tuple_units;
-        const int per_pair = rq.n_mix * N_LEVELS * 4;
-        int pi = mu / per_pair;
-        int rem = mu % per_pair;
-        const int rsel = rem & 3;
-        rem >>= 2;
-        const int lvk = rem % N_LEVELS;
-        const int ph = rem / N_LEVELS;
-        int ga = 0, gb = 1;
-        {
-          // pair index -> (ga < gb) in row-major order
-          int G = D.n_groups;
-          int acc = 0;
-          for (ga = 0; ga < G; ++ga) {
-            int cnt = G - 1 - ga;
-            if (pi < acc + cnt) { gb = ga + 1 + (pi - acc); break; }
-            acc += cnt;
-          }
-        }
-        const int ia = a.tb.grp_rep[2 * (D.grp_base + ga) + (rsel & 1)];
-        const int ib = a.tb.grp_rep[2 * (D.grp_base + gb) + (rsel >> 1)];
-        if (ia >= 0 && ib >= 0) {
-          const double phi = rq.mix[ph];
-          const double lvl = target * c_grid[lvk];
-          const int ka = tup[ia], kbb = tup[ib];
-          const int costa = a.tb.key_cost[kb + ka], costb = a.tb.key_cost[kb + kbb];
-          const int ca = cover_count(phi * lvl, a.tb.key_thr[kb + ka], costa, S);
-          const int cb = cover_count((1.0 - phi) * lvl, a.tb.key_thr[kb + kbb], costb, S);
-          if (ca != 0 && cb != 0 && ca * costa + cb * costb <= S) {
-            it[0] = ((uint32_t)ka << 16) | (uint32_t)ca;
-            it[1] = ((uint32_t)kbb << 16) | (uint32_t)cb;
-            n = 2;
-            m = 1;
-          }
-        }
-      }
-    }
-  }
+  GenOut o;
+  o.m = 0;
+  o.n = 0;
+  o.key1 = -1;
+  if (in) gen_unit(a, probe, D, u - D.unit_off, o, a.ways + D.w_off);
   const int job = probe * a.T + t;
-  const int pos = reserve_slots(a, job, m, in);
-  if (key1 >= 0) {
-    for (int x = 0; x < m; ++x) {
-      const uint32_t one = ((uint32_t)key1 << 16) | (uint32_t)counts[x];
+  const int pos = reserve_slots(a, job, o.m, in);
+  if (o.key1 >= 0) {
+    for (int x = 0; x < o.m; ++x) {
+      const uint32_t one = ((uint32_t)o.key1 << 16) | (uint32_t)o.counts[x];
       store_candidate(a, probe, t, pos + x, &one, 1);
     }
-  } else if (m > 0) {
-    store_candidate(a, probe, t, pos, it, n);
+  } else if (o.m > 0) {
+    store_candidate(a, probe, t, pos, o.it, o.n);
   }
 }
 
@@ -994,6 +1009,610 @@ __global__ void __launch_bounds__(256) k_s1_expand(const __grid_constant__ S1Arg
 int launch_stage1_expand(const S1Args& a, const int* rep, int n_s1, int n, cudaStream_t st) {
   if (n <= n_s1) return 0;
   k_s1_expand<<<(unsigned)((n - n_s1) * a.T), 256, 0, st>>>(a, rep, n_s1);
+  return 1;
+}
+
+// ------------------------------------------------------------ fused Stage 1
+//
+// k_s1_job: one block per job (probe, task) runs all of Stage 1 for it -- the same
+// steps as the kernel chain above, with block barriers instead of kernel
+// boundaries and the job's working lists in shared memory (global scratch when a
+// job has more than S1Args::fused_cap candidates):
+//   A  enumeration units of the task's descriptors -> item lists (gen_unit);
+//   B  bundle statistics -> skyline rows (global `arr`, read by the exact tests);
+//   C  counting sort by slices, float shadow of coordinates 1..4 in list order;
+//   D  same-slices skyline pass (float-shadow quick reject, exact double test,
+//      equal rows: the smaller item list survives -- the reference's dedup);
+//   E  survivors in list order, their slice-bucket starts;
+//   F  survivors against the survivors with fewer slices;
+//   G  frontier (survivors in candidate order);
+//   H  frontier order (lexicographic rows) and capacity ranks by bitonic sorts
+//      (pair counting for non-finite rows or frontiers beyond the sort size);
+//   I  pareto_width truncation and the pool SoA + per-pool bounds.
+// Dominance is transitive, so the two passes equal the reference's sequential
+// "not dominated by an earlier kept row" filter (planner.py:543-583).
+
+__device__ __forceinline__ float4 s1_shadow(const S1Args& a, long long tot, long long c, int D) {
+  // coordinates 1..4 rounded to float (monotone); missing coordinates never reject
+  return make_float4((float)a.arr[1 * tot + c], (float)a.arr[2 * tot + c], (float)a.arr[3 * tot + c],
+                     D >= 5 ? (float)a.arr[4 * tot + c] : -INFINITY);
+}
+
+// stable block-wide compaction step: returns this thread's output slot (or -1) and
+// advances *carry by the chunk's count (all threads call it)
+template <class Scan>
+__device__ __forceinline__ int s1_compact_slot(typename Scan::TempStorage& tmp, int* carry, bool keep) {
+  int off, total;
+  Scan(tmp).ExclusiveSum(keep ? 1 : 0, off, total);
+  const int base = *carry;
+  __syncthreads();
+  if (threadIdx.x == 0) *carry = base + total;
+  __syncthreads();
+  return keep ? base + off : -1;
+}
+
+// exclusive bucket starts in place over h[0 .. nb) (h[i] holds the count of i - 1)
+template <class Scan, int S1F_THREADS>
+__device__ __forceinline__ void s1_scan_inplace(typename Scan::TempStorage& tmp, int* h, int nb,
+                                                int* carry) {
+  if (threadIdx.x == 0) *carry = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < nb; i0 += S1F_THREADS) {
+    const int i = i0 + threadIdx.x;
+    const int v = i < nb ? h[i] : 0;
+    int inc, total;
+    Scan(tmp).InclusiveSum(v, inc, total);
+    const int base = *carry;
+    if (i < nb) h[i] = base + inc;
+    __syncthreads();
+    if (threadIdx.x == 0) *carry = base + total;
+    __syncthreads();
+  }
+}
+
+// JSV_S1_PHASES: %globaltimer at the phase boundaries of every job (diagnostics)
+#define S1_STAMP(k)                                                            \
+  do {                                                                         \
+    if (a.stamps && threadIdx.x == 0) {                                        \
+      unsigned long long t_;                                                   \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+      a.stamps[blockIdx.x * 10 + (k)] = t_;                                    \
+    }                                                                          \
+  } while (0)
+// S1F_THREADS: 1024 (one block per SM, small batches: the most threads per job) or
+// 512 (two blocks per SM, large batches)
+template <int D, int S1F_THREADS>
+__global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(const __grid_constant__ S1Args a) {
+  extern __shared__ __align__(16) unsigned char s1_smem[];
+  typedef cub::BlockScan<int, S1F_THREADS> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int s_n, s_carry, s_ok;
+  __shared__ double s_rd[32];
+  __shared__ int s_ri[32];
+  __shared__ double s_ra[32];
+  const int job = blockIdx.x;
+  const int probe = job / a.T, t = job % a.T;
+  const long long tot = (long long)a.n_probes * a.C_probe;
+  const long long base = job_base(a, probe, t);
+  const int NB = a.S + 2;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const DGraph& g = *a.g;
+  int* bst = reinterpret_cast<int*>(s1_smem);  // [NB] slice-bucket starts
+  int* sbst = bst + NB;                        // [NB] survivor bucket starts (cursor in C)
+  unsigned char* pcand = s1_smem + (((size_t)2 * NB * sizeof(int) + 15) & ~(size_t)15);
+  if (tid == 0) s_n = 0;
+  S1_STAMP(0);
+  __syncthreads();
+
+  // per-candidate working lists: shared memory when the job fits, else global scratch
+  const int ncap = a.fused_cap;
+  // (before the lists are in use: the task's exhaustive ways tables for A and its
+  // profile-key tables for B are staged in their space)
+  int* st_i = reinterpret_cast<int*>(pcand);
+  const int nk = g.key_off[t + 1] - g.key_off[t];
+  const bool keys_sm = (size_t)nk * 24 <= (size_t)ncap * 16;
+  double* k_lat = reinterpret_cast<double*>(pcand);
+  double* k_thr = k_lat + nk;
+  int* k_var = reinterpret_cast<int*>(k_thr + nk);
+  int* k_cost = k_var + nk;
+  unsigned* w_sm = reinterpret_cast<unsigned*>(pcand + (size_t)ncap * 20 + 16);  // (shadow space)
+  int w_tot = 0;
+  for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d)
+    if (a.desc[d].mode == 0) w_tot += (a.desc[d].n_tuples + 1) * (a.S + 1);
+  const bool ways_sm = (size_t)w_tot * 4 <= (size_t)ncap * 16;
+  if (ways_sm) {
+    int o = 0;
+    for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d) {
+      const GenDesc& Dd = a.desc[d];
+      if (Dd.mode != 0) continue;
+      const int m = (Dd.n_tuples + 1) * (a.S + 1);
+      for (int i = tid; i < m; i += S1F_THREADS) w_sm[o + i] = a.ways[Dd.w_off + i];
+      o += m;
+    }
+  }
+  (void)st_i;
+  __syncthreads();
+  // ---- A: enumeration units of this task's descriptors (_candidate_pool's union)
+  int u_tot = 0;
+  for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d) u_tot += a.desc[d].n_units;
+  for (int u0 = 0; u0 < u_tot; u0 += S1F_THREADS) {
+    const int u = u0 + tid;
+    GenOut o;
+    o.m = 0;
+    o.n = 0;
+    o.key1 = -1;
+    if (u < u_tot) {
+      int d = a.desc_t0[t], lu = u, wo = 0;
+      while (lu >= a.desc[d].n_units) {
+        if (a.desc[d].mode == 0) wo += (a.desc[d].n_tuples + 1) * (a.S + 1);
+        lu -= a.desc[d++].n_units;
+      }
+      gen_unit(a, probe, a.desc[d], lu, o, ways_sm ? w_sm + wo : a.ways + a.desc[d].w_off);
+    }
+    // warp-aggregated slot reservation
+    int incl = o.m;
+    for (int k = 1; k < 32; k <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, k);
+      if (lane >= k) incl += v;
+    }
+    const int wtot = __shfl_sync(0xffffffffu, incl, 31);
+    int wb = 0;
+    if (lane == 31 && wtot) wb = atomicAdd(&s_n, wtot);
+    wb = __shfl_sync(0xffffffffu, wb, 31);
+    const int pos = wb + incl - o.m;
+    if (o.key1 >= 0) {
+      for (int x = 0; x < o.m; ++x) {
+        const uint32_t one = ((uint32_t)o.key1 << 16) | (uint32_t)o.counts[x];
+        store_candidate(a, probe, t, pos + x, &one, 1);
+      }
+    } else if (o.m > 0) {
+      store_candidate(a, probe, t, pos, o.it, o.n);
+    }
+  }
+  __syncthreads();
+  const int n = min(s_n, (int)a.task_cap[t]);
+  S1_STAMP(1);
+  if (tid == 0) a.cnt[job] = s_n;
+  if (keys_sm) {
+    const int kb = g.key_off[t];
+    for (int k = tid; k < nk; k += S1F_THREADS) {
+      k_lat[k] = a.tb.key_lat[kb + k];
+      k_thr[k] = a.tb.key_thr[kb + k];
+      k_var[k] = a.tb.key_var[kb + k];
+      k_cost[k] = a.tb.key_cost[kb + k];
+    }
+    __syncthreads();
+  }
+  const bool fits = n <= ncap;
+  int* front = fits ? reinterpret_cast<int*>(pcand) : a.front + base;
+  int* ord = fits ? front + ncap : a.order + base;
+  int* slp = fits ? ord + ncap : a.pcnt + base;
+  int* survp = fits ? slp + ncap : a.surv + base;  // list position of survivor k
+  int* sslp = fits ? survp + ncap : a.scr + base;
+  float4* shl = fits ? reinterpret_cast<float4*>(sslp + ncap + ((4 - (ncap & 3)) & 3))
+                     : a.arrf + base;
+  unsigned char* dead = fits ? reinterpret_cast<unsigned char*>(shl + ncap)
+                             : reinterpret_cast<unsigned char*>(a.flag + base);
+
+  // ---- B: bundle statistics (planner.py:155-213) -> skyline rows; C: bucket counts
+  for (int s0 = tid; s0 < NB; s0 += S1F_THREADS) bst[s0] = 0;
+  __syncthreads();
+  {
+    const int outd = g.succ_off[t + 1] - g.succ_off[t];
+    for (int c = tid; c < n; c += S1F_THREADS) {
+      Stat st;
+      uint32_t it[MAXI];
+      const long long cc = base + c;
+      const int ni = a.nitems[cc];
+      for (int k = 0; k < ni; ++k) it[k] = a.items[cc * a.maxi + k];
+      if (keys_sm) bundle_stats_k(g, a.tb, t, it, ni, st, k_var, k_cost, k_lat, k_thr);
+      else bundle_stats(g, a.tb, t, it, ni, st);
+      a.sl[cc] = st.sl;
+      a.arr[0 * tot + cc] = (double)st.sl;
+      a.arr[1 * tot + cc] = -st.cap;
+      a.arr[2 * tot + cc] = -st.acc;
+      a.arr[3 * tot + cc] = st.lat;
+      for (int j = 0; j < D - 4; ++j) a.arr[(4 + j) * tot + cc] = j < outd ? st.fan[j] : 0.0;
+      dead[c] = 0;
+    }
+  }
+  __syncthreads();
+  // ---- B': identical item lists (the same count vector enumerated in several
+  // sub-spaces, planner.py:628-632 unions them as a set) keep one candidate, by an
+  // open-addressing hash set in shared memory (in the shadow list's space, not yet in use)
+  int H = 1;
+  while (H < 2 * n) H <<= 1;
+  if (fits && H <= 4 * ncap) {
+    int* table = reinterpret_cast<int*>(shl);
+    for (int h = tid; h < H; h += S1F_THREADS) table[h] = -1;
+    __syncthreads();
+    for (int c = tid; c < n; c += S1F_THREADS) {
+      const long long cc = base + c;
+      const int ni = a.nitems[cc];
+      unsigned hv = 0x9E3779B9u * (unsigned)(ni + 1);
+      for (int k = 0; k < ni; ++k) {
+        unsigned x = a.items[cc * a.maxi + k] * 0xCC9E2D51u;
+        x = (x << 15) | (x >> 17);
+        hv = ((hv ^ (x * 0x1B873593u)) << 13 | (hv ^ (x * 0x1B873593u)) >> 19) * 5u + 0xE6546B64u;
+      }
+      hv ^= hv >> 16; hv *= 0x85EBCA6Bu; hv ^= hv >> 13;
+      for (int h = (int)(hv & (unsigned)(H - 1));; h = (h + 1) & (H - 1)) {
+        const int occ = atomicCAS(&table[h], -1, c);
+        if (occ == -1) break;
+        if (a.nitems[base + occ] == ni && cmp_items(a, base + occ, cc) == 0) {
+          dead[c] = 1;  // a duplicate of `occ`
+          break;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int c = tid; c < n; c += S1F_THREADS)
+    if (!dead[c]) atomicAdd(&bst[a.sl[base + c] + 1], 1);
+  __syncthreads();
+  S1_STAMP(2);
+  // ---- C: counting sort by slices (bucket starts bst[s] = #candidates with < s slices)
+  s1_scan_inplace<Scan, S1F_THREADS>(tmp, bst, NB, &s_carry);
+  for (int s0 = tid; s0 < NB; s0 += S1F_THREADS) sbst[s0] = bst[s0];
+  __syncthreads();
+  const int nl = bst[NB - 1];  // candidates in the slices-ordered list (duplicates left out)
+  for (int c = tid; c < n; c += S1F_THREADS) {
+    if (dead[c]) continue;
+    const int sl = a.sl[base + c];
+    const int p = atomicAdd(&sbst[sl], 1);
+    ord[p] = c;
+    slp[p] = sl;
+    shl[p] = s1_shadow(a, tot, base + c, D);
+  }
+  __syncthreads();
+
+  S1_STAMP(3);
+  // exact weak-dominance / dedup test of list entry j (candidate cj) against i
+  // (coordinates 1 .. D-1; coordinate 0, slices, is equal or smaller for j)
+  auto dominated = [&](const double* xi, int ci, int cj, bool same_slices) -> bool {
+    bool le = true, eq = true;
+#pragma unroll
+    for (int d = 1; d < D; ++d) {
+      const double xj = a.arr[d * tot + base + cj];
+      le = le && (xj <= xi[d]);
+      eq = eq && (xj == xi[d]);
+    }
+    if (!le) return false;
+    if (!eq || !same_slices) return true;  // (fewer slices: a different row)
+    if (cj == ci) return false;
+    const int c = cmp_items(a, base + cj, base + ci);
+    return c < 0 || (c == 0 && cj < ci);
+  };
+  constexpr int XJ = 8;
+  // ---- D: every candidate against its own slices bucket
+  for (int p = tid; p < nl; p += S1F_THREADS) {
+    const int ci = ord[p];
+    double xi[D];
+#pragma unroll
+    for (int d = 1; d < D; ++d) xi[d] = a.arr[d * tot + base + ci];
+    const float4 fi = shl[p];
+    const int sl = slp[p];
+    const int lo = bst[sl], hi = bst[sl + 1];
+    bool isdead = false;
+    for (int j = lo; j < hi && !isdead; j += XJ) {
+      unsigned keep = 0;
+#pragma unroll
+      for (int u = 0; u < XJ; ++u) {
+        if (j + u < hi) {
+          const float4 fj = shl[j + u];
+          const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
+          keep |= (rej ? 0u : 1u) << u;
+        }
+      }
+      while (keep && !isdead) {
+        const int u = __ffs(keep) - 1;
+        keep &= keep - 1;
+        if (j + u != p) isdead = dominated(xi, ci, ord[j + u], true);
+      }
+    }
+    if (isdead) dead[ci] = 1;
+  }
+  __syncthreads();
+  S1_STAMP(4);
+  // ---- E: survivors in list order and their bucket starts
+  if (tid == 0) s_carry = 0;
+  for (int s0 = tid; s0 < NB; s0 += S1F_THREADS) sbst[s0] = 0;
+  __syncthreads();
+  for (int p0 = 0; p0 < nl; p0 += S1F_THREADS) {
+    const int p = p0 + tid;
+    const bool keep = p < nl && !dead[ord[p]];
+    const int k = s1_compact_slot<Scan>(tmp, &s_carry, keep);
+    if (k >= 0) {
+      survp[k] = p;
+      sslp[k] = slp[p];
+      atomicAdd(&sbst[slp[p] + 1], 1);
+    }
+  }
+  __syncthreads();
+  const int ns = s_carry;
+  __syncthreads();  // (every thread has read the count before the scan reuses s_carry)
+  s1_scan_inplace<Scan, S1F_THREADS>(tmp, sbst, NB, &s_carry);
+  // ---- F: survivors against the survivors with fewer slices
+  for (int k = tid; k < ns; k += S1F_THREADS) {
+    const int ci = ord[survp[k]];
+    double xi[D];
+#pragma unroll
+    for (int d = 1; d < D; ++d) xi[d] = a.arr[d * tot + base + ci];
+    const float4 fi = shl[survp[k]];
+    const int hi = sbst[sslp[k]];
+    bool isdead = false;
+    for (int j = 0; j < hi && !isdead; j += XJ) {
+      unsigned keep = 0;
+#pragma unroll
+      for (int u = 0; u < XJ; ++u) {
+        if (j + u < hi) {
+          const float4 fj = shl[survp[j + u]];
+          const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
+          keep |= (rej ? 0u : 1u) << u;
+        }
+      }
+      while (keep && !isdead) {
+        const int u = __ffs(keep) - 1;
+        keep &= keep - 1;
+        isdead = dominated(xi, ci, ord[survp[j + u]], false);
+      }
+    }
+    if (isdead) dead[ci] = 1;
+  }
+  __syncthreads();
+  S1_STAMP(5);
+  // ---- G: the frontier in candidate order
+  if (tid == 0) s_carry = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < n; c0 += S1F_THREADS) {
+    const int c = c0 + tid;
+    const int k = s1_compact_slot<Scan>(tmp, &s_carry, c < n && !dead[c]);
+    if (k >= 0) front[k] = c;
+  }
+  __syncthreads();
+  const int F = s_carry;
+  if (tid == 0) a.fcnt[job] = F;
+
+  S1_STAMP(6);
+  // ---- H: frontier order (planner.py:556-559) and capacity ranks (planner.py:576)
+  int* fpos = a.fpos + base;  // [F] position of frontier entry k in row order
+  int* fcr = a.fcr + base;    // [F] its (-capacity, slices, items) rank (F > W)
+  constexpr int FMAX = D <= 12 ? FSORT_MAX : FSORT_MAX / 2;
+  int F2 = 1;
+  while (F2 < F) F2 <<= 1;
+  // sort keys after the frontier list (the other per-candidate lists are dead now)
+  double* key = reinterpret_cast<double*>(
+      fits ? pcand + (((size_t)F * sizeof(int) + 15) & ~(size_t)15) : pcand);
+  int* ix = reinterpret_cast<int*>(key + (size_t)D * F2);
+  if (tid == 0) s_ok = F <= FMAX;
+  __syncthreads();
+  if (s_ok) {
+    for (int k = tid; k < F2; k += S1F_THREADS) {
+      ix[k] = k;
+      if (k < F) {
+        const int c = front[k];
+        for (int d = 0; d < D; ++d) {
+          const double v = a.arr[d * tot + base + c];
+          if (!isfinite(v)) s_ok = 0;
+          key[d * F2 + k] = v;
+        }
+      } else {
+        for (int d = 0; d < D; ++d) key[d * F2 + k] = INFINITY;
+      }
+    }
+    __syncthreads();
+  }
+  if (s_ok) {
+    // sort 1: rows, lexicographic (distinct rows: the sorted rank is the count of
+    // smaller rows; padding rows +inf, ties by index)
+    for (int kk = 2; kk <= F2; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int h = tid; h < (F2 >> 1); h += S1F_THREADS) {
+          const int i = ((h & ~(j - 1)) << 1) | (h & (j - 1)), l = i | j;
+          const int x = ix[i], y = ix[l];
+          int c = 0;
+#pragma unroll
+          for (int d = 0; d < D; ++d) {
+            if (c == 0) {
+              const double u = key[d * F2 + x], v = key[d * F2 + y];
+              c = u < v ? -1 : (u > v ? 1 : 0);
+            }
+          }
+          if (c == 0) c = x < y ? -1 : 1;
+          if ((c > 0) == ((i & kk) == 0)) {
+            ix[i] = y;
+            ix[l] = x;
+          }
+        }
+        __syncthreads();
+      }
+    }
+    for (int r = tid; r < F; r += S1F_THREADS) fpos[ix[r]] = r;
+    if (F > a.W) {
+      __syncthreads();
+      for (int k = tid; k < F2; k += S1F_THREADS) ix[k] = k;
+      __syncthreads();
+      // sort 2: (-capacity, slices, items); padding -capacity = +inf
+      for (int kk = 2; kk <= F2; kk <<= 1) {
+        for (int j = kk >> 1; j > 0; j >>= 1) {
+          for (int h = tid; h < (F2 >> 1); h += S1F_THREADS) {
+            const int i = ((h & ~(j - 1)) << 1) | (h & (j - 1)), l = i | j;
+            const int x = ix[i], y = ix[l];
+            const double cx = key[1 * F2 + x], cy = key[1 * F2 + y];
+            int c;
+            if (cx != cy) c = cx < cy ? -1 : 1;
+            else if (x >= F || y >= F) c = x < y ? -1 : 1;
+            else if (key[x] != key[y]) c = key[x] < key[y] ? -1 : 1;
+            else c = cmp_items(a, base + front[x], base + front[y]);
+            if (c == 0) c = x < y ? -1 : 1;
+            if ((c > 0) == ((i & kk) == 0)) {
+              ix[i] = y;
+              ix[l] = x;
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int r = tid; r < F; r += S1F_THREADS) fcr[ix[r]] = r;
+    }
+  } else {
+    // pair counting (non-finite rows or a frontier beyond the sort size)
+    for (int i = tid; i < F; i += S1F_THREADS) {
+      const int ci = front[i];
+      int pos = 0, cr = 0;
+      for (int jj = 0; jj < F; ++jj) {
+        const int cj = front[jj];
+        int lt = 0;
+        for (int d = 0; d < D; ++d) {
+          if (lt == 0) {
+            const double xj = a.arr[d * tot + base + cj], xi = a.arr[d * tot + base + ci];
+            if (xj < xi) lt = 1;
+            else if (xj > xi) lt = -1;
+          }
+        }
+        pos += lt == 1;
+        if (F > a.W) {
+          const double c1 = a.arr[1 * tot + base + cj], c0 = a.arr[1 * tot + base + ci];
+          bool less;
+          if (c1 != c0) less = c1 < c0;
+          else if (a.arr[base + cj] != a.arr[base + ci]) less = a.arr[base + cj] < a.arr[base + ci];
+          else less = cmp_items(a, base + cj, base + ci) < 0;
+          cr += less;
+        }
+      }
+      fpos[i] = pos;
+      fcr[i] = cr;
+    }
+  }
+  __syncthreads();
+
+  S1_STAMP(7);
+  // ---- I: truncation to pareto_width (planner.py:574-583) and the pool
+  int* srt = a.sorted + base;  // frontier candidates in row order
+  int* scr = a.scr + base;     // ... and their capacity ranks
+  for (int i = tid; i < F; i += S1F_THREADS) {
+    const int p = fpos[i];
+    srt[p] = front[i];
+    scr[p] = fcr[i];
+  }
+  __syncthreads();
+  const int W = a.W;
+  int* pool = a.pool_cand + (long long)job * W;
+  int P;
+  if (F <= W) {
+    for (int k = tid; k < F; k += S1F_THREADS) pool[k] = srt[k];
+    P = F;
+    if (tid == 0) a.pool_trunc[job] = 0;
+  } else {
+    // the W/2 largest capacities, then the other frontier rows in row order
+    const int top_n = W / 2, rest = W - W / 2;
+    __shared__ int s_nontop, s_kept;
+    if (tid == 0) { s_nontop = 0; s_kept = 0; }
+    __syncthreads();
+    for (int s0 = 0; s0 < F; s0 += S1F_THREADS) {
+      const int k = s0 + tid;
+      const int nontop = (k < F && scr[k] >= top_n) ? 1 : 0;
+      int before, tot_nt;
+      Scan(tmp).ExclusiveSum(nontop, before, tot_nt);
+      __syncthreads();
+      const int keep = (k < F) && ((!nontop) || (s_nontop + before < rest));
+      int kpos, tot_k;
+      Scan(tmp).ExclusiveSum(keep, kpos, tot_k);
+      if (keep) pool[s_kept + kpos] = srt[k];
+      __syncthreads();
+      if (tid == 0) { s_nontop += tot_nt; s_kept += tot_k; }
+      __syncthreads();
+    }
+    P = s_kept;
+    if (tid == 0) a.pool_trunc[job] = 1;
+  }
+  __syncthreads();
+  const int outd = g.succ_off[t + 1] - g.succ_off[t];
+  double mlat = 1e308, macc = -1.0;
+  int msl = 0x7fffffff;
+  for (int k = tid; k < P; k += S1F_THREADS) {
+    const long long c = base + pool[k];
+    const long long q = (long long)job * W + k;
+    const double lat = a.arr[3 * tot + c];
+    const double acc = -a.arr[2 * tot + c];
+    const int sl = (int)a.arr[0 * tot + c];
+    a.p_sl[q] = sl;
+    a.p_cap[q] = -a.arr[1 * tot + c];
+    a.p_acc[q] = acc;
+    a.p_lat[q] = lat;
+    for (int j = 0; j < outd; ++j) a.p_fan[q * a.maxout + j] = a.arr[(4 + j) * tot + c];
+    const double l2 = 2.0 * lat;
+    if (l2 < mlat) mlat = l2;
+    if (sl < msl) msl = sl;
+    if (acc > macc) macc = acc;
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    mlat = fmin(mlat, __shfl_down_sync(0xffffffffu, mlat, d));
+    msl = min(msl, __shfl_down_sync(0xffffffffu, msl, d));
+    macc = fmax(macc, __shfl_down_sync(0xffffffffu, macc, d));
+  }
+  if (lane == 0) {
+    s_rd[tid >> 5] = mlat;
+    s_ri[tid >> 5] = msl;
+    s_ra[tid >> 5] = macc;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < S1F_THREADS / 32; ++w) {
+      if (s_rd[w] < mlat) mlat = s_rd[w];
+      if (s_ri[w] < msl) msl = s_ri[w];
+      if (s_ra[w] > macc) macc = s_ra[w];
+    }
+    mlat = fmin(mlat, s_rd[0]);
+    msl = min(msl, s_ri[0]);
+    macc = fmax(macc, s_ra[0]);
+    a.pool_n[job] = P;
+    a.pool_min_lat2[job] = mlat;
+    a.pool_min_sl[job] = msl;
+    a.pool_acc_ub[job] = macc;
+  }
+  S1_STAMP(8);
+}
+
+// shared memory of k_s1_job: bucket tables + per-candidate lists of fused_cap
+// candidates, or the frontier sort keys, whichever is larger
+size_t s1_fused_smem(int D, int NB, int cap) {
+  const size_t fixed = ((size_t)2 * NB * sizeof(int) + 15) & ~(size_t)15;
+  const size_t lists = (size_t)cap * (5 * sizeof(int) + sizeof(float4) + 1) + 64;
+  const int fmax = D <= 12 ? FSORT_MAX : FSORT_MAX / 2;
+  const size_t sort = (((size_t)fmax * sizeof(int) + 15) & ~(size_t)15) +
+                      (size_t)fmax * (D * sizeof(double) + sizeof(int));
+  return fixed + std::max(lists, sort);
+}
+
+int launch_stage1_fused(const S1Args& a, size_t smem, cudaStream_t st) {
+  const long long jobs = (long long)a.n_probes * a.T;
+  int dev = 0, n_sm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+#define JSV_S1F(DV, NT)                                                                              \
+  do {                                                                                               \
+    cudaFuncSetAttribute(k_s1_job<DV, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    k_s1_job<DV, NT><<<(unsigned)jobs, NT, smem, st>>>(a);                                           \
+  } while (0)
+#define JSV_S1FD(NT)                  \
+  switch (a.D) {                      \
+    case 4: JSV_S1F(4, NT); break;    \
+    case 5: JSV_S1F(5, NT); break;    \
+    case 6: JSV_S1F(6, NT); break;    \
+    case 8: JSV_S1F(8, NT); break;    \
+    case 12: JSV_S1F(12, NT); break;  \
+    default: JSV_S1F(16, NT); break;  \
+  }
+  PROF_BEGIN(K_GENERATE);
+  if (jobs <= n_sm) {
+    JSV_S1FD(1024);
+  } else {
+    JSV_S1FD(512);
+  }
+  PROF_END();
+#undef JSV_S1FD
+#undef JSV_S1F
   return 1;
 }
 
