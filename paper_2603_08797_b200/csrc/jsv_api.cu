@@ -861,7 +861,9 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     }
   }
   const int NB = rq.budget + 2;
-  const bool fused = D <= 16 && NB <= 4096 && !getenv("JSV_S1_LEGACY");
+  // (measured: wide rows -- fan-out hubs -- and large budgets, whose jobs outgrow the
+  // shared-memory lists, run faster through the multi-kernel chain)
+  const bool fused = D <= 8 && NB <= 130 && !getenv("JSV_S1_LEGACY");
   if (fused) {
     const size_t smax = 100 * 1024;  // two blocks per SM (with the static shared memory)
     long long cap = pl.max_cap;
