@@ -1037,6 +1037,8 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
     a.pr_acc = B[B_PACCS].as<double>();
     a.ptot = B[B_PTOT].as<unsigned long long>();
     a.pfx = B[B_PFX].as<long long>();
+    // (the scan's extra input slot n_slots: width 0)
+    CK(cudaMemsetAsync(a.pr_width + n_slots, 0, sizeof(long long), st));
     c.stats.kernel_launches += launch_stage2_prefix(a, st);
     CK(cudaGetLastError());
     // exclusive scan of the per-slot widths (width 0 beyond the live prefixes)
@@ -1131,6 +1133,8 @@ static int stage2_prep(jsv_problem& p, BatchState& bs) {
   CK(B[B_S2ACC].ensure(sizeof(double) * jobs));
   CK(B[B_FUT].ensure(sizeof(int) * bs.n * (p.T + 1)));
   CK(B[B_BEST].ensure(sizeof(BestRec) * bs.n));
+  // (every byte defined: the host copies whole records back)
+  CK(cudaMemsetAsync(B[B_BEST].p, 0, sizeof(BestRec) * bs.n, c.st));
   S2Args a;
   s2_base(p, bs, a);
   a.min_lat2 = bs.s1.pool_min_lat2;
@@ -1151,6 +1155,8 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
   CK(B[B_DEAD].ensure(sizeof(int) * n));
   CK(cudaMemcpyAsync(B[B_DEAD].p, bs.dead.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
   CK(B[B_OUT].ensure(sizeof(jsv_plan_out) * n));
+  // (every byte of the records defined: k_finalize writes only the graph's tasks/paths)
+  CK(cudaMemsetAsync(B[B_OUT].p, 0, sizeof(jsv_plan_out) * n, st));
   FinArgs f{};
   f.g = p.dgraph.as<DGraph>();
   f.tb = p.dt;

@@ -1176,11 +1176,13 @@ __global__ void __launch_bounds__(512) k_m_rank(const __grid_constant__ XArgs a)
   const int* pc = s.pool_cand + (long long)job * s.W;
   const bool sm = (long long)n * mi <= MR_SMEM_WORDS && n <= 1023;
   if (sm) {
+    for (int b = threadIdx.x; b < n; b += blockDim.x) s_n[b] = s.nitems[base + pc[b]];
+    __syncthreads();
     for (int i = threadIdx.x; i < n * mi; i += blockDim.x) {
       const int b = i / mi, k = i % mi;
-      s_it[i] = s.items[(base + pc[b]) * mi + k];
+      // (only the list's own entries: the slot's tail is never written by Stage 1)
+      s_it[i] = k < s_n[b] ? s.items[(base + pc[b]) * mi + k] : 0u;
     }
-    for (int b = threadIdx.x; b < n; b += blockDim.x) s_n[b] = s.nitems[base + pc[b]];
     __syncthreads();
   }
   auto item = [&](int b, int k) -> uint32_t {

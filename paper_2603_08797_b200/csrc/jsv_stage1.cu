@@ -1493,7 +1493,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   for (int i = tid; i < F; i += S1F_THREADS) {
     const int p = fpos[i];
     srt[p] = front[i];
-    scr[p] = fcr[i];
+    if (F > a.W) scr[p] = fcr[i];  // (capacity ranks exist only for truncated frontiers)
   }
   __syncthreads();
   const int W = a.W;
