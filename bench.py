@@ -256,6 +256,56 @@ def cpu_sample(args) -> dict:
             "solve_ms": wall * 1e3 * cores / n, "evaluated": sum(o[1] for o in outs)}
 
 
+def sweep_detail(dstat: dict, st: dict, kt: dict) -> dict:
+    """configs[2] beyond points/s: probes (the reference bisection's sequential count vs
+    the GPU's, speculation included), the device time of the sweep and its kernel
+    split, and the exhaustive kernel's work against the issue roof (as `roofline`)."""
+    dev_ms = st["ms_total"]
+    ms, cnt = kt.get("s2_exh", (0.0, 0))
+    f_clk = 1.965e9
+    peak = 148 * 4 * 32 * f_clk / 1e12
+    ops = st.get("swept", 0) * OPS_SWEPT + st.get("live_prefixes", 0) * OPS_PREFIX
+    achieved = ops / (ms / 1e3) / 1e12 if ms > 0 else 0.0
+    tot_k = sum(v[0] for v in kt.values()) or 1.0
+    return {"probes_reference": dstat.get("probes"), "probes_gpu": dstat.get("gpu_probes"),
+            "speculation_overhead": (dstat.get("gpu_probes", 0) / max(1, dstat.get("probes", 1))),
+            "device_ms": dev_ms, "probes_per_s_device": dstat.get("gpu_probes", 0) / (dev_ms / 1e3)
+            if dev_ms else None,
+            "decided_candidates_per_s_device": st["exh_candidates"] / (dev_ms / 1e3) if dev_ms else None,
+            "kernel_share": {k: round(v[0] / tot_k, 3) for k, v in sorted(kt.items(), key=lambda x: -x[1][0])
+                             if v[1] and v[0] / tot_k >= 0.02},
+            "roofline": {"bound": "issue", "kernel": "k_s2_exh", "achieved": achieved, "peak": peak,
+                         "unit": "Tops/s", "frac": achieved / peak, "launches": cnt,
+                         "ms": ms, "swept": st.get("swept", 0), "live_prefixes": st.get("live_prefixes", 0)}}
+
+
+def _cpu_point(i):
+    from oracle import planner_oracle as O
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    app, table = workloads.xr()
+    a = c3_apps(app)[i]
+    return O.max_demand(a, table, SLICE_BUDGET, SearchSpace(True, True, True)).demand_rps
+
+
+def cpu_sweep_all_cores(n_points: int = 32) -> dict:
+    """configs[2] on every host core: independent grid points through the oracle port
+    in a multiprocessing.Pool(os.cpu_count()) (max_demand is pure)."""
+    import multiprocessing as mp
+
+    cores = os.cpu_count() or 1
+    idx = list(range(0, 64, max(1, 64 // n_points)))[:n_points]
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_cpu_point, idx, chunksize=1)
+    wall = time.perf_counter() - t0
+    return {"value": len(idx) / wall, "unit": "points/s", "cores": cores, "kind": "port",
+            "sample": f"{len(idx)} of the 64 grid points (max_demand, rel_tol 1e-3) by "
+                      f"oracle/planner_oracle.py on {cores} processes in {wall:.1f}s"}
+
+
 def cpu_sweep_sample(app) -> dict:
     """configs[2] on the host: the oracle port's max_demand for two of the 64 grid
     points (one core), next to the GPU sweep's points/s."""
@@ -353,29 +403,39 @@ def star12_solve(P, torch, flush) -> dict:
             "solver": "fan-out knapsack-DP bounded enumeration + exact evaluation"}
 
 
-def traffic840(P) -> dict:
+def traffic840(P, rank: int = 0, world: int = 1, device=None) -> dict:
     """configs[4]: traffic-analysis on 840 slices -- max_demand in all 8 spaces, then the
-    288-bin day trace planned for A+S+T and the three ablations (one batch per space)."""
+    288-bin day trace planned for A+S+T and the three ablations (one batch per space).
+    Sharded over the ranks (independent units, no data-path collective):
+    spaces [rank::world] for max_demand and a contiguous block of the trace's bins per
+    space (shard.block_range); the caller takes the max of the times over ranks."""
     from paper_2603_08797_b200 import workload, workloads
     from paper_2603_08797_b200.plan_types import ALL_SPACES, SearchSpace
+    from paper_2603_08797_b200.shard import block_range
 
     app, table = workloads.traffic()
-    for sp in ALL_SPACES:  # warm-up (device buffers grown to this budget's sizes)
-        P.max_demand(app, table, 840, sp)
+    md_all = {}
+    for sp in ALL_SPACES:  # warm-up (device buffers grown to this budget's sizes); every
+        md_all[sp.label] = P.max_demand(app, table, 840, sp).demand_rps  # rank needs A+S+T
+    mine = ALL_SPACES[rank::world]
     t0 = time.perf_counter()
-    md = {sp.label: P.max_demand(app, table, 840, sp).demand_rps for sp in ALL_SPACES}
+    md = {sp.label: P.max_demand(app, table, 840, sp).demand_rps for sp in mine}
     md_ms = (time.perf_counter() - t0) * 1e3
-    trace = workload.gen_trace(workload.TraceShape(0.35, 0.65, 0.03, 288), md["A+S+T"], 21)
+    trace = workload.gen_trace(workload.TraceShape(0.35, 0.65, 0.03, 288), md_all["A+S+T"], 21)
     spaces = [SearchSpace.from_label(x) for x in ("A+S+T", "S+T", "A+T", "A+S")]
+    part = block_range(len(trace.bins), world, rank)
     for sp in spaces:  # warm-up
-        workload.plan_day(app, table, trace, 840, sp)
+        workload.plan_day(app, table, trace, 840, sp, device=device, part=part)
     t0 = time.perf_counter()
-    days = {sp.label: workload.plan_day(app, table, trace, 840, sp) for sp in spaces}
+    days = {sp.label: workload.plan_day(app, table, trace, 840, sp, device=device, part=part)
+            for sp in spaces}
     day_ms = (time.perf_counter() - t0) * 1e3
-    return {"max_demand_8_spaces_ms": md_ms, "max_demand_rps": md,
+    return {"max_demand_8_spaces_ms": md_ms, "max_demand_rps": md_all,
             "trace_bins": len(trace), "trace_plans": len(trace) * len(spaces), "trace_ms": day_ms,
             "trace_plans_per_s": len(trace) * len(spaces) / (day_ms / 1e3),
-            "fallback_bins": {k: sum(d.used_fallback for d in v) for k, v in days.items()}}
+            "fallback_bins": {k: sum(d.used_fallback for d in v) for k, v in days.items()},
+            "sharding": f"max_demand spaces [rank::{world}], trace bins [{part[0]}, {part[1]}) "
+                        f"of {len(trace)} on rank {rank}"}
 
 
 def main() -> None:
@@ -522,19 +582,37 @@ def main() -> None:
             sw.append((time.perf_counter() - t0) * 1e3)
         sweep_ms = min(sw)
         probes = sum(r.probes for r in mres)
+        dstat = P.last_demand_stats()
+        # one more pass with libjsv's per-kernel events: device time split and the
+        # exhaustive kernel's work (the sweep's feasibility probes use the same kernels)
+        N.profile(ctx, True)
+        N.kernel_times(ctx)  # (reset)
+        P.max_demand_grid(grid, table, SLICE_BUDGET, space, device=local)
+        sst = P.last_stats(local)
+        skt = N.kernel_times(ctx)
+        N.profile(ctx, False)
         extras["sweep_local"] = (len(grid), sweep_ms, probes)
+        extras["sweep_detail"] = sweep_detail(dstat, sst, skt)
+        c4 = traffic840(P, rank, world, device=local)
+        extras["c4_local"] = (c4["max_demand_8_spaces_ms"], c4["trace_ms"])
         if rank == 0:
             extras["configs3_star12"] = star12_solve(P, torch, flush)
-            extras["configs4_traffic840"] = traffic840(P)
+            extras["configs4_traffic840"] = c4
             extras["placement"] = place_plans(app, table, reqs)
 
-    t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1]],
-                     dtype=torch.float64, device="cpu" if one_gpu else "cuda")
+    c4_local = extras.pop("c4_local", (0.0, 0.0))
+    t = torch.tensor([dev_ms, e2e_ms, extras.get("sweep_local", (0, 0.0, 0))[1], c4_local[0],
+                      c4_local[1]], dtype=torch.float64, device="cpu" if one_gpu else "cuda")
     tc = torch.tensor([float(tot["exh_candidates"])], dtype=torch.float64, device=t.device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.all_reduce(tc, op=dist.ReduceOp.SUM)  # every rank's own demand points
-    dev_ms_max, e2e_ms_max, sweep_ms_max = t.tolist()
+    dev_ms_max, e2e_ms_max, sweep_ms_max, md_ms_max, day_ms_max = t.tolist()
+    if "configs4_traffic840" in extras:
+        c4 = extras["configs4_traffic840"]
+        c4["max_demand_8_spaces_ms"] = md_ms_max  # (max over ranks)
+        c4["trace_ms"] = day_ms_max
+        c4["trace_plans_per_s"] = c4["trace_plans"] / (day_ms_max / 1e3)
     total_cand = int(tc.item())
     value = total_cand / (dev_ms_max / 1e3)
     e2e_value = total_cand / (e2e_ms_max / 1e3)
@@ -587,12 +665,14 @@ def main() -> None:
                            "points": len(C3_LAT) * len(C3_ACC), "wall_ms": sweep_ms_max,
                            "points_per_s": len(C3_LAT) * len(C3_ACC) / (sweep_ms_max / 1e3),
                            "probes_rank0": probes}
+        extras["sweep"].update(extras.pop("sweep_detail"))
         line.update(extras)
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = {k: v for k, v in cpu_sample(args).items()
                                 if k in ("value", "unit", "cores", "kind", "sample")}
         if "sweep" in line:
             line["sweep"]["cpu_baseline"] = cpu_sweep_sample(app)
+            line["sweep"]["cpu_baseline_all_cores"] = cpu_sweep_all_cores()
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -63,6 +63,7 @@ __all__ = [
     "brute_force_plan",
     "plan_result_to_dict",
     "last_stats",
+    "last_demand_stats",
     "set_strategy",
 ]
 
@@ -506,6 +507,9 @@ def max_demand_grid(
     N.check(N.load_library().jsv_max_demand_batch(lw.ctx, lw.handle, C.byref(req), len(apps),
                                                   points, float(rel_tol), outs, plans))
     wall = (time.perf_counter() - t0) * 1000.0
+    global _LAST_DEMAND
+    _LAST_DEMAND = {"points": len(apps), "probes": sum(int(o.probes) for o in outs),
+                    "gpu_probes": sum(int(o.gpu_probes) for o in outs), "wall_ms": wall}
     res = []
     for i, a in enumerate(apps):
         o = outs[i]
@@ -514,6 +518,16 @@ def max_demand_grid(
         pr = _result_from(plans[i], a, lw, PlanRequest(plan_dem, slice_budget, space, slack), wall)
         res.append(MaxDemandResult(dem, pr, int(o.probes)))
     return res
+
+
+_LAST_DEMAND: dict = {}
+
+
+def last_demand_stats() -> dict:
+    """Probe counts of the last max_demand / max_demand_grid call: `probes` is the
+    reference bisection's sequential count (MaxDemandResult.probes), `gpu_probes` the
+    probes the GPU evaluated, speculation included."""
+    return dict(_LAST_DEMAND)
 
 
 def max_demand(

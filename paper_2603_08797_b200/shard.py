@@ -180,3 +180,26 @@ def plan_sharded(app, profile, request, options=None, group=None, device=None):
         records = all_gather_records(records[0], group, device)
     return combine_sharded(app, profile, request, lw, local, records,
                            bool(options.feasible_only))
+
+
+def plan_day_sharded(app, profile, trace, slice_budget: int, space, slack: float = 0.05,
+                     options=None, group=None, device=None) -> list:
+    """workload.plan_day with the trace's bins split into contiguous blocks over the
+    ranks of ``group`` (bins are independent plans once the sequential demand
+    predictions are made; every rank computes those); the blocks are gathered on
+    every rank (result plumbing, not a data-path collective)."""
+    import torch.distributed as dist
+
+    from . import workload
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    lo, hi = block_range(len(trace.bins), world, rank)
+    local = workload.plan_day(app, profile, trace, slice_budget, space, slack, options, device,
+                              part=(lo, hi))
+    if world == 1:
+        return local
+    parts = [None] * world
+    dist.all_gather_object(parts, local, group=group)
+    return [p for part in parts for p in part]
+

@@ -161,21 +161,26 @@ class DayPlan:
 
 def plan_day(app, profile, trace: DemandTrace, slice_budget: int, space: SearchSpace,
              slack: float = 0.05, options: PlannerOptions | None = None,
-             device: int | None = None) -> list[DayPlan]:
+             device: int | None = None, part: tuple[int, int] | None = None) -> list[DayPlan]:
     """run_day's planning decisions for a whole trace in one GPU batch.
 
     Same plans as the reference loop with no simulated factor history
     (factor_overrides None): ``plan()`` at each bin's predicted demand, and the
     memoised ``max_demand`` plan for bins whose prediction is infeasible.
+    ``part = (lo, hi)`` plans only bins lo..hi-1 (the predictions still run over
+    the whole trace: each depends on the bins before it) -- one rank's share.
     """
     from . import planner
 
     preds = predicted_demands(trace, slack)
+    lo, hi = part if part is not None else (0, len(preds))
+    bins = trace.bins[lo:hi]
+    preds = preds[lo:hi]
     reqs = [PlanRequest(d, slice_budget, space, slack) for d in preds]
-    results = planner.plan_batch(app, profile, reqs, options, device=device)
+    results = planner.plan_batch(app, profile, reqs, options, device=device) if reqs else []
     fallback = None
     out = []
-    for (idx, actual), pred, res in zip(trace.bins, preds, results):
+    for (idx, actual), pred, res in zip(bins, preds, results):
         used = False
         if not res.feasible:
             if fallback is None:

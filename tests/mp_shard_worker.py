@@ -53,6 +53,19 @@ def main() -> None:
             if got != row["result"]:
                 bad.append(f"bench@{row['demand']}")
         n = len(docs)
+    elif mode == "day":
+        from paper_2603_08797_b200 import workload as W
+
+        gold = load("day_traffic_840_full.json.gz")
+        app, table = workloads.traffic()
+        tr = W.DemandTrace(tuple(enumerate(gold["demands"])))
+        day = shard.plan_day_sharded(app, table, tr, gold["budget"], SearchSpace(True, True, True),
+                                     gold["slack"], device=local)
+        for row in gold["plans"]["A+S+T"]:
+            d = day[row["bin"]]
+            if d.used_fallback != row["used_fallback"] or result_dict(d.plan) != row["plan"]:
+                bad.append(f"bin{row['bin']}")
+        n = len(day)
     else:
         gold = load("max_demand_c3.json")
         app, table = workloads.xr()

@@ -96,3 +96,31 @@ def test_torchrun_two_ranks_sharded_sweep():
     assert sorted(x["rank"] for x in lines) == [0, 1]
     for x in lines:
         assert x["mismatches"] == [], x
+
+
+def test_torchrun_two_ranks_sharded_day_trace():
+    """configs[4]'s day trace with its bins split over two ranks (shard.plan_day_sharded)."""
+    lines = _torchrun(["day"])
+    assert sorted(x["rank"] for x in lines) == [0, 1]
+    for x in lines:
+        assert x["cases"] == 288 and x["mismatches"] == [], x
+
+
+
+def test_torchrun_two_rank_bench_line():
+    """bench.py's multi-rank path (the driver's SCALE run) on one GPU: two ranks over gloo,
+    weak-scaled solves, the sweep and configs[4] sharded, one JSON line from rank 0."""
+    port = 20000 + random.Random().randrange(20000)
+    env = dict(os.environ, JSV_BENCH_ONE_GPU="1", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline"]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env, cwd=ROOT)
+    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    lines = [json.loads(x) for x in p.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["e2e"]["value"] > 0
+    c4 = d["configs4_traffic840"]
+    assert c4["trace_plans"] == 1152 and c4["max_demand_rps"]["A+S+T"] == 65152.0
+    assert d["sweep"]["points"] == 64

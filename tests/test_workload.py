@@ -57,3 +57,27 @@ def test_plan_day_matches_reference(gold, space):
         assert d.predicted_rps == gold["predicted"][row["bin"]]
         assert d.used_fallback == row["used_fallback"], row["bin"]
         assert result_dict(d.plan) == row["plan"], row["bin"]
+
+
+@pytest.mark.gpu
+def test_plan_day_parts_match_reference(gold):
+    """The ranks' shares (plan_day(part=...), as shard.plan_day_sharded and the
+    bench's sharded configs[4] extra use them) reassemble the reference's day."""
+    from paper_2603_08797_b200 import workload as W
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import SearchSpace
+    from paper_2603_08797_b200.shard import block_range
+
+    app, table = workloads.traffic()
+    tr = W.DemandTrace(tuple(enumerate(gold["demands"])))
+    sp = SearchSpace.from_label("A+S+T")
+    for world in (3, 8):
+        day = []
+        for r in range(world):
+            day += W.plan_day(app, table, tr, gold["budget"], sp, gold["slack"],
+                              part=block_range(288, world, r))
+        assert [d.bin_index for d in day] == list(range(288))
+        for row in gold["plans"]["A+S+T"][::3]:
+            d = day[row["bin"]]
+            assert d.used_fallback == row["used_fallback"], row["bin"]
+            assert result_dict(d.plan) == row["plan"], row["bin"]
