@@ -960,7 +960,7 @@ static void s2_base(jsv_problem& p, BatchState& bs, S2Args& a) {
 
 // Level-synchronous search over the active probes (T-informed plans).
 static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_config,
-                      const std::vector<int>& active, long long* nodes_out) {
+                      const std::vector<int>& active, std::vector<long long>* nodes_out) {
   jsv_context& c = *p.ctx;
   cudaStream_t st = c.st;
   auto& B = c.buf;
@@ -1058,6 +1058,7 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
       pstart[i] = total;
       total += (long long)ptot[i];
       nodes += (long long)fcnt[i];
+      if (nodes_out) (*nodes_out)[i] += (long long)fcnt[i];  // frontier prefixes of probe i
     }
     if (last && !diag) c.stats.leaf_work += total;
     if (total > 0) {
@@ -1120,7 +1121,7 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   CK(cudaMemcpyAsync(&err, B[B_ERR].p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (err) return fail(JSV_ERR_CAPACITY, "stage-2 frontier capacity exceeded");
-  if (nodes_out) *nodes_out += nodes;
+  if (nodes_out) c.stats.nodes += nodes;  // (not the diagnostic re-run)
   return JSV_OK;
 }
 
@@ -1602,14 +1603,12 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     JSV_T("exhaustive issued");
     rc = run_fanout(p, bs, active);
     if (rc) return rc;
-    long long nn = 0;
     bool any_search = false;
     for (int i = 0; i < n; ++i) any_search = any_search || (active[i] && !bs.dead[i]);
     if (any_search) {
-      rc = run_stage2(p, bs, false, want_config, active, &nn);
+      rc = run_stage2(p, bs, false, want_config, active, &nodes);
       if (rc) return rc;
     }
-    c.stats.nodes += nn;
     JSV_T("search issued");
     // infeasible full plans: diagnostic re-run for the binding constraint
     std::vector<BestRec> best(n);

@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(128) k_fo_eval(const __grid_constant__ FoArgs 
     for (int k = 0; k < T; ++k) B->choice[k] = ch[k];
   }
   atomicAdd(&B->leaves, 1ull);
+  atomicAdd(&B->nodes, 1ull);  // (stats.nodes: candidates evaluated one by one)
   spin_unlock(&B->lock);
 }
 

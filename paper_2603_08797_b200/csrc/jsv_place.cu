@@ -35,7 +35,7 @@ struct Geo {
 };
 
 int load_geo(const jsv_geometry* g, Geo& G) {
-  if (!g || g->n_profiles <= 0 || g->slices_per_gpu <= 0 || g->slices_per_gpu > 30)
+  if (!g || g->n_profiles <= 0 || g->slices_per_gpu <= 0 || g->slices_per_gpu > 63)
     return jsv_fail_msg(JSV_ERR_ARG, "bad geometry");
   G.np = g->n_profiles;
   G.spg = g->slices_per_gpu;
@@ -55,7 +55,8 @@ int load_geo(const jsv_geometry* g, Geo& G) {
   return JSV_OK;
 }
 
-inline uint32_t span(int start, int width) { return ((1u << width) - 1u) << start; }
+// 64-bit occupancy masks: up to 63 slices per GPU
+inline uint64_t span(int start, int width) { return ((1ull << width) - 1ull) << start; }
 
 // _exact_pack (placement.py:219-266): (gpu, start, width) per sorted position
 struct Exact {
@@ -64,11 +65,11 @@ struct Exact {
   int gpus;
   long long budget, nodes = 0;
   bool exhausted = false;
-  uint32_t full;
-  std::vector<uint32_t> fr;
+  uint64_t full;
+  std::vector<uint64_t> fr;
   std::vector<int> cg, cs, cw;
   Exact(const Geo& g, const std::vector<int>& m, int n, long long b)
-      : G(g), migs(m), gpus(n), budget(b), full((1u << g.spg) - 1u), fr(n, (1u << g.spg) - 1u) {}
+      : G(g), migs(m), gpus(n), budget(b), full((1ull << g.spg) - 1ull), fr(n, (1ull << g.spg) - 1ull) {}
   bool place(size_t i, int floor_gpu, int floor_start) {
     if (i == migs.size()) return true;
     ++nodes;
@@ -85,7 +86,7 @@ struct Exact {
       for (const auto& sw : G.starts[migs[i]]) {
         const int s = sw.first, w = sw.second;
         if (same_as_prev && (g < floor_gpu || (g == floor_gpu && s < floor_start))) continue;
-        const uint32_t m = span(s, w);
+        const uint64_t m = span(s, w);
         if ((fr[g] & m) == m) {
           fr[g] &= ~m;
           cg.push_back(g); cs.push_back(s); cw.push_back(w);
@@ -107,7 +108,7 @@ int pack_impl(const Geo& G, const int32_t* prof, int n, int gpu_count, long long
   for (int i = 0; i < n; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(),
                    [&](int x, int y) { return G.rank[prof[x]] < G.rank[prof[y]]; });
-  std::vector<uint32_t> fr(gpu_count, 0u);  // occupied bits
+  std::vector<uint64_t> fr(gpu_count, 0ull);  // occupied bits
   bool any_unplaced = false;
   for (int i = 0; i < n; ++i) placed[i] = 0;
   for (int idx : order) {
@@ -115,7 +116,7 @@ int pack_impl(const Geo& G, const int32_t* prof, int n, int gpu_count, long long
     bool done = false;
     for (int g = 0; g < gpu_count && !done; ++g)
       for (const auto& sw : G.starts[p]) {
-        const uint32_t m = span(sw.first, sw.second);
+        const uint64_t m = span(sw.first, sw.second);
         if (!(fr[g] & m)) {
           fr[g] |= m;
           gpu[idx] = g; start[idx] = sw.first; width[idx] = sw.second; placed[idx] = 1;

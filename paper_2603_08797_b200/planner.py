@@ -374,9 +374,28 @@ def plan_batch(
     if not requests:
         return []
     t0 = time.perf_counter()
+    w = int((options or PlannerOptions()).pareto_width)
+    if w == 0 and requests[0].space.task_graph_informed:
+        return [_zero_width_result(a, profile, r, device)
+                for a, r in zip(list(apps) if apps is not None else [app] * len(requests), requests)]
+    if not 1 <= w <= 32766:
+        raise ConfigError(f"pareto_width {w} is outside the supported range 1..32766 "
+                          "(0 only with a task-graph-informed space)")
     outs, lw, apps = solve_records(app, profile, requests, options, apps, device)
     wall = (time.perf_counter() - t0) * 1000.0
     return _results_from(outs, apps, lw, requests, wall)
+
+
+def _zero_width_result(app, profile, request: PlanRequest, device=None) -> PlanResult:
+    """pareto_width = 0: _pareto_filter keeps no bundle of any (non-empty) frontier
+    (planner.py:574-583), so every pool is empty and truncated and the first task is
+    dead -- plan() returns its "resources" result (planner.py:930-938)."""
+    t0 = time.perf_counter()
+    lw, _ = _prepare(app, profile, request, PlannerOptions(), device)
+    order = tuple(app.graph.topological_order)
+    stats = SolverStats(nodes=0, wall_ms=(time.perf_counter() - t0) * 1000.0,
+                        pool_sizes={t: 0 for t in order}, truncated_tasks=order)
+    return PlanResult(False, None, None, lw.a_max, "resources", (), stats)
 
 
 def solve_records(app, profile, requests: Sequence[PlanRequest], options=None, apps=None,

@@ -181,3 +181,42 @@ def test_star_through_generic_strategies_matches_reference(monkeypatch):
         if len(app.graph.task_ids) > 4:
             continue
         assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]
+
+
+def test_pareto_width_zero_matches_reference():
+    """pareto_width = 0 empties every pool: the reference's dead-task "resources" result
+    (tests/golden/plans_width0.json, tools/make_golden_width0.py)."""
+    from paper_2603_08797_b200 import planner
+
+    for doc in load("plans_width0.json"):
+        app, table, req, opt = case_inputs(doc)
+        assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]
+
+
+def test_pareto_width_out_of_range_is_a_config_error():
+    from paper_2603_08797_b200 import planner, workloads
+    from paper_2603_08797_b200.errors import ConfigError
+    from paper_2603_08797_b200.plan_types import PlannerOptions, PlanRequest, SearchSpace
+
+    app, table = workloads.xr()
+    for w in (-1, 40000):
+        with pytest.raises(ConfigError, match="pareto_width"):
+            planner.plan(app, table, PlanRequest(300.0, 28, SearchSpace(True, True, True)),
+                         PlannerOptions(pareto_width=w))
+
+
+@pytest.mark.parametrize("strategy", ["exhaustive", "search"])
+def test_stats_nodes_reported(strategy):
+    """SolverStats.nodes is filled per plan (the reference counts _visit calls; here:
+    allocations compared one by one in the sweep, or frontier prefixes of the
+    level-synchronous search) -- positive for a solved plan, 0 for a dead one."""
+    from paper_2603_08797_b200 import planner, workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    app, table = workloads.xr()
+    planner.set_strategy(strategy, 1 << 32)
+    try:
+        res = planner.plan(app, table, PlanRequest(480.0, 28, SearchSpace(True, True, True)))
+    finally:
+        planner.set_strategy("auto")
+    assert res.feasible and res.stats.nodes > 0

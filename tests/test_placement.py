@@ -158,3 +158,14 @@ def test_random_packings_are_geometry_clean():
                 assert (p.gpu, c) not in grid
                 grid[(p.gpu, c)] = p.instance
         assert len(plan.placements) + len(plan.unplaced) == len(items)
+
+
+def test_wide_geometry_matches_reference(tmp_path):
+    """48 slices per GPU (64-bit occupancy masks in libjsv): the reference's packings."""
+    p = tmp_path / "wide.json"
+    p.write_text(json.dumps(G["wide_geometry"]))
+    geo = load_geometry(p)
+    for c in G["wide"]:
+        segs = segs_of(c["segs"])
+        assert plan_doc(pack(segs, c["gpus"], geo)) == c["pack"]
+        assert min_gpus(segs, geo) == c["min_gpus"]

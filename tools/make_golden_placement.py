@@ -75,8 +75,22 @@ def main() -> None:
                              "pack": plan_doc(pack(segs, n, custom)),
                              "min_gpus": min_gpus(segs, custom),
                              "render": render_plan(pack(segs, n, custom), custom)})
+    # a wide geometry (48 slices per GPU: six 8-slice blocks of the custom layout),
+    # beyond 32-bit occupancy masks
+    wide = MigGeometry(slices_per_gpu=48, placements={
+        m: {b * 8 + s: w for b in range(6) for s, w in custom.placements[m].items()}
+        for m in custom.placements})
+    rng = random.Random(4848)
+    wide_cases = []
+    for _ in range(40):
+        segs = [SegmentType(rng.choice(profiles), 1) for _ in range(rng.randint(1, 30))]
+        n = rng.randint(1, 3)
+        wide_cases.append({"segs": [[s.mig, s.mps] for s in segs], "gpus": n,
+                           "pack": plan_doc(pack(segs, n, wide)),
+                           "min_gpus": min_gpus(segs, wide)})
     out = {"default_digest": DEFAULT_GEOMETRY.digest(), "cases": cases, "plans": plans,
-           "custom_geometry": json.loads(custom.canonical_json()), "custom": custom_cases}
+           "custom_geometry": json.loads(custom.canonical_json()), "custom": custom_cases,
+           "wide_geometry": json.loads(wide.canonical_json()), "wide": wide_cases}
     (OUT / "placement.json").write_text(json.dumps(out))
     print(len(cases), "pack cases,", len(plans), "plans,", len(custom_cases), "custom")
 
