@@ -398,9 +398,17 @@ def star12_solve(P, torch, flush) -> dict:
         r = P.plan(app, table, req)
         wall.append((time.perf_counter() - t0) * 1e3)
         dev.append(P.last_stats()["ms_total"])
+    # max_demand: the bisection's feasibility probes answered by the fan-out solver
+    sp = SearchSpace(True, True, True)
+    P.max_demand(app, table, 84, sp)
+    t0 = time.perf_counter()
+    md = P.max_demand(app, table, 84, sp)
+    md_ms = (time.perf_counter() - t0) * 1e3
     return {"solve_ms": statistics.median(dev), "solve_wall_ms": statistics.median(wall),
             "objective": r.objective, "total_slices": r.config.total_slices,
-            "solver": "fan-out knapsack-DP bounded enumeration + exact evaluation"}
+            "solver": "fan-out knapsack-DP bounded enumeration + exact evaluation",
+            "max_demand_rps": md.demand_rps, "max_demand_probes": md.probes,
+            "max_demand_ms": md_ms}
 
 
 def traffic840(P, rank: int = 0, world: int = 1, device=None) -> dict:

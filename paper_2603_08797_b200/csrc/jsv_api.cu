@@ -1416,9 +1416,14 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
 // cross-product is too large to sweep: knapsack-DP bounded enumeration of the
 // near-optimal class vectors + exact evaluation (jsv_fanout.cuh).  Full plans
 // only; clears active[i] for the probes it solved.
-static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active) {
+static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active, bool want_config) {
   jsv_context& c = *p.ctx;
-  if (c.strategy == JSV_STRATEGY_SEARCH || bs.feasible_only || !p.lat_fast) return JSV_OK;
+  // feasible_only with a configuration wanted returns the first feasible leaf in DFS
+  // order, not an argmax: the branch-and-bound's job.  Verdict-only probes
+  // (max_demand's feasibility probes) need only whether the argmax exists.
+  const bool verdict = bs.feasible_only && !want_config;
+  if (c.strategy == JSV_STRATEGY_SEARCH || (bs.feasible_only && want_config) || !p.lat_fast)
+    return JSV_OK;
   if (getenv("JSV_NO_FANOUT")) return JSV_OK;
   const int n = bs.n, T = p.T;
   if (T < 3 || p.P != T - 1) return JSV_OK;
@@ -1502,6 +1507,12 @@ static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active) 
       if (!act[i]) continue;
       if (!std::isfinite(tau[i])) {  // no entry bundle reaches the accuracy SLO: infeasible
         act[i] = 0;
+        if (verdict) active[i] = 0;  // (a full plan's re-run supplies the binding constraint)
+        continue;
+      }
+      if (best[i].has && verdict) {  // a feasible allocation exists: the probe's verdict
+        act[i] = 0;
+        active[i] = 0;
         continue;
       }
       if (best[i].has) {
@@ -1601,7 +1612,7 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     rc = run_exhaustive(p, bs, want_config, active);
     if (rc) return rc;
     JSV_T("exhaustive issued");
-    rc = run_fanout(p, bs, active);
+    rc = run_fanout(p, bs, active, want_config);
     if (rc) return rc;
     bool any_search = false;
     for (int i = 0; i < n; ++i) any_search = any_search || (active[i] && !bs.dead[i]);

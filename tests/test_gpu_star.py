@@ -42,3 +42,40 @@ def test_star_large_matches_exact_oracle(doc):
     app, table = workloads.star(doc["n_tasks"])
     r = P.plan(app, table, PlanRequest(200.0, 84, SearchSpace(True, True, True)))
     assert result_dict(r) == doc["result"]
+
+
+@pytest.mark.parametrize("doc", load("max_demand_star.json"), ids=lambda d: d["name"])
+@pytest.mark.parametrize("fanout", [True, False])
+def test_star_max_demand_matches_reference(doc, fanout, monkeypatch):
+    """max_demand on the 3- and 4-task stars (reference: 68 s / 131 s): the fan-out
+    solver answers the bisection's feasibility probes (verdict mode) exactly as the
+    reference's branch-and-bound does (JSV_NO_FANOUT: the GPU branch-and-bound)."""
+    from golden_io import app_from_dict, profile_of
+
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    if not fanout:
+        monkeypatch.setenv("JSV_NO_FANOUT", "1")
+    app = app_from_dict(doc["app"])
+    r = P.max_demand(app, profile_of(doc), doc["budget"], SearchSpace.from_label(doc["space"]),
+                     doc["slack"], None, doc["rel_tol"])
+    assert r.demand_rps == doc["demand"] and r.probes == doc["probes"]
+    assert result_dict(r.plan) == doc["plan"]
+
+
+def test_star12_max_demand_solves():
+    """configs[3] at 12 tasks: max_demand's ~25 feasibility probes answered by the fan-out
+    solver (the GPU branch-and-bound runs out of frontier memory here and the
+    reference does not finish a single plan); the final plan at the returned demand
+    is feasible and equals plan() there (pinned to the exact CPU star solver above)."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    app, table = workloads.star(12)
+    sp = SearchSpace(True, True, True)
+    r = P.max_demand(app, table, 84, sp)
+    assert r.demand_rps > 0 and r.plan.feasible and 10 <= r.probes <= 40
+    again = P.plan(app, table, PlanRequest(r.demand_rps, 84, sp))
+    assert result_dict(again) == result_dict(r.plan)
