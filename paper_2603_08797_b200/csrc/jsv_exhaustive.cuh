@@ -1524,15 +1524,13 @@ size_t x_smem_bytes(int max_pn_last, int P, bool rank) {
 #define JSV_XOCC(PMV, F, RP)                                                                  \
   do {                                                                                        \
     if (smem > 40 * 1024)                                                                     \
-      cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                        \
+      jsv_smem_attr((const void*)k_s2_exh<PMV, F, RP>, smem);                                                        \
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_s2_exh<PMV, F, RP>, XBLOCK, smem); \
   } while (0)
 #define JSV_XLAUNCH(PMV, F, RP)                                                                \
   do {                                                                                        \
     if (smem > 40 * 1024)                                                                     \
-      cudaFuncSetAttribute(k_s2_exh<PMV, F, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                           (int)smem);                                                        \
+      jsv_smem_attr((const void*)k_s2_exh<PMV, F, RP>, smem);                                                        \
     k_s2_exh<PMV, F, RP><<<(unsigned)grid, XBLOCK, smem, st>>>(a);                            \
   } while (0)
 
@@ -1561,7 +1559,7 @@ int launch_x_rank(const XArgs& a, cudaStream_t st) {
   int n2 = 1;
   while (n2 < a.max_pn_last) n2 <<= 1;
   const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;
-  if (sm2 > 48 * 1024) cudaFuncSetAttribute(k_x_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+  if (sm2 > 48 * 1024) jsv_smem_attr((const void*)k_x_rank, sm2);
   cudaMemsetAsync(a.xr_done, 0, sizeof(int) * a.s.n_probes, st);
   PROF_BEGIN_ON(K_S2_XSORT, st);
   k_x_rank<<<dim3(a.s.n_probes, 3), 512, sm2, st>>>(a, n2);

@@ -40,6 +40,20 @@ struct Prof {
 };
 
 extern thread_local Prof* g_prof;
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size):
+// the call costs microseconds of host time on every launch otherwise
+#include <map>
+inline void jsv_smem_attr(const void* fn, size_t bytes) {
+  static thread_local std::map<std::pair<int, const void*>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  size_t& cur = done[{dev, fn}];
+  if (bytes > cur) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    cur = bytes;
+  }
+}
 #define PROF_BEGIN(id) \
   do {                 \
     if (g_prof) g_prof->begin(id); \

@@ -1087,6 +1087,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   typedef cub::BlockScan<int, S1F_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_n, s_carry, s_ok;
+  __shared__ int s_work[3];  // dynamic work counters: units (A), list positions (D), survivors (F)
   __shared__ double s_rd[32];
   __shared__ int s_ri[32];
   __shared__ double s_ra[32];
@@ -1100,7 +1101,10 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   int* bst = reinterpret_cast<int*>(s1_smem);  // [NB] slice-bucket starts
   int* sbst = bst + NB;                        // [NB] survivor bucket starts (cursor in C)
   unsigned char* pcand = s1_smem + (((size_t)2 * NB * sizeof(int) + 15) & ~(size_t)15);
-  if (tid == 0) s_n = 0;
+  if (tid == 0) {
+    s_n = 0;
+    s_work[0] = s_work[1] = s_work[2] = 0;
+  }
   S1_STAMP(0);
   __syncthreads();
 
@@ -1135,8 +1139,13 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   // ---- A: enumeration units of this task's descriptors (_candidate_pool's union)
   int u_tot = 0;
   for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d) u_tot += a.desc[d].n_units;
-  for (int u0 = 0; u0 < u_tot; u0 += S1F_THREADS) {
-    const int u = u0 + tid;
+  // warps take groups of 32 units from a shared counter (unit costs differ: exhaustive
+  // unranking, cover levels, mixes)
+  for (int u0 = 0;;) {
+    if (lane == 0) u0 = atomicAdd(&s_work[0], 32);
+    u0 = __shfl_sync(0xffffffffu, u0, 0);
+    if (u0 >= u_tot) break;
+    const int u = u0 + lane;
     GenOut o;
     o.m = 0;
     o.n = 0;
@@ -1285,7 +1294,13 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   };
   constexpr int XJ = 8;
   // ---- D: every candidate against its own slices bucket
-  for (int p = tid; p < nl; p += S1F_THREADS) {
+  // (warps take 32 list positions at a time: the bucket scans differ in length)
+  for (int p0 = 0;;) {
+    if (lane == 0) p0 = atomicAdd(&s_work[1], 32);
+    p0 = __shfl_sync(0xffffffffu, p0, 0);
+    if (p0 >= nl) break;
+    const int p = p0 + lane;
+    if (p >= nl) continue;
     const int ci = ord[p];
     double xi[D];
 #pragma unroll
@@ -1333,7 +1348,12 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   __syncthreads();  // (every thread has read the count before the scan reuses s_carry)
   s1_scan_inplace<Scan, S1F_THREADS>(tmp, sbst, NB, &s_carry);
   // ---- F: survivors against the survivors with fewer slices
-  for (int k = tid; k < ns; k += S1F_THREADS) {
+  for (int k0 = 0;;) {
+    if (lane == 0) k0 = atomicAdd(&s_work[2], 32);
+    k0 = __shfl_sync(0xffffffffu, k0, 0);
+    if (k0 >= ns) break;
+    const int k = k0 + lane;
+    if (k >= ns) continue;
     const int ci = ord[survp[k]];
     double xi[D];
 #pragma unroll
@@ -1592,7 +1612,7 @@ int launch_stage1_fused(const S1Args& a, size_t smem, cudaStream_t st) {
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
 #define JSV_S1F(DV, NT)                                                                              \
   do {                                                                                               \
-    cudaFuncSetAttribute(k_s1_job<DV, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);  \
+    jsv_smem_attr((const void*)k_s1_job<DV, NT>, smem);                                    \
     k_s1_job<DV, NT><<<(unsigned)jobs, NT, smem, st>>>(a);                                           \
   } while (0)
 #define JSV_S1FD(NT)                  \
@@ -1724,7 +1744,7 @@ int launch_stage1(const S1Args& a0, const S1Launch& L, cudaStream_t st) {
       const size_t fsm = (size_t)F2 * (a.D * sizeof(double) + sizeof(int));
 #define JSV_FS(DV)                                                                               \
   do {                                                                                           \
-    cudaFuncSetAttribute(k_front_sort<DV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fsm); \
+    jsv_smem_attr((const void*)k_front_sort<DV>, fsm);                                   \
     k_front_sort<DV><<<a.n_probes * a.T, 512, fsm, st>>>(a);                                      \
   } while (0)
       switch (a.D) {
