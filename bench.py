@@ -208,6 +208,45 @@ def roofline(kt: dict, tot: dict, dom: str = "s2_exh") -> dict:
                            "(not in MEASURED_PEAKS)"}
 
 
+# fused Stage 1 (k_s1_job) algorithmic lane-ops per unit: a skyline pair test on the
+# float shadow (4 compares), an exact test behind it (2 (D - 1) double compares, D = 5
+# for XR rows), a generated candidate's statistics (bundle_stats: per item a multiply,
+# max, add and integer multiply-add, ~2.5 items -> 12)
+OPS_SHADOW = 4
+OPS_EXACT = 8
+OPS_CAND = 12
+
+
+def roofline_s1(kt: dict, tot: dict) -> dict:
+    """k_s1_job (fused Stage 1) against the same SM issue roof as `roofline` (the work
+    it does per launch: pair tests of both skyline passes and candidate statistics;
+    generation, hash dedup, frontier sorts and truncation counted as overhead)."""
+    ms, cnt = kt.get("generate", (0.0, 0))
+    per_launch_ms = ms / max(1, cnt)
+    peak = 148 * 4 * 32 * 1.965e9 / 1e12
+    ops = (tot.get("s1_shadow_tests", 0) * OPS_SHADOW + tot.get("s1_exact_tests", 0) * OPS_EXACT +
+           tot.get("candidates_generated", 0) * OPS_CAND) / max(1, cnt)
+    achieved = ops / (per_launch_ms / 1e3) / 1e12 if per_launch_ms > 0 else 0.0
+    traffic = issue = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            d = json.load(fh).get("k_s1_job")
+        if d:
+            traffic = d["dram_read_bytes"] + d["dram_write_bytes"]
+            issue = d.get("issue_active_pct")
+    return {"bound": "issue", "kernel": "k_s1_job", "achieved": achieved, "peak": peak,
+            "unit": "Tops/s", "frac": achieved / peak if peak else None, "traffic": traffic,
+            "ops_per_shadow_test": OPS_SHADOW, "ops_per_exact_test": OPS_EXACT,
+            "ops_per_candidate": OPS_CAND,
+            "shadow_tests_per_launch": tot.get("s1_shadow_tests", 0) / max(1, cnt),
+            "exact_tests_per_launch": tot.get("s1_exact_tests", 0) / max(1, cnt),
+            "candidates_per_launch": tot.get("candidates_generated", 0) / max(1, cnt),
+            "per_launch_ms": per_launch_ms, "share_of_step": ms / max(1e-9, tot["ms_total"]),
+            "issue_active": issue,
+            "peak_source": "derived: 148 SM x 4 schedulers x 32 lanes x 1.965 GHz issue"}
+
+
 def place_plans(app, table, reqs) -> dict:
     """the cli `plan` tail (cli.py:173-174) -- every plan's
     instance_segments -> min_gpus -> pack, through placement.py (libjsv host code)."""
@@ -516,7 +555,8 @@ def main() -> None:
     dev_ms = e2e_ms = 0.0
     launches = 0
     tot = {"exh_candidates": 0, "leaves": 0, "swept": 0, "live_prefixes": 0, "ms_total": 0.0,
-           "ms_stage1": 0.0, "ms_stage2": 0.0}
+           "ms_stage1": 0.0, "ms_stage2": 0.0, "s1_shadow_tests": 0, "s1_exact_tests": 0,
+           "candidates_generated": 0}
     for _ in range(args.steps):
         flush.zero_()
         torch.cuda.synchronize()
@@ -663,7 +703,10 @@ def main() -> None:
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms_max / args.steps},
         "gpu_launches": launches,
         "clocks": clk,
-        "roofline": roofline(kt, tot),
+        # the dominant kernel of the step (largest share of the device time) first
+        **dict(zip(("roofline", "roofline_next"),
+                   sorted((roofline(kt, tot), roofline_s1(kt, tot)),
+                          key=lambda r: -r["share_of_step"]))),
         "kernel_ms": {k: round(v[0], 4) for k, v in kt.items() if v[1]},
     }
     if extras:

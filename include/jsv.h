@@ -196,6 +196,8 @@ typedef struct {
                                            throughput verdicts */
   int64_t live_prefixes;                /* prefixes the exhaustive sweep derived in full (the
                                            others failed a prefix task's throughput verdict) */
+  int64_t s1_shadow_tests;              /* fused Stage 1: skyline pair tests on the float shadow */
+  int64_t s1_exact_tests;               /* ... and exact double tests behind them */
 } jsv_stats;
 
 const char* jsv_last_error(void);

@@ -90,7 +90,8 @@ class Stats(C.Structure):
                 ("kernel_launches", C.c_int32), ("dims", C.c_int32), ("pair_tests_a", C.c_int64),
                 ("pair_tests_b", C.c_int64), ("leaf_work", C.c_int64),
                 ("exh_candidates", C.c_int64), ("exh_probes", C.c_int32), ("exh_pad_", C.c_int32),
-                ("swept", C.c_int64), ("live_prefixes", C.c_int64)]
+                ("swept", C.c_int64), ("live_prefixes", C.c_int64),
+                ("s1_shadow_tests", C.c_int64), ("s1_exact_tests", C.c_int64)]
 
 
 EXPORTS = {

@@ -86,7 +86,7 @@ enum BufId {
   B_REQ, B_PROBES, B_DESC, B_WAYS, B_TILE_TASK, B_TILE_START, B_ITEMS, B_NITEMS, B_ARR, B_SL, B_FLAG,
   B_CNT, B_FRONT, B_FCNT, B_FPOS, B_FCR, B_SORTED, B_SCR, B_POOLC, B_POOLN, B_POOLT, B_PSL,
   B_PCAP, B_PACC, B_PLAT, B_PFAN, B_S1LAT2, B_S1SL, B_S1ACC, B_S2LAT2, B_S2SL,
-  B_XLIVE, B_MRANK, B_XRDONE, B_STAMPS, B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
+  B_XLIVE, B_MRANK, B_XRDONE, B_STAMPS, B_S1TESTS, B_S2ACC, B_FUT, B_BEST, B_FR0, B_FR1, B_FLAGS, B_NXTCNT, B_NXTOFF, B_NXTCAP, B_WOFF, B_FOFF,
   B_WIDTH, B_PPROBE, B_DEAD, B_PICK, B_UKILL, B_OUT, B_ERR, B_DITEMS, B_DN, B_VAL, B_ACTIVE,
   B_BOFF, B_PART, B_INC, B_ORDER, B_BSTART, B_PFX, B_PFXOFF, B_SCAN, B_CNT2, B_FCAP,
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
@@ -878,6 +878,9 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
       CK(B[B_STAMPS].ensure(sizeof(unsigned long long) * 10 * (size_t)n_s1 * T));
       a.stamps = B[B_STAMPS].as<unsigned long long>();
     }
+    CK(B[B_S1TESTS].ensure(2 * sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(B[B_S1TESTS].p, 0, 2 * sizeof(unsigned long long), st));
+    a.tests = B[B_S1TESTS].as<unsigned long long>();
     c.stats.kernel_launches += launch_stage1_fused(a, smem, st);
     if (phases) {
       // mean phase durations over the jobs (diagnostics on stderr)
@@ -910,9 +913,14 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   bs.n = n;
   bs.pool_n.resize(jobs);
   CK(cudaMemcpyAsync(bs.pool_n.data(), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
+  unsigned long long tests[2] = {0, 0};
+  if (a.tests)
+    CK(cudaMemcpyAsync(tests, a.tests, sizeof(tests), cudaMemcpyDeviceToHost, st));
   int err = 0;
   CK(cudaMemcpyAsync(&err, a.err, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  c.stats.s1_shadow_tests += (long long)tests[0];
+  c.stats.s1_exact_tests += (long long)tests[1];
   if (err) return fail(JSV_ERR_CAPACITY, "stage-1 candidate capacity exceeded (code " +
                                              std::to_string(err) + ")");
   bs.dead.assign(n, 0);

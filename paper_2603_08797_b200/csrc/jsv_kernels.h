@@ -123,6 +123,7 @@ struct S1Args {
   int desc_t0[MAXT + 1];  // fused Stage 1: first descriptor of each task (descriptors by task)
   int fused_cap;  // fused Stage 1: candidates whose working lists fit shared memory
   unsigned long long* stamps;  // JSV_S1_PHASES: [jobs x 10] phase timestamps (else null)
+  unsigned long long* tests;   // fused Stage 1: [2] skyline pair tests (float shadow, exact)
 };
 
 struct S1Launch {

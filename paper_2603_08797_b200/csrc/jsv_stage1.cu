@@ -1293,6 +1293,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
     return c < 0 || (c == 0 && cj < ci);
   };
   constexpr int XJ = 8;
+  unsigned n_sh = 0, n_ex = 0;  // pair tests of the two passes: float shadow / exact
   // ---- D: every candidate against its own slices bucket
   // (warps take 32 list positions at a time: the bucket scans differ in length)
   for (int p0 = 0;;) {
@@ -1315,6 +1316,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
       for (int u = 0; u < XJ; ++u) {
         if (j + u < hi) {
           const float4 fj = shl[j + u];
+          ++n_sh;
           const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
           keep |= (rej ? 0u : 1u) << u;
         }
@@ -1322,7 +1324,10 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
       while (keep && !isdead) {
         const int u = __ffs(keep) - 1;
         keep &= keep - 1;
-        if (j + u != p) isdead = dominated(xi, ci, ord[j + u], true);
+        if (j + u != p) {
+          isdead = dominated(xi, ci, ord[j + u], true);
+          ++n_ex;
+        }
       }
     }
     if (isdead) dead[ci] = 1;
@@ -1367,6 +1372,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
       for (int u = 0; u < XJ; ++u) {
         if (j + u < hi) {
           const float4 fj = shl[survp[j + u]];
+          ++n_sh;
           const bool rej = (fj.x > fi.x) | (fj.y > fi.y) | (fj.z > fi.z) | (fj.w > fi.w);
           keep |= (rej ? 0u : 1u) << u;
         }
@@ -1375,12 +1381,24 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
         const int u = __ffs(keep) - 1;
         keep &= keep - 1;
         isdead = dominated(xi, ci, ord[survp[j + u]], false);
+        ++n_ex;
       }
     }
     if (isdead) dead[ci] = 1;
   }
   __syncthreads();
   S1_STAMP(5);
+  if (a.tests) {
+    unsigned long long sh = n_sh, ex = n_ex;
+    for (int d = 16; d > 0; d >>= 1) {
+      sh += __shfl_down_sync(0xffffffffu, sh, d);
+      ex += __shfl_down_sync(0xffffffffu, ex, d);
+    }
+    if (lane == 0) {
+      atomicAdd(&a.tests[0], sh);
+      atomicAdd(&a.tests[1], ex);
+    }
+  }
   // ---- G: the frontier in candidate order
   if (tid == 0) s_carry = 0;
   __syncthreads();
