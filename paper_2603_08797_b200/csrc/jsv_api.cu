@@ -1490,6 +1490,8 @@ static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active, 
   a.ncand = B[B_FONCAND].as<unsigned long long>();
   a.cand_cap = cap;
   a.overflow = B[B_FOOVF].as<int>();
+  a.shard_rank = c.shard_rank;
+  a.shard_world = c.shard_world;
   c.stats.kernel_launches += launch_fanout_prep(a, st);
   c.stats.kernel_launches += launch_fanout_tau(a, 1e-9, st);
   CK(cudaGetLastError());
@@ -1515,7 +1517,10 @@ static int run_fanout(jsv_problem& p, BatchState& bs, std::vector<int>& active, 
       if (!act[i]) continue;
       if (!std::isfinite(tau[i])) {  // no entry bundle reaches the accuracy SLO: infeasible
         act[i] = 0;
-        if (verdict) active[i] = 0;  // (a full plan's re-run supplies the binding constraint)
+        // (a full plan's re-run supplies the binding constraint; a shard of a split
+        // solve reports "nothing in my block" -- shard.combine_sharded re-runs the
+        // whole solve when no shard is feasible)
+        if (verdict || c.shard_world > 1) active[i] = 0;
         continue;
       }
       if (best[i].has && verdict) {  // a feasible allocation exists: the probe's verdict
@@ -1642,7 +1647,9 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
         fprintf(stderr, "[jsv] probe %d has %d leaves %llu obj %.17g\n", i, best[i].has,
                 best[i].leaves, best[i].obj);
     for (int i = 0; i < n; ++i) {
-      if (!best[i].has && !bs.dead[i] && want_config) {
+      // (a shard of a split solve skips the diagnosis: shard.combine_sharded re-runs the
+      // whole solve when no shard is feasible)
+      if (!best[i].has && !bs.dead[i] && want_config && c.shard_world == 1) {
         redo[i] = 1;
         any = true;
       }

@@ -80,7 +80,10 @@ __global__ void __launch_bounds__(256) k_fo_prep(const __grid_constant__ FoArgs 
   const int T = s.T;
   const int P0 = s.pool_n[probe * T + a.entry];
   const long long bq = ((long long)probe * a.P0max + b0);
-  if (!a.act[probe] || b0 >= P0) {
+  // (sharded solve: this rank's block of entry bundles)
+  const int lo0 = (int)((long long)P0 * a.shard_rank / a.shard_world);
+  const int hi0 = (int)((long long)P0 * (a.shard_rank + 1) / a.shard_world);
+  if (!a.act[probe] || b0 >= P0 || b0 < lo0 || b0 >= hi0) {
     if (threadIdx.x == 0) a.b0best[bq] = -INFINITY;
     return;
   }

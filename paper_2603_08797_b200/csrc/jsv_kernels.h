@@ -329,6 +329,7 @@ struct FoArgs {
   unsigned long long* ncand;
   long long cand_cap;
   int* overflow;
+  int shard_rank, shard_world;  // entry bundles b0 in [P0 r / W, P0 (r + 1) / W) only
 };
 
 int launch_fanout_prep(const FoArgs& a, cudaStream_t st);

@@ -121,7 +121,8 @@ def all_gather_records(words: Sequence[int], group=None, device=None) -> list[li
     return out.view(world, t.numel()).cpu().tolist()
 
 
-def combine_sharded(app, profile, request, lw, local, records, feasible_only: bool = False):
+def combine_sharded(app, profile, request, lw, local, records, feasible_only: bool = False,
+                    options=None, device=None):
     """The global PlanResult on every rank from the gathered shard records.
 
     No shard feasible: every rank ran the same replicated infeasibility
@@ -136,8 +137,13 @@ def combine_sharded(app, profile, request, lw, local, records, feasible_only: bo
 
     T = len(lw.ids)
     win = pick_record(records, T, feasible_only)
+    if win is None:
+        # no shard holds a feasible allocation: the whole solve, unsharded, gives the
+        # reference's infeasible result with its binding constraint (every rank alike)
+        outs, lw, _ = planner.solve_records(app, profile, [request], options, device=device)
+        return planner.decode_records((N.PlanOut * 1).from_buffer_copy(outs[0]), app, lw, [request])[0]
     own = plan_record(local, T)
-    if win is None or list(records[win]) == own:
+    if list(records[win]) == own:
         return planner.decode_records((N.PlanOut * 1).from_buffer_copy(local), app, lw, [request])[0]
     words = records[win]
     n_items = [int(words[3 + t * (1 + N.MAX_ITEMS)]) for t in range(T)] + [0] * (N.MAX_TASKS - T)
@@ -179,7 +185,7 @@ def plan_sharded(app, profile, request, options=None, group=None, device=None):
     if world > 1:
         records = all_gather_records(records[0], group, device)
     return combine_sharded(app, profile, request, lw, local, records,
-                           bool(options.feasible_only))
+                           bool(options.feasible_only), options, device)
 
 
 def plan_day_sharded(app, profile, trace, slice_budget: int, space, slack: float = 0.05,

@@ -45,7 +45,8 @@ def _sharded(planner, shard, app, table, req, opt, world):
         o, lw, _ = planner.solve_records(app, table, [req], opt, shard=(r, world))
         outs.append(o[0])
     records = [shard.plan_record(o, len(lw.ids)) for o in outs]
-    return [shard.combine_sharded(app, table, req, lw, outs[r], records, bool(opt.feasible_only))
+    return [shard.combine_sharded(app, table, req, lw, outs[r], records, bool(opt.feasible_only),
+                                  opt)
             for r in range(world)]
 
 
@@ -124,3 +125,25 @@ def test_torchrun_two_rank_bench_line():
     c4 = d["configs4_traffic840"]
     assert c4["trace_plans"] == 1152 and c4["max_demand_rps"]["A+S+T"] == 65152.0
     assert d["sweep"]["points"] == 64
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_sharded_star_fanout_matches_goldens(env, world):
+    """Row (e3): the fan-out solver of a wide star split over shards by entry bundle
+    (each shard's block of b0, one record combine): the 3..7-task ladder against the
+    reference and 8/10/12 tasks against the exact star oracle, on every rank."""
+    planner, shard = env
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlannerOptions, PlanRequest, SearchSpace
+
+    planner.set_strategy("auto")
+    for doc in load("plans_star.json") + load("plans_star_ladder.json"):
+        app, table, req, opt = case_inputs(doc)
+        for res in _sharded(planner, shard, app, table, req, opt, world):
+            assert result_dict(res) == doc["result"], doc["name"]
+    for doc in load("plans_star_large.json"):
+        app, table = workloads.star(doc["n_tasks"])
+        req = PlanRequest(200.0, 84, SearchSpace(True, True, True))
+        for res in _sharded(planner, shard, app, table, req, PlannerOptions(), world):
+            assert result_dict(res) == doc["result"], doc["n_tasks"]
+
