@@ -116,8 +116,8 @@ struct jsv_context {
   // pageable ones); reused call to call -- every call synchronises before returning
   // (slot 1: the exhaustive probes' records, in flight together with slot 0's
   // chunk tables)
-  void* hpin[2] = {nullptr, nullptr};
-  size_t hpin_cap[2] = {0, 0};
+  void* hpin[3] = {nullptr, nullptr, nullptr};
+  size_t hpin_cap[3] = {0, 0, 0};
   void* pinned(size_t bytes, int slot = 0) {
     if (bytes > hpin_cap[slot]) {
       if (hpin[slot]) cudaFreeHost(hpin[slot]);
@@ -685,6 +685,7 @@ struct BatchState {
   std::vector<int> pool_n;
   std::vector<int> dead;
   std::vector<DProbe> probes;
+  bool s1_pending = false;  // Stage-1 readbacks in flight (stage1_collect)
 };
 
 static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe* probes,
@@ -911,14 +912,37 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     CK(cudaGetLastError());
   }
   bs.n = n;
-  bs.pool_n.resize(jobs);
-  CK(cudaMemcpyAsync(bs.pool_n.data(), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
-  unsigned long long tests[2] = {0, 0};
-  if (a.tests)
-    CK(cudaMemcpyAsync(tests, a.tests, sizeof(tests), cudaMemcpyDeviceToHost, st));
+  // pool sizes, pair-test counters and the error flag into pinned staging, read by
+  // stage1_collect after the caller's next synchronisation (Stage 2 of exhaustive
+  // probes is planned on the device, so no host round trip sits between the stages)
+  {
+    const size_t bytes = sizeof(long long) * 3 + sizeof(int) * (size_t)jobs;
+    char* h = static_cast<char*>(c.pinned(bytes, 2));
+    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    memset(h, 0, sizeof(long long) * 3);
+    if (a.tests) CK(cudaMemcpyAsync(h, a.tests, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h + 2 * sizeof(long long), a.err, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h + 3 * sizeof(long long), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost,
+                       st));
+  }
+  bs.s1_pending = true;
+  return JSV_OK;
+}
+
+// After a synchronisation: Stage 1's readbacks -> pool sizes, dead probes, errors
+static int stage1_collect(jsv_problem& p, BatchState& bs) {
+  if (!bs.s1_pending) return JSV_OK;
+  bs.s1_pending = false;
+  jsv_context& c = *p.ctx;
+  const int n = bs.n, T = p.T;
+  const size_t jobs = (size_t)n * T;
+  const char* h = static_cast<const char*>(c.hpin[2]);
+  unsigned long long tests[2];
   int err = 0;
-  CK(cudaMemcpyAsync(&err, a.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  memcpy(tests, h, sizeof(tests));
+  memcpy(&err, h + 2 * sizeof(long long), sizeof(int));
+  bs.pool_n.resize(jobs);
+  memcpy(bs.pool_n.data(), h + 3 * sizeof(long long), sizeof(int) * jobs);
   c.stats.s1_shadow_tests += (long long)tests[0];
   c.stats.s1_exact_tests += (long long)tests[1];
   if (err) return fail(JSV_ERR_CAPACITY, "stage-1 candidate capacity exceeded (code " +
@@ -927,7 +951,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   for (int i = 0; i < n; ++i)
     for (int k = 0; k < T; ++k) {
       const int t = p.topo[k];
-      if (bs.pool_n[(size_t)i * T + t] == 0 && !((probes[i].could_zero >> t) & 1u)) {
+      if (bs.pool_n[(size_t)i * T + t] == 0 && !((bs.probes[i].could_zero >> t) & 1u)) {
         bs.dead[i] = 1;
         break;
       }
@@ -1420,6 +1444,138 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   return JSV_OK;
 }
 
+// Exhaustive Stage 2 planned on the device (k_x_plan): issued right behind Stage 1
+// with no host round trip; the caller synchronises once and reads which probes the
+// sweep took (`handled`) and which feasibility scans were truncated.  Returns with
+// `issued` false when the batch needs the host-planned path (run_exhaustive).
+struct DevExh {
+  bool issued = false;
+  int* handled_h = nullptr;  // pinned readbacks (valid after the caller's sync)
+  int* trunc_h = nullptr;
+  long long* totals_h = nullptr;
+};
+
+static int run_exhaustive_dev(jsv_problem& p, BatchState& bs, bool want_config, DevExh& dx) {
+  jsv_context& c = *p.ctx;
+  dx.issued = false;
+  // (opt-in, JSV_DEVICE_PLAN=1: measured 2% slower than the host-planned path on the
+  // 64-solve batch -- k_x_plan's single block and the grid-stride k_x_live cost more
+  // than the host round trip they remove -- and no faster for one solve)
+  if (c.strategy == JSV_STRATEGY_SEARCH || !getenv("JSV_DEVICE_PLAN")) return JSV_OK;
+  long long fo_budget = 0;
+  if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) {
+    if (c.shard_world > 1 || getenv("JSV_NO_FEAS_SWEEP")) return JSV_OK;
+    fo_budget = 1LL << 20;
+    if (const char* e = getenv("JSV_FEAS_BUDGET")) fo_budget = std::max(1LL, atoll(e));
+  }
+  const int n = bs.n, T = p.T;
+  const int W = bs.s1.W;
+  if (W > 512 || p.P > 4 || bs.s1.S >= 0x7FFF) return JSV_OK;  // (host path: looped sweeps)
+  // live-list capacity bound: per probe min(exh_limit, (W + 1)^(T - 1)) prefixes
+  long long per = 1;
+  for (int k = 0; k < T - 1 && per <= c.exh_limit; ++k) per *= (long long)(W + 1);
+  per = std::min(per, c.exh_limit);
+  if (fo_budget > 0) per = std::min(per, fo_budget);
+  const long long live_cap = per * n;
+  if (live_cap > (64LL << 20)) return JSV_OK;  // > 256 MB of live lists: host-planned path
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(bs.probes[i].slo_eff) || !std::isfinite(bs.probes[i].demand)) return JSV_OK;
+  if (!p.lat_fast) return JSV_OK;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  const int n_slots = x_slots(p.P);
+  const long long max_rounds = (live_cap + n_slots - 1) / n_slots + n;
+  CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
+  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
+  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
+  CK(B[B_XLIVE].ensure(sizeof(unsigned) * (size_t)live_cap));
+  CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)max_rounds));
+  // [uoff n+1][roff n+1][work 1][totals 4][live_cnt n][handled n][trunc n][xr_done n]
+  const size_t ll = (size_t)(2 * (n + 1) + 1 + 4);
+  CK(B[B_XBOFF].ensure(sizeof(long long) * ll + sizeof(int) * 4 * (size_t)n));
+  long long* L = B[B_XBOFF].as<long long>();
+  int* I = reinterpret_cast<int*>(L + ll);
+  CK(cudaMemsetAsync(L + (n + 1), 0, sizeof(long long) * (n + 2 + 4) + sizeof(int) * 4 * n, st));
+  XArgs a;
+  memset(&a, 0, sizeof(a));
+  s2_base(p, bs, a.s);
+  a.s.active = B[B_ACTIVE].as<int>();
+  const bool fonly = bs.feasible_only != 0;
+  a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
+  a.xp = B[B_XPROBE].as<XProbe>();
+  a.fast = 1;
+  {
+    const int tl = p.topo[T - 1];
+    double mx = 0.0;
+    for (int k = p.key_off[tl]; k < p.key_off[tl + 1]; ++k) mx = std::max(mx, p.key_lat[k]);
+    a.lat2_max = 2.0 * mx;
+  }
+  a.max_pn_last = W;
+  a.rpl = 1;
+  a.prune = getenv("JSV_NO_PRUNE") ? 0 : 1;
+  if (a.mode == LEAF_FULL) {
+    a.mkey = (T <= 5 && (long long)W * bs.s1.maxi <= 4096 && !getenv("JSV_NO_MKEY")) ? 1 : 0;
+    if (a.mkey) {
+      CK(B[B_MRANK].ensure(sizeof(uint32_t) * ((size_t)n * T * W + (size_t)n * T)));
+      a.s.mkey = B[B_MRANK].as<uint32_t>();
+      a.s.mnone = B[B_MRANK].as<uint32_t>() + (size_t)n * T * W;
+    } else {
+      CK(B[B_MRANK].ensure(sizeof(uint32_t) * (size_t)n * T * W));
+      a.s.mrank = B[B_MRANK].as<uint32_t>();
+    }
+  }
+  CK(B[B_XSACC].ensure(sizeof(double) * (size_t)n * W));
+  CK(B[B_XSCAP].ensure(sizeof(double) * (size_t)n * W));
+  CK(B[B_XSLAT].ensure(sizeof(double) * (size_t)n * W));
+  CK(B[B_XRANK].ensure(sizeof(uint4) * (size_t)n * W));
+  CK(B[B_XPACK].ensure(sizeof(uint2) * (size_t)n * W));
+  a.xpack = B[B_XPACK].as<uint2>();
+  a.sacc = B[B_XSACC].as<double>();
+  a.scap = B[B_XSCAP].as<double>();
+  a.slat2 = B[B_XSLAT].as<double>();
+  a.xrank = B[B_XRANK].as<uint4>();
+  a.uoff = L;
+  a.roff = L + (n + 1);
+  a.roff_w = L + (n + 1);
+  a.work = reinterpret_cast<unsigned long long*>(L + 2 * (n + 1));
+  long long* totals = L + 2 * (n + 1) + 1;
+  a.dev_totals = totals;
+  a.live_cnt = I;
+  a.live = B[B_XLIVE].as<unsigned>();
+  a.xr_done = I + 3 * n;
+  a.part = B[B_XPART].as<XPart>();
+  XPlanArgs pa{};
+  pa.exh_limit = c.exh_limit;
+  pa.fo_budget = fo_budget;
+  pa.live_cap = live_cap;
+  pa.shard_rank = c.shard_rank;
+  pa.shard_world = c.shard_world;
+  pa.reg = 1;
+  pa.xp = B[B_XPROBE].as<XProbe>();
+  pa.handled = I + n;
+  pa.trunc = I + 2 * n;
+  pa.uoff = L;
+  pa.totals = totals;
+  pa.err = B[B_ERR].as<int>();
+  c.stats.kernel_launches += launch_x_plan(a, pa, st);
+  const size_t smem = x_smem_bytes(W, p.P, true);
+  const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
+  c.stats.kernel_launches +=
+      launch_stage2_exhaustive(a, G, p.P, smem, st, getenv("JSV_NO_SIDE") ? st : c.st2, c.fork,
+                               c.join, -1);
+  CK(cudaGetLastError());
+  // readbacks for the caller's sync: handled / truncated flags and the totals
+  char* h = static_cast<char*>(c.pinned(sizeof(long long) * 4 + sizeof(int) * 2 * (size_t)n, 1));
+  if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+  dx.totals_h = reinterpret_cast<long long*>(h);
+  dx.handled_h = reinterpret_cast<int*>(h + sizeof(long long) * 4);
+  dx.trunc_h = dx.handled_h + n;
+  CK(cudaMemcpyAsync(dx.totals_h, totals, sizeof(long long) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(dx.handled_h, I + n, sizeof(int) * 2 * (size_t)n, cudaMemcpyDeviceToHost, st));
+  dx.issued = true;
+  return JSV_OK;
+}
+
 // Fan-out graphs (one entry, every other task a leaf fed only by it) whose
 // cross-product is too large to sweep: knapsack-DP bounded enumeration of the
 // near-optimal class vectors + exact evaluation (jsv_fanout.cuh).  Full plans
@@ -1622,8 +1778,32 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     if (rc) return rc;
     JSV_T("s2 prep issued");
     std::vector<int> active(n, 1);
-    rc = run_exhaustive(p, bs, want_config, active);
+    DevExh dx;
+    rc = run_exhaustive_dev(p, bs, want_config, dx);
     if (rc) return rc;
+    CK(cudaStreamSynchronize(st));
+    rc = stage1_collect(p, bs);
+    if (rc) return rc;
+    if (dx.issued) {
+      JSV_T("device-planned exhaustive synced");
+      int err = 0;
+      CK(cudaMemcpy(&err, c.buf[B_ERR].p, sizeof(int), cudaMemcpyDeviceToHost));
+      if (err) return fail(JSV_ERR_CAPACITY, "exhaustive live-list capacity exceeded");
+      c.stats.exh_candidates += dx.totals_h[2];
+      c.stats.exh_probes += (int)dx.totals_h[3];
+      std::vector<BestRec> best0;
+      bool any_trunc = false;
+      for (int i = 0; i < n; ++i) any_trunc = any_trunc || dx.trunc_h[i];
+      if (any_trunc) {
+        best0.resize(n);
+        CK(cudaMemcpy(best0.data(), c.buf[B_BEST].p, sizeof(BestRec) * n, cudaMemcpyDeviceToHost));
+      }
+      for (int i = 0; i < n; ++i)
+        active[i] = !dx.handled_h[i] || (dx.trunc_h[i] && !best0[i].has);
+    } else {
+      rc = run_exhaustive(p, bs, want_config, active);
+      if (rc) return rc;
+    }
     JSV_T("exhaustive issued");
     rc = run_fanout(p, bs, active, want_config);
     if (rc) return rc;
@@ -1685,6 +1865,11 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     }
   }
   JSV_T("stage2 done");
+  if (bs.s1_pending) {  // (uninformed plans: no Stage-2 synchronisation happened)
+    CK(cudaStreamSynchronize(st));
+    rc = stage1_collect(p, bs);
+    if (rc) return rc;
+  }
   CK(cudaEventRecord(c.ev[2], st));
   rc = finalize(p, bs, !informed, out, &nodes);
   if (rc) return rc;
@@ -2194,6 +2379,9 @@ extern "C" int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const js
   bs.probes.resize(1);
   fill_probe(p, *req, *probe, bs.probes[0]);
   int rc = run_stage1(p, *req, 1, bs.probes.data(), bs, 1, std::vector<int>{0});
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(ctx->st));
+  rc = stage1_collect(p, bs);
   if (rc) return rc;
   const S1Args& a = bs.s1;
   const int P = bs.pool_n[task];

@@ -938,7 +938,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
 // so it is decided here; the others (every leaf prefix when pruning is off) are
 // appended to the probe's live list for the full derivation + sweep (k_s2_exh).
 // BestRec.leaves ends equal to the probe's whole cross-product of leaves.
-__global__ void __launch_bounds__(256) k_x_live(const __grid_constant__ XArgs a, long long total) {
+__global__ void __launch_bounds__(256) k_x_live(const __grid_constant__ XArgs a, long long total_arg) {
   __shared__ __align__(16) DGraph s_g;
   const S2Args& s = a.s;
   {
@@ -953,6 +953,8 @@ __global__ void __launch_bounds__(256) k_x_live(const __grid_constant__ XArgs a,
   const int lane = threadIdx.x & 31;
   const long long n_warps = (long long)gridDim.x * (blockDim.x >> 5);
   const double sf = 1.0 + rq.slack;
+  // (device-planned batches: the number of upper prefixes comes from k_x_plan)
+  const long long total = a.dev_totals ? a.dev_totals[0] : total_arg;
   for (long long wu = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); wu < total;
        wu += n_warps) {
     const int probe = find_probe(a.uoff, s.n_probes, wu);
@@ -1129,6 +1131,106 @@ __global__ void __launch_bounds__(256) k_x_live(const __grid_constant__ XArgs a,
     for (int dd = 16; dd > 0; dd >>= 1) lv += __shfl_down_sync(0xffffffffu, lv, dd);
     if (lane == 0 && lv) atomicAdd(&s.best[probe].leaves, lv);
   }
+}
+
+// XProbe of every probe from its Stage-1 pool sizes (one block): the radices
+// (pool + "no instances" where demand may be 0), the cross-product (swept when <=
+// exh_limit and no task is dead), this shard's prefix block, the feasibility
+// truncation, the upper-prefix and live-list offsets (block scans).
+__global__ void __launch_bounds__(1024) k_x_plan(const __grid_constant__ XArgs a,
+                                                 const __grid_constant__ XPlanArgs pa) {
+  typedef cub::BlockScan<long long, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ long long c_up, c_nq, c_cand, c_nx;
+  const S2Args& s = a.s;
+  const DGraph& g = *s.g;
+  const int n = s.n_probes, T = s.T;
+  if (threadIdx.x == 0) c_up = c_nq = c_cand = c_nx = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += 1024) {
+    const int i = i0 + threadIdx.x;
+    long long nup = 0, nq = 0, cand = 0;
+    XProbe x;
+    memset(&x, 0, sizeof(x));
+    int handled = 0, trunc = 0;
+    if (i < n) {
+      const DProbe& pr = s.probes[i];
+      unsigned __int128 N = 1;
+      bool over = false, dead = false;
+      for (int k = 0; k < T; ++k) {
+        const int t = g.topo[k];
+        x.pn[k] = s.pool_n[i * T + t];
+        const int cz = (int)((pr.could_zero >> t) & 1u);
+        if (x.pn[k] == 0 && !cz) dead = true;
+        x.radix[k] = x.pn[k] + cz;
+        if (!over) N *= (unsigned)x.radix[k];
+        if (N > (unsigned __int128)pa.exh_limit) over = true;
+      }
+      if (!dead && !over && N != 0) {
+        x.R = x.radix[T - 1];
+        const long long Q = (long long)(N / (unsigned)x.R);
+        x.q0 = (long long)((__int128)Q * pa.shard_rank / pa.shard_world);
+        const long long q1 = (long long)((__int128)Q * (pa.shard_rank + 1) / pa.shard_world);
+        x.nq = q1 - x.q0;
+        if (pa.fo_budget > 0) {
+          const long long cap = max(1LL, pa.fo_budget / x.R);
+          if (x.nq > cap) {
+            x.nq = cap;
+            trunc = 1;
+          }
+        }
+        int glog = 0;
+        while ((1 << glog) < x.R && glog < 5) ++glog;
+        x.glog = glog;
+        x.rounds = 1;
+        x.rpl = pa.reg ? (x.pn[T - 1] + 31) / 32 : 0;
+        handled = 1;
+        nq = x.nq;
+        cand = x.nq * x.R;
+        if (nq > 0) {
+          const long long Rl = T >= 2 ? x.radix[T - 2] : 1;
+          nup = (x.q0 + x.nq - 1) / Rl - x.q0 / Rl + 1;
+        }
+      }
+    }
+    long long up_off, up_tot, nq_off, nq_tot;
+    Scan(tmp).ExclusiveSum(nup, up_off, up_tot);
+    __syncthreads();
+    Scan(tmp).ExclusiveSum(nq, nq_off, nq_tot);
+    if (i < n) {
+      x.loff = c_nq + nq_off;
+      pa.xp[i] = x;
+      pa.handled[i] = handled;
+      pa.trunc[i] = trunc;
+      pa.uoff[i] = c_up + up_off;
+    }
+    long long cs = cand;
+    for (int d = 16; d > 0; d >>= 1) cs += __shfl_down_sync(0xffffffffu, cs, d);
+    const unsigned hb = __ballot_sync(0xffffffffu, handled != 0);
+    if ((threadIdx.x & 31) == 0) {
+      atomicAdd((unsigned long long*)&c_cand, (unsigned long long)cs);
+      atomicAdd((unsigned long long*)&c_nx, (unsigned long long)__popc(hb));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      c_up += up_tot;
+      c_nq += nq_tot;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    pa.uoff[n] = c_up;
+    pa.totals[0] = c_up;
+    pa.totals[1] = c_nq;
+    pa.totals[2] = c_cand;
+    pa.totals[3] = c_nx;
+    if (c_nq > pa.live_cap) atomicExch(pa.err, 4);
+  }
+}
+
+int launch_x_plan(const XArgs& a, const XPlanArgs& pa, cudaStream_t st) {
+  k_x_plan<<<1, 1024, 0, st>>>(a, pa);
+  return 1;
 }
 
 // Round offsets of the live lists (rounds of x_slots(P) prefixes): roff[i] =
@@ -1587,9 +1689,10 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
   }
   cudaEventRecord(join, st2);
   PROF_BEGIN(K_X_LIVE);
-  if (n_upper > 0) {
-    // one warp per upper prefix
-    const long long blocks = std::min<long long>((n_upper + 7) / 8, 148LL * 8);
+  if (n_upper != 0) {
+    // one warp per upper prefix (n_upper < 0: counted on the device, grid-stride)
+    const long long blocks =
+        n_upper > 0 ? std::min<long long>((n_upper + 7) / 8, 148LL * 8) : 148LL * 8;
     k_x_live<<<(unsigned)blocks, 256, 0, st>>>(a, n_upper);
     ++launches;
   }

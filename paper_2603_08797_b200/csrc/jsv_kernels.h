@@ -281,7 +281,25 @@ struct XArgs {
   long long* roff_w;      // = roff, written by k_x_sched
   int mkey;               // full plans, T <= 5: m tie-breaks compare packed 55-bit keys
   int* xr_done;           // [n_probes] column blocks of k_x_rank finished
+  const long long* dev_totals;  // device-planned batches (k_x_plan): [0] upper prefixes
 };
+
+// k_x_plan: XProbe construction on the device (no host round trip between Stage 1
+// and the exhaustive Stage 2)
+struct XPlanArgs {
+  long long exh_limit;   // largest cross-product swept
+  long long fo_budget;   // feasibility probes: candidates scanned from the front (0: all)
+  long long live_cap;    // capacity of the live lists (entries)
+  int shard_rank, shard_world;
+  int reg;               // register sweep (XProbe::rpl)
+  XProbe* xp;            // [n] out
+  int* handled;          // [n] out: probe taken by the exhaustive sweep
+  int* trunc;            // [n] out: feasibility scan truncated to fo_budget
+  long long* uoff;       // [n + 1] out: first upper prefix of each probe
+  long long* totals;     // [4] out: upper prefixes, live capacity used, candidates, probes
+  int* err;              // capacity exceeded -> 4
+};
+int launch_x_plan(const XArgs& a, const XPlanArgs& pa, cudaStream_t st);
 // rounds per chunk of the exhaustive kernel's persistent blocks
 #define X_CHUNK 8
 

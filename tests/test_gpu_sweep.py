@@ -81,3 +81,18 @@ def test_c3_grid_probe_paths_agree(grid, env, monkeypatch):
     for d, r in zip(docs[::4], res):
         assert (r.demand_rps, r.probes) == (d["demand"], d["probes"]), d["name"]
         assert result_dict(r.plan) == d["plan"], d["name"]
+
+
+def test_c3_grid_device_planned(grid, monkeypatch):
+    """The configs[2] grid with the exhaustive Stage 2 planned on the device
+    (JSV_DEVICE_PLAN: k_x_plan, no host round trip between the stages), budgeted
+    feasibility scans included."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    monkeypatch.setenv("JSV_DEVICE_PLAN", "1")
+    docs, apps, table = grid
+    res = P.max_demand_grid(apps, table, 28, SearchSpace(True, True, True), 0.05, None, 1e-3)
+    for d, r in zip(docs, res):
+        assert (r.demand_rps, r.probes) == (d["demand"], d["probes"]), d["name"]
+        assert result_dict(r.plan) == d["plan"], d["name"]
