@@ -991,13 +991,216 @@ static void s2_base(jsv_problem& p, BatchState& bs, S2Args& a) {
 }
 
 // Level-synchronous search over the active probes (T-informed plans).
+//
+// Frontier memory is bounded: when a level's children (an upper bound: every
+// bundle passing the slices trim of every live prefix) would exceed
+// JSV_BB_MAX_SLOTS (default 2^25), the level's frontier is split in two halves per
+// probe and each half is expanded depth-first on its own (recursively, so deeper
+// levels split the same way).  Every filter is admissible and the per-probe
+// incumbent, kill counts, deepest blocked level and best leaf persist across the
+// chunks (k_s2_reduce merges), so the result does not depend on the chunking.
+struct BBState {
+  jsv_problem* p;
+  BatchState* bs;
+  S2Args a;
+  bool diag;
+  long long max_slots;
+  long long nodes = 0;
+  std::vector<long long>* nodes_out;
+  std::vector<std::unique_ptr<DevBuf>> lvl_fr, lvl_cnt;  // per-level frontier / live-count caches
+};
+
+static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vector<long long>& foff,
+                    const std::vector<long long>& fcap) {
+  jsv_problem& p = *S.p;
+  BatchState& bs = *S.bs;
+  jsv_context& c = *p.ctx;
+  cudaStream_t st = c.st;
+  auto& B = c.buf;
+  S2Args& a = S.a;
+  const int n = bs.n, T = p.T, P = p.P;
+  const bool diag = S.diag;
+  long long n_slots = 0;
+  for (int i = 0; i < n; ++i) n_slots = std::max(n_slots, foff[i] + fcap[i]);
+  std::vector<long long> pstart(n), nxt_off(n), nxt_cap(n), boff(n + 1);
+  std::vector<unsigned long long> ptot(n), fcnt(n);
+  JSV_T("s2 level begin");
+  if (timing_on()) fprintf(stderr, "[jsv t] level %d slots %lld\n", L, n_slots);
+  const bool last = (L == T - 1);
+  const size_t S1 = (size_t)std::max<long long>(1, n_slots);
+  CK(B[B_FOFF].ensure(sizeof(long long) * n));
+  CK(B[B_FCAP].ensure(sizeof(long long) * n));
+  CK(cudaMemcpyAsync(B[B_FOFF].p, foff.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(B[B_FCAP].p, fcap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+  CK(B[B_PWIDTH].ensure(sizeof(long long) * (S1 + 1)));
+  CK(B[B_PFLAG].ensure(sizeof(int) * S1));
+  CK(B[B_PPROBE].ensure(sizeof(int) * S1));
+  CK(B[B_PR].ensure(sizeof(double) * S1));
+  CK(B[B_PUSED].ensure(sizeof(int) * S1));
+  CK(B[B_PLATS].ensure(sizeof(double) * S1 * P));
+  CK(B[B_PACCS].ensure(sizeof(double) * S1 * P));
+  CK(B[B_PTOT].ensure(sizeof(unsigned long long) * n));
+  CK(B[B_PFX].ensure(sizeof(long long) * (S1 + 1)));
+  CK(cudaMemsetAsync(B[B_PTOT].p, 0, sizeof(unsigned long long) * n, st));
+  if (diag) {
+    CK(B[B_FLAGS].ensure(sizeof(int) * S1));
+    CK(cudaMemsetAsync(B[B_FLAGS].p, 0, sizeof(int) * S1, st));
+  }
+  a.level = L;
+  a.last = last ? 1 : 0;
+  a.n_slots = n_slots;
+  a.foff = B[B_FOFF].as<long long>();
+  a.fcap = B[B_FCAP].as<long long>();
+  a.fcnt = ccnt->as<unsigned long long>();
+  a.cur = cur->as<uint16_t>();
+  a.cur_flag = B[B_FLAGS].as<int>();
+  a.pr_width = B[B_PWIDTH].as<long long>();
+  a.pr_flag = B[B_PFLAG].as<int>();
+  a.pr_probe = B[B_PPROBE].as<int>();
+  a.pr_r = B[B_PR].as<double>();
+  a.pr_used = B[B_PUSED].as<int>();
+  a.pr_lat = B[B_PLATS].as<double>();
+  a.pr_acc = B[B_PACCS].as<double>();
+  a.ptot = B[B_PTOT].as<unsigned long long>();
+  a.pfx = B[B_PFX].as<long long>();
+  // (the scan's extra input slot n_slots: width 0)
+  CK(cudaMemsetAsync(a.pr_width + n_slots, 0, sizeof(long long), st));
+  c.stats.kernel_launches += launch_stage2_prefix(a, st);
+  CK(cudaGetLastError());
+  // exclusive scan of the per-slot widths (width 0 beyond the live prefixes)
+  {
+    size_t tmp = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, a.pr_width, a.pfx, n_slots + 1, st));
+    CK(B[B_SCAN].ensure(tmp));
+    CK(cub::DeviceScan::ExclusiveSum(B[B_SCAN].p, tmp, a.pr_width, a.pfx, n_slots + 1, st));
+  }
+  CK(cudaMemcpyAsync(ptot.data(), a.ptot, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(fcnt.data(), a.fcnt, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  long long total = 0;
+  for (int i = 0; i < n; ++i) {
+    fcnt[i] = std::min<unsigned long long>(fcnt[i], (unsigned long long)fcap[i]);
+    pstart[i] = total;
+    total += (long long)ptot[i];
+  }
+  // ---- split: the children would not fit -> two halves of every probe's frontier
+  if (!last && total > S.max_slots) {
+    bool can = false;
+    for (int i = 0; i < n; ++i) can = can || fcnt[i] >= 2;
+    if (can) {
+      if (timing_on()) fprintf(stderr, "[jsv t] level %d split (%lld children)\n", L, total);
+      for (int half = 0; half < 2; ++half) {
+        std::vector<long long> hoff(n), hcap(n);
+        std::vector<unsigned long long> hcnt(n);
+        long long rows = 0;
+        for (int i = 0; i < n; ++i) {
+          const long long m = (long long)fcnt[i], h = (m + 1) / 2;
+          const long long lo = half ? h : 0, hi = half ? m : (m >= 2 ? h : m);
+          hoff[i] = rows;
+          hcap[i] = hi - lo;
+          hcnt[i] = (unsigned long long)(hi - lo);
+          rows += hi - lo;
+        }
+        auto fr = std::make_unique<DevBuf>();
+        auto cn = std::make_unique<DevBuf>();
+        CK(fr->ensure(sizeof(uint16_t) * std::max<long long>(1, rows) * T));
+        CK(cn->ensure(sizeof(unsigned long long) * n));
+        for (int i = 0; i < n; ++i) {
+          const long long m = (long long)fcnt[i], h = (m + 1) / 2;
+          const long long lo = half ? h : 0;
+          if (hcap[i] > 0)
+            CK(cudaMemcpyAsync(fr->as<uint16_t>() + hoff[i] * T, cur->as<uint16_t>() + (foff[i] + lo) * T,
+                               sizeof(uint16_t) * hcap[i] * T, cudaMemcpyDeviceToDevice, st));
+        }
+        CK(cudaMemcpyAsync(cn->p, hcnt.data(), sizeof(unsigned long long) * n, cudaMemcpyHostToDevice, st));
+        int rc = bb_level(S, L, fr.get(), cn.get(), hoff, hcap);
+        if (rc) return rc;
+        CK(cudaStreamSynchronize(st));  // (before the halves' buffers are freed)
+      }
+      return JSV_OK;
+    }
+  }
+  for (int i = 0; i < n; ++i) {
+    S.nodes += (long long)fcnt[i];
+    if (S.nodes_out) (*S.nodes_out)[i] += (long long)fcnt[i];  // frontier prefixes of probe i
+  }
+  if (last && !diag) c.stats.leaf_work += total;
+  DevBuf* nxt = nullptr;
+  DevBuf* ncnt = nullptr;
+  std::vector<long long> noff(n), ncap(n);
+  if (total > 0) {
+    CK(B[B_PSTART].ensure(sizeof(long long) * n));
+    CK(cudaMemcpyAsync(B[B_PSTART].p, pstart.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+    a.pstart = B[B_PSTART].as<long long>();
+    if (last) {
+      long long nb = 0;
+      const long long per_block = 256LL * a.ipt;
+      for (int i = 0; i < n; ++i) {
+        boff[i] = nb;
+        nb += ((long long)ptot[i] + per_block - 1) / per_block;
+      }
+      boff[n] = nb;
+      CK(B[B_BOFF].ensure(sizeof(long long) * (n + 1)));
+      CK(cudaMemcpyAsync(B[B_BOFF].p, boff.data(), sizeof(long long) * (n + 1), cudaMemcpyHostToDevice,
+                         st));
+      CK(B[B_PART].ensure(sizeof(LeafPart) * std::max<long long>(1, nb)));
+      a.boff = B[B_BOFF].as<long long>();
+      a.part = B[B_PART].as<LeafPart>();
+      c.stats.kernel_launches += launch_stage2_leaf(a, nb, st);
+    } else {
+      long long NO = 0;
+      for (int i = 0; i < n; ++i) {
+        nxt_off[i] = NO;
+        nxt_cap[i] = (long long)ptot[i];
+        NO += nxt_cap[i];
+      }
+      if ((int)S.lvl_fr.size() <= L + 1) {
+        S.lvl_fr.resize(L + 2);
+        S.lvl_cnt.resize(L + 2);
+      }
+      if (!S.lvl_fr[L + 1]) {
+        S.lvl_fr[L + 1] = std::make_unique<DevBuf>();
+        S.lvl_cnt[L + 1] = std::make_unique<DevBuf>();
+      }
+      nxt = S.lvl_fr[L + 1].get();
+      ncnt = S.lvl_cnt[L + 1].get();
+      CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
+      CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
+      CK(ncnt->ensure(sizeof(unsigned long long) * n));
+      CK(cudaMemcpyAsync(B[B_NXTOFF].p, nxt_off.data(), sizeof(long long) * n, cudaMemcpyHostToDevice,
+                         st));
+      CK(cudaMemcpyAsync(B[B_NXTCAP].p, nxt_cap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice,
+                         st));
+      CK(cudaMemsetAsync(ncnt->p, 0, sizeof(unsigned long long) * n, st));
+      CK(nxt->ensure(sizeof(uint16_t) * std::max<long long>(1, NO) * T));
+      a.nxt = nxt->as<uint16_t>();
+      a.nxt_cnt = ncnt->as<unsigned long long>();
+      a.nxt_off = B[B_NXTOFF].as<long long>();
+      a.nxt_cap = B[B_NXTCAP].as<long long>();
+      c.stats.kernel_launches += launch_stage2_level(a, total, st);
+    }
+    CK(cudaGetLastError());
+  }
+  if (diag) c.stats.kernel_launches += launch_stage2_blocked(a, st);
+  if (last || total == 0) return JSV_OK;
+  // next frontier: slots [nxt_off, nxt_off + nxt_cap) per probe, live counts on the device
+  return bb_level(S, L + 1, nxt, ncnt, nxt_off, nxt_cap);
+}
+
 static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_config,
                       const std::vector<int>& active, std::vector<long long>* nodes_out) {
   jsv_context& c = *p.ctx;
   cudaStream_t st = c.st;
   auto& B = c.buf;
-  const int n = bs.n, T = p.T, P = p.P;
-  S2Args a;
+  const int n = bs.n, T = p.T;
+  BBState S;
+  S.p = &p;
+  S.bs = &bs;
+  S.diag = diag;
+  S.nodes_out = nodes_out;
+  S.max_slots = 1LL << 25;
+  if (const char* e = getenv("JSV_BB_MAX_SLOTS")) S.max_slots = std::max(1LL, atoll(e));
+  S2Args& a = S.a;
   s2_base(p, bs, a);
   a.diag = diag ? 1 : 0;
   a.want_config = want_config ? 1 : 0;
@@ -1012,148 +1215,24 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   a.inc = B[B_INC].as<unsigned long long>();
   a.active = B[B_ACTIVE].as<int>();
   // level-0 frontier: one empty prefix per active probe
-  std::vector<long long> foff(n), fcap(n, 1), pstart(n), nxt_off(n), nxt_cap(n), boff(n + 1);
-  std::vector<unsigned long long> cnt0(n), ptot(n), fcnt(n);
+  std::vector<long long> foff(n), fcap(n, 1);
+  std::vector<unsigned long long> cnt0(n);
   for (int i = 0; i < n; ++i) {
     foff[i] = i;
     cnt0[i] = (active[i] && !bs.dead[i]) ? 1 : 0;
   }
-  long long n_slots = n;
   CK(B[B_FR0].ensure(sizeof(uint16_t) * n * T));
   CK(cudaMemsetAsync(B[B_FR0].p, 0xFF, sizeof(uint16_t) * n * T, st));
   CK(B[B_CNT2].ensure(sizeof(unsigned long long) * n));
   CK(cudaMemcpyAsync(B[B_CNT2].p, cnt0.data(), sizeof(unsigned long long) * n,
                      cudaMemcpyHostToDevice, st));
-  DevBuf* cur = &B[B_FR0];
-  DevBuf* nxt = &B[B_FR1];
-  DevBuf* ccnt = &B[B_CNT2];     // live counts of the current frontier
-  DevBuf* ncnt = &B[B_NXTCNT];   // counts of the next frontier
-  long long nodes = 0;
-  for (int L = 0; L < T; ++L) {
-    JSV_T("s2 level begin");
-    if (timing_on()) fprintf(stderr, "[jsv t] level %d slots %lld\n", L, n_slots);
-    const bool last = (L == T - 1);
-    const size_t S1 = (size_t)std::max<long long>(1, n_slots);
-    CK(B[B_FOFF].ensure(sizeof(long long) * n));
-    CK(B[B_FCAP].ensure(sizeof(long long) * n));
-    CK(cudaMemcpyAsync(B[B_FOFF].p, foff.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(B[B_FCAP].p, fcap.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
-    CK(B[B_PWIDTH].ensure(sizeof(long long) * (S1 + 1)));
-    CK(B[B_PFLAG].ensure(sizeof(int) * S1));
-    CK(B[B_PPROBE].ensure(sizeof(int) * S1));
-    CK(B[B_PR].ensure(sizeof(double) * S1));
-    CK(B[B_PUSED].ensure(sizeof(int) * S1));
-    CK(B[B_PLATS].ensure(sizeof(double) * S1 * P));
-    CK(B[B_PACCS].ensure(sizeof(double) * S1 * P));
-    CK(B[B_PTOT].ensure(sizeof(unsigned long long) * n));
-    CK(B[B_PFX].ensure(sizeof(long long) * (S1 + 1)));
-    CK(cudaMemsetAsync(B[B_PTOT].p, 0, sizeof(unsigned long long) * n, st));
-    if (diag) {
-      CK(B[B_FLAGS].ensure(sizeof(int) * S1));
-      CK(cudaMemsetAsync(B[B_FLAGS].p, 0, sizeof(int) * S1, st));
-    }
-    a.level = L;
-    a.last = last ? 1 : 0;
-    a.n_slots = n_slots;
-    a.foff = B[B_FOFF].as<long long>();
-    a.fcap = B[B_FCAP].as<long long>();
-    a.fcnt = ccnt->as<unsigned long long>();
-    a.cur = cur->as<uint16_t>();
-    a.cur_flag = B[B_FLAGS].as<int>();
-    a.pr_width = B[B_PWIDTH].as<long long>();
-    a.pr_flag = B[B_PFLAG].as<int>();
-    a.pr_probe = B[B_PPROBE].as<int>();
-    a.pr_r = B[B_PR].as<double>();
-    a.pr_used = B[B_PUSED].as<int>();
-    a.pr_lat = B[B_PLATS].as<double>();
-    a.pr_acc = B[B_PACCS].as<double>();
-    a.ptot = B[B_PTOT].as<unsigned long long>();
-    a.pfx = B[B_PFX].as<long long>();
-    // (the scan's extra input slot n_slots: width 0)
-    CK(cudaMemsetAsync(a.pr_width + n_slots, 0, sizeof(long long), st));
-    c.stats.kernel_launches += launch_stage2_prefix(a, st);
-    CK(cudaGetLastError());
-    // exclusive scan of the per-slot widths (width 0 beyond the live prefixes)
-    {
-      size_t tmp = 0;
-      CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, a.pr_width, a.pfx, n_slots + 1, st));
-      CK(B[B_SCAN].ensure(tmp));
-      CK(cub::DeviceScan::ExclusiveSum(B[B_SCAN].p, tmp, a.pr_width, a.pfx, n_slots + 1, st));
-    }
-    CK(cudaMemcpyAsync(ptot.data(), a.ptot, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
-                       st));
-    CK(cudaMemcpyAsync(fcnt.data(), a.fcnt, sizeof(unsigned long long) * n, cudaMemcpyDeviceToHost,
-                       st));
-    CK(cudaStreamSynchronize(st));
-    long long total = 0;
-    for (int i = 0; i < n; ++i) {
-      pstart[i] = total;
-      total += (long long)ptot[i];
-      nodes += (long long)fcnt[i];
-      if (nodes_out) (*nodes_out)[i] += (long long)fcnt[i];  // frontier prefixes of probe i
-    }
-    if (last && !diag) c.stats.leaf_work += total;
-    if (total > 0) {
-      CK(B[B_PSTART].ensure(sizeof(long long) * n));
-      CK(cudaMemcpyAsync(B[B_PSTART].p, pstart.data(), sizeof(long long) * n,
-                         cudaMemcpyHostToDevice, st));
-      a.pstart = B[B_PSTART].as<long long>();
-      if (last) {
-        long long nb = 0;
-        const long long per_block = 256LL * a.ipt;
-        for (int i = 0; i < n; ++i) {
-          boff[i] = nb;
-          nb += ((long long)ptot[i] + per_block - 1) / per_block;
-        }
-        boff[n] = nb;
-        CK(B[B_BOFF].ensure(sizeof(long long) * (n + 1)));
-        CK(cudaMemcpyAsync(B[B_BOFF].p, boff.data(), sizeof(long long) * (n + 1),
-                           cudaMemcpyHostToDevice, st));
-        CK(B[B_PART].ensure(sizeof(LeafPart) * std::max<long long>(1, nb)));
-        a.boff = B[B_BOFF].as<long long>();
-        a.part = B[B_PART].as<LeafPart>();
-        c.stats.kernel_launches += launch_stage2_leaf(a, nb, st);
-      } else {
-        long long NO = 0;
-        for (int i = 0; i < n; ++i) {
-          nxt_off[i] = NO;
-          nxt_cap[i] = (long long)ptot[i];
-          NO += nxt_cap[i];
-        }
-        CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
-        CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
-        CK(ncnt->ensure(sizeof(unsigned long long) * n));
-        CK(cudaMemcpyAsync(B[B_NXTOFF].p, nxt_off.data(), sizeof(long long) * n,
-                           cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(B[B_NXTCAP].p, nxt_cap.data(), sizeof(long long) * n,
-                           cudaMemcpyHostToDevice, st));
-        CK(cudaMemsetAsync(ncnt->p, 0, sizeof(unsigned long long) * n, st));
-        CK(nxt->ensure(sizeof(uint16_t) * std::max<long long>(1, NO) * T));
-        a.nxt = nxt->as<uint16_t>();
-        a.nxt_cnt = ncnt->as<unsigned long long>();
-        a.nxt_off = B[B_NXTOFF].as<long long>();
-        a.nxt_cap = B[B_NXTCAP].as<long long>();
-        c.stats.kernel_launches += launch_stage2_level(a, total, st);
-      }
-      CK(cudaGetLastError());
-    }
-    if (diag) c.stats.kernel_launches += launch_stage2_blocked(a, st);
-    if (last || total == 0) break;
-    // next frontier: slots [nxt_off, nxt_off + nxt_cap) per probe, live counts on the device
-    n_slots = 0;
-    for (int i = 0; i < n; ++i) {
-      foff[i] = nxt_off[i];
-      fcap[i] = nxt_cap[i];
-      n_slots = std::max(n_slots, nxt_off[i] + nxt_cap[i]);
-    }
-    std::swap(cur, nxt);
-    std::swap(ccnt, ncnt);
-  }
+  int rc = bb_level(S, 0, &B[B_FR0], &B[B_CNT2], foff, fcap);
+  if (rc) return rc;
   int err = 0;
   CK(cudaMemcpyAsync(&err, B[B_ERR].p, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   if (err) return fail(JSV_ERR_CAPACITY, "stage-2 frontier capacity exceeded");
-  if (nodes_out) c.stats.nodes += nodes;  // (not the diagnostic re-run)
+  if (nodes_out) c.stats.nodes += S.nodes;  // (not the diagnostic re-run)
   return JSV_OK;
 }
 

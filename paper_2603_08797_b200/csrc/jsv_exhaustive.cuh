@@ -726,7 +726,7 @@ __device__ __forceinline__ void x_sweep_reg(const XCtx<PM>& cx, const uint2* __r
 // probe).  No block barriers: the sink pool's rank records and sorted columns
 // are read through L1 (a few KB per probe, shared by every warp on the SM).
 template <int PM, bool RANK, bool REG>
-__global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? 2 : 1)
+__global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? JSV_XMINB : 1)
     k_s2_exh(const __grid_constant__ XArgs a) {
   constexpr int NS = x_slots(PM);
   using WS = XWarpState<PM, NS>;

@@ -302,6 +302,9 @@ struct XPlanArgs {
 int launch_x_plan(const XArgs& a, const XPlanArgs& pa, cudaStream_t st);
 // rounds per chunk of the exhaustive kernel's persistent blocks
 #define X_CHUNK 8
+#ifndef JSV_XMINB
+#define JSV_XMINB 2
+#endif
 
 // prefix-state slots per warp of the exhaustive kernel for a graph with P paths
 __host__ __device__ constexpr int x_slots(int pm) { return pm <= 8 ? 32 : (pm <= 16 ? 8 : 2); }

@@ -398,7 +398,30 @@ __global__ void __launch_bounds__(256) k_s2_leaf(const __grid_constant__ S2Args 
     atomicAdd(&a.best[probe].kills[L][threadIdx.x], sk[threadIdx.x]);
 }
 
-// per-probe fold of the leaf-block partials into BestRec
+// m(choices x) vs m(choices y), both by topo position (planner.py:852)
+__device__ inline int cmp_choice_m(const S2Args& a, int probe, const uint16_t* x, const uint16_t* y) {
+  MCursor cx{&a, probe, x, 0, 0, 0, 0}, cy{&a, probe, y, 0, 0, 0, 0};
+  cx.open_task();
+  cy.open_task();
+  while (true) {
+    unsigned long long ex = 0, ey = 0;
+    const bool hx = cx.next(ex), hy = cy.next(ey);
+    if (!hx || !hy) return hx == hy ? 0 : (hx ? 1 : -1);  // a strict prefix is smaller
+    if (ex != ey) return ex < ey ? -1 : 1;
+  }
+}
+
+// DFS order of two choice vectors (cmp_leaf's order)
+__device__ inline int cmp_choice_dfs(int T, const uint16_t* x, const uint16_t* y) {
+  for (int k = 0; k < T; ++k) {
+    const unsigned u = x[k] == NONE16 ? 0u : x[k], v = y[k] == NONE16 ? 0u : y[k];
+    if (u != v) return u < v ? -1 : 1;
+  }
+  return 0;
+}
+
+// per-probe fold of the leaf-block partials into BestRec (merged with what an earlier
+// frontier chunk of the same probe left there: the chunks of a split level)
 __global__ void __launch_bounds__(256) k_s2_reduce(const __grid_constant__ S2Args a) {
   __shared__ Cand sc[256];
   __shared__ unsigned long long s_leaves;
@@ -436,17 +459,29 @@ __global__ void __launch_bounds__(256) k_s2_reduce(const __grid_constant__ S2Arg
     if (c.has) {
       uint16_t ch[MAXT];
       code_choices(a, c.code, ch);
-      for (int k = 0; k < a.T; ++k) B->choice[k] = ch[k];
+      bool take = !B->has;
+      if (!take && a.mode == LEAF_FULL) {
+        if (c.obj != B->obj) take = c.obj > B->obj;
+        else if (c.sl != B->sl) take = c.sl < B->sl;
+        else take = cmp_choice_m(a, probe, ch, B->choice) < 0;
+      } else if (!take && a.mode == LEAF_FIRST) {
+        take = cmp_choice_dfs(a.T, ch, B->choice) < 0;
+      }
+      if (take) {
+        for (int k = 0; k < a.T; ++k) B->choice[k] = ch[k];
+        B->obj = c.obj;
+        B->sl = c.sl;
+      }
       B->has = 1;
       B->found = 1;
-      B->obj = c.obj;
-      B->sl = c.sl;
     }
     if (c.has_leaf) {
       uint16_t ch[MAXT];
       code_choices(a, c.leaf, ch);
-      for (int k = 0; k < a.T; ++k) B->leaf_choice[k] = ch[k];
-      B->has_leaf = 1;
+      if (!B->has_leaf || cmp_choice_dfs(a.T, ch, B->leaf_choice) > 0) {
+        for (int k = 0; k < a.T; ++k) B->leaf_choice[k] = ch[k];
+        B->has_leaf = 1;
+      }
     }
   }
 }

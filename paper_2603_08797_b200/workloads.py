@@ -77,6 +77,47 @@ def star(n_tasks: int = 12):
     return app, synth_profile(graph, knobs)
 
 
+def layered(widths=(1, 4, 4, 3), variants: int = 8):
+    """SURVEY 8(d) configs[3] stress variant: a layered DAG (default 1 -> 4 -> 4 -> 3),
+    every task feeding every task of the next layer with fan-out factor 1/outdegree
+    (demand conserved per layer), uniform path fractions (the last absorbs
+    rounding), the star's variants, segments, batches and SLOs.  Plan it at
+    PlanRequest(200.0, 84, A+S+T)."""
+    layers = []
+    k = 0
+    for w in widths:
+        layers.append([f"l{k + i:02d}" for i in range(w)])
+        k += w
+    names = [nm for lay in layers for nm in lay]
+    succ = {nm: [] for nm in names}
+    for a, b in zip(layers, layers[1:]):
+        for u in a:
+            succ[u] = list(b)
+    tasks = []
+    for nm in names:
+        vs = []
+        for j in range(variants):
+            f = {d: 1.0 / len(succ[nm]) for d in succ[nm]}
+            vs.append(ModelVariant(f"{nm}_v{j}", 0.70 + 0.03 * j, f))
+        tasks.append(Task(nm, tuple(vs)))
+    edges = tuple((u, d) for u in names for d in succ[u])
+    paths = [[u] for u in layers[0]]
+    for lay in layers[1:]:
+        paths = [p + [d] for p in paths for d in lay]
+    fr = {}
+    acc = 0.0
+    for i, p in enumerate(paths):
+        f = 1.0 / len(paths) if i < len(paths) - 1 else 1.0 - acc
+        fr[tuple(p)] = f
+        acc += f
+    graph = TaskGraph(tuple(tasks), edges, fr)
+    app = AppSpec("layered", graph, 1500.0, 0.85, 1.0, 0.035, 20.0, 10.0)
+    segs = tuple(SegmentType(m, p) for m in ("1g", "2g", "3g", "4g", "7g") for p in (1, 2))
+    base = {v.id: 10.0 + 3.0 * j for t in tasks for j, v in enumerate(t.variants)}
+    knobs = SynthKnobs(base, 0.7, 0.65, 0.15, 0.0, 5, {}, segs, (1, 4, 16, 64))
+    return app, synth_profile(graph, knobs)
+
+
 def traffic():
     """configs[4]: traffic-analysis (1,280 profile entries); plan at 840 slices."""
     return bundled("traffic-analysis")

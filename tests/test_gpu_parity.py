@@ -221,3 +221,32 @@ def test_stats_nodes_reported(strategy):
     finally:
         planner.set_strategy("auto")
     assert res.feasible and res.stats.nodes > 0
+
+
+@pytest.mark.parametrize("max_slots", ["1", "64", "4096"])
+def test_search_with_split_frontiers_matches_reference(max_slots, monkeypatch):
+    """The level-synchronous branch-and-bound with its frontier memory bounded
+    (JSV_BB_MAX_SLOTS: a level whose children would exceed it is expanded in halves,
+    depth-first, recursively): every bundled / tiny / star golden plan -- optimum, m
+    tie-breaks, feasible-only first leaves and infeasible binding constraints -- and
+    max_demand results are unchanged by the chunking."""
+    from paper_2603_08797_b200 import planner
+    from paper_2603_08797_b200.plan_types import SearchSpace
+
+    monkeypatch.setenv("JSV_BB_MAX_SLOTS", max_slots)
+    planner.set_strategy("search")
+    try:
+        docs = load("plans_bundled.json")[::4] + load("plans_tiny.json")[::10] + load("plans_star.json")
+        for doc in docs:
+            app, table, req, opt = case_inputs(doc)
+            assert result_dict(planner.plan(app, table, req, opt)) == doc["result"], doc["name"]
+        for doc in load("max_demand.json")[::12]:
+            from golden_io import app_from_dict
+
+            app = app_from_dict(doc["app"])
+            r = planner.max_demand(app, profile_of(doc), doc["budget"], SearchSpace.from_label(doc["space"]),
+                                   doc["slack"], None, doc["rel_tol"])
+            assert (r.demand_rps, r.probes) == (doc["demand"], doc["probes"]), doc["name"]
+            assert result_dict(r.plan) == doc["plan"], doc["name"]
+    finally:
+        planner.set_strategy("auto")
