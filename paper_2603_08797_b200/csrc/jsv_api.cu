@@ -111,6 +111,9 @@ struct jsv_context {
   long long kcnt[K_COUNT_] = {};
   int strategy = JSV_STRATEGY_AUTO;
   long long exh_limit = 1LL << 31;
+  // branch-and-bound per-level frontier / live-count buffers (reused call to call:
+  // cudaMalloc / cudaFree per call would serialise the device)
+  std::vector<std::unique_ptr<DevBuf>> bb_fr, bb_cnt;
   int shard_rank = 0, shard_world = 1;
   // pinned host staging for per-solve tables (one async copy instead of several
   // pageable ones); reused call to call -- every call synchronises before returning
@@ -1007,7 +1010,6 @@ struct BBState {
   long long max_slots;
   long long nodes = 0;
   std::vector<long long>* nodes_out;
-  std::vector<std::unique_ptr<DevBuf>> lvl_fr, lvl_cnt;  // per-level frontier / live-count caches
 };
 
 static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vector<long long>& foff,
@@ -1154,16 +1156,16 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
         nxt_cap[i] = (long long)ptot[i];
         NO += nxt_cap[i];
       }
-      if ((int)S.lvl_fr.size() <= L + 1) {
-        S.lvl_fr.resize(L + 2);
-        S.lvl_cnt.resize(L + 2);
+      if ((int)c.bb_fr.size() <= L + 1) {
+        c.bb_fr.resize(L + 2);
+        c.bb_cnt.resize(L + 2);
       }
-      if (!S.lvl_fr[L + 1]) {
-        S.lvl_fr[L + 1] = std::make_unique<DevBuf>();
-        S.lvl_cnt[L + 1] = std::make_unique<DevBuf>();
+      if (!c.bb_fr[L + 1]) {
+        c.bb_fr[L + 1] = std::make_unique<DevBuf>();
+        c.bb_cnt[L + 1] = std::make_unique<DevBuf>();
       }
-      nxt = S.lvl_fr[L + 1].get();
-      ncnt = S.lvl_cnt[L + 1].get();
+      nxt = c.bb_fr[L + 1].get();
+      ncnt = c.bb_cnt[L + 1].get();
       CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
       CK(B[B_NXTCAP].ensure(sizeof(long long) * n));
       CK(ncnt->ensure(sizeof(unsigned long long) * n));
@@ -1198,7 +1200,11 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   S.bs = &bs;
   S.diag = diag;
   S.nodes_out = nodes_out;
-  S.max_slots = 1LL << 25;
+  // Deep graphs' full plans: small chunks make the search depth-first enough that
+  // leaves -- and with them the incumbent whose objective bound prunes every level --
+  // come early (layered 1->4->4->3: 3 s; one 2^25-slot level at a time does not finish).
+  // Shallow graphs and feasibility probes keep wide levels (fewer round trips).
+  S.max_slots = (!bs.feasible_only && T >= 6) ? (1LL << 16) : (1LL << 25);
   if (const char* e = getenv("JSV_BB_MAX_SLOTS")) S.max_slots = std::max(1LL, atoll(e));
   S2Args& a = S.a;
   s2_base(p, bs, a);

@@ -214,7 +214,9 @@ __global__ void __launch_bounds__(256) k_s2_level(const __grid_constant__ S2Args
     const int probe = a.pr_probe[s];
     const int b = (int)(w - a.pfx[s]);
     double ub = 0.0;
-    const int st = filter_item(a, probe, s, b, false, ub);
+    // the objective bound against the probe's incumbent (planner.py:897-903) prunes
+    // internal levels too once a leaf has set one (depth-first frontier chunks do early)
+    const int st = filter_item(a, probe, s, b, a.mode == LEAF_FULL && !a.diag, ub);
     if (st == ST_SKIP) continue;
     const bool rpos = a.pr_flag[s] & 1;
     if (a.diag && rpos) {

@@ -79,3 +79,30 @@ def test_star12_max_demand_solves():
     assert r.demand_rps > 0 and r.plan.feasible and 10 <= r.probes <= 40
     again = P.plan(app, table, PlanRequest(r.demand_rps, 84, sp))
     assert result_dict(again) == result_dict(r.plan)
+
+
+@pytest.mark.parametrize("doc", load("plans_layered.json"), ids=lambda d: d["name"])
+def test_layered_dag_matches_reference(doc):
+    """SURVEY 8(d)'s layered stress variant at the sizes the reference finishes
+    (1-2-1: 6 s, 1-2-2: 4 s, 1-2-2-1: 696 s there): the GPU branch-and-bound
+    (depth-first frontier chunks, objective bound at every level) bit-exactly."""
+    from paper_2603_08797_b200 import planner as P
+
+    app, table, req, opt = case_inputs(doc)
+    assert result_dict(P.plan(app, table, req, opt)) == doc["result"]
+
+
+def test_layered_1_4_4_3_solves_and_is_chunking_independent(monkeypatch):
+    """configs[3]'s 1 -> 4 -> 4 -> 3 layered DAG (12 tasks, 32 edges, 48 paths; no
+    reference result): solved by the branch-and-bound, identical under two frontier
+    chunk sizes (the chunking changes the traversal, never the result)."""
+    from paper_2603_08797_b200 import planner as P
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    app, table = workloads.layered((1, 4, 4, 3))
+    req = PlanRequest(200.0, 84, SearchSpace(True, True, True))
+    a = P.plan(app, table, req)
+    monkeypatch.setenv("JSV_BB_MAX_SLOTS", "32768")
+    b = P.plan(app, table, req)
+    assert a.feasible and result_dict(a) == result_dict(b)
