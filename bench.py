@@ -421,7 +421,7 @@ def c3_apps(app):
     return [dataclasses.replace(app, latency_slo_ms=L, accuracy_slo=a) for L in C3_LAT for a in C3_ACC]
 
 
-def star12_solve(P, torch, flush) -> dict:
+def star12_solve(P, torch, flush, layered: bool = True) -> dict:
     """configs[3]: the 12-task star at 200 rps / 84 slices (reference: no result in 600 s)."""
     from paper_2603_08797_b200 import workloads
     from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
@@ -447,7 +447,8 @@ def star12_solve(P, torch, flush) -> dict:
             "objective": r.objective, "total_slices": r.config.total_slices,
             "solver": "fan-out knapsack-DP bounded enumeration + exact evaluation",
             "max_demand_rps": md.demand_rps, "max_demand_probes": md.probes,
-            "max_demand_ms": md_ms, "layered_1_4_4_3": layered_solve(P)}
+            "max_demand_ms": md_ms,
+            **({"layered_1_4_4_3": layered_solve(P)} if layered else {})}
 
 
 def layered_solve(P) -> dict:
@@ -664,7 +665,8 @@ def main() -> None:
         c4 = traffic840(P, rank, world, device=local)
         extras["c4_local"] = (c4["max_demand_8_spaces_ms"], c4["trace_ms"])
         if rank == 0:
-            extras["configs3_star12"] = star12_solve(P, torch, flush)
+            # (the layered solve is a single-GPU figure; multi-rank runs skip it)
+            extras["configs3_star12"] = star12_solve(P, torch, flush, layered=world == 1)
             extras["configs4_traffic840"] = c4
             extras["placement"] = place_plans(app, table, reqs)
 
