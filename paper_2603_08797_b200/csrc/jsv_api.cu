@@ -885,6 +885,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     CK(B[B_S1TESTS].ensure(2 * sizeof(unsigned long long)));
     CK(cudaMemsetAsync(B[B_S1TESTS].p, 0, 2 * sizeof(unsigned long long), st));
     a.tests = B[B_S1TESTS].as<unsigned long long>();
+    a.tma = getenv("JSV_NO_TMA") ? 0 : 1;
     c.stats.kernel_launches += launch_stage1_fused(a, smem, st);
     if (phases) {
       // mean phase durations over the jobs (diagnostics on stderr)

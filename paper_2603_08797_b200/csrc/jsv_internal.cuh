@@ -387,3 +387,55 @@ __device__ __forceinline__ void spin_unlock(int* l) {
   __threadfence();
   atomicExch(l, 0);
 }
+
+// ------------------------------------------------------------- TMA bulk copies
+// (cp.async.bulk global -> shared completing on an mbarrier: UBLKCP in SASS)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+  } while (!done);
+}
+
+// Stage `bytes` from global `src` into shared memory at 16-byte aligned `dst_a`
+// with one bulk copy of the enclosing 16-byte aligned range; returns where the data
+// starts in shared memory.  Called by one thread; the copy completes on `bar`.
+__device__ __forceinline__ void* bulk_stage(void* dst_a, const void* src, size_t bytes,
+                                            unsigned long long* bar, unsigned* tx) {
+  const size_t s = reinterpret_cast<size_t>(src);
+  const size_t s_a = s & ~(size_t)15;
+  const unsigned n = (unsigned)((s - s_a + bytes + 15) & ~(size_t)15);
+  if (bytes > 0) {
+    bulk_g2s(dst_a, reinterpret_cast<const void*>(s_a), n, bar);
+    *tx += n;
+  }
+  return static_cast<char*>(dst_a) + (s - s_a);
+}
+// shared-memory bytes bulk_stage may write for `bytes` of data
+__host__ __device__ constexpr size_t bulk_span(size_t bytes) { return (bytes + 31) & ~(size_t)15; }
+

@@ -124,6 +124,7 @@ struct S1Args {
   int fused_cap;  // fused Stage 1: candidates whose working lists fit shared memory
   unsigned long long* stamps;  // JSV_S1_PHASES: [jobs x 10] phase timestamps (else null)
   unsigned long long* tests;   // fused Stage 1: [2] skyline pair tests (float shadow, exact)
+  int tma;        // fused Stage 1: stage the task's tables with cp.async.bulk (JSV_NO_TMA: loops)
 };
 
 struct S1Launch {

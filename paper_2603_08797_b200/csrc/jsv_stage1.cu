@@ -1088,6 +1088,9 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_n, s_carry, s_ok;
   __shared__ int s_work[3];  // dynamic work counters: units (A), list positions (D), survivors (F)
+  __shared__ __align__(8) unsigned long long s_bar;  // TMA staging of the task's tables
+  __shared__ void* s_kptr[4];                        // staged key tables (lat, thr, var, cost)
+  __shared__ const unsigned* s_wptr[8];              // staged ways table per descriptor
   __shared__ double s_rd[32];
   __shared__ int s_ri[32];
   __shared__ double s_ra[32];
@@ -1112,29 +1115,83 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   const int ncap = a.fused_cap;
   // (before the lists are in use: the task's exhaustive ways tables for A and its
   // profile-key tables for B are staged in their space)
-  int* st_i = reinterpret_cast<int*>(pcand);
   const int nk = g.key_off[t + 1] - g.key_off[t];
-  const bool keys_sm = (size_t)nk * 24 <= (size_t)ncap * 16;
-  double* k_lat = reinterpret_cast<double*>(pcand);
-  double* k_thr = k_lat + nk;
-  int* k_var = reinterpret_cast<int*>(k_thr + nk);
-  int* k_cost = k_var + nk;
-  unsigned* w_sm = reinterpret_cast<unsigned*>(pcand + (size_t)ncap * 20 + 16);  // (shadow space)
-  int w_tot = 0;
-  for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d)
-    if (a.desc[d].mode == 0) w_tot += (a.desc[d].n_tuples + 1) * (a.S + 1);
-  const bool ways_sm = (size_t)w_tot * 4 <= (size_t)ncap * 16;
-  if (ways_sm) {
-    int o = 0;
-    for (int d = a.desc_t0[t]; d < a.desc_t0[t + 1]; ++d) {
-      const GenDesc& Dd = a.desc[d];
-      if (Dd.mode != 0) continue;
-      const int m = (Dd.n_tuples + 1) * (a.S + 1);
-      for (int i = tid; i < m; i += S1F_THREADS) w_sm[o + i] = a.ways[Dd.w_off + i];
-      o += m;
+  const int kb = g.key_off[t];
+  const int d0 = a.desc_t0[t], d1 = a.desc_t0[t + 1];
+  // (key tables in the lists' space, ways tables in the shadow list's space)
+  const bool keys_sm = bulk_span(16 * (size_t)nk) + bulk_span(16 * (size_t)nk) <= (size_t)ncap * 16;
+  size_t w_span = 0;
+  for (int d = d0; d < d1; ++d)
+    if (a.desc[d].mode == 0) w_span += bulk_span(4 * (size_t)(a.desc[d].n_tuples + 1) * (a.S + 1));
+  const bool ways_sm = w_span <= (size_t)ncap * 16 && d1 - d0 <= 8;
+  unsigned char* kreg = pcand;
+  unsigned char* wreg = pcand + (((size_t)ncap * 20 + 15) & ~(size_t)15);
+  // TMA (cp.async.bulk) staging of both, completing on one mbarrier; JSV_NO_TMA: loops
+  if (tid == 0) {
+    if (a.tma) {
+      mbar_init(&s_bar, 1);
+      unsigned tx = 0;
+      unsigned char* kp = kreg;
+      if (keys_sm) {
+        s_kptr[0] = bulk_stage(kp, a.tb.key_lat + kb, 8 * (size_t)nk, &s_bar, &tx);
+        kp += bulk_span(8 * (size_t)nk);
+        s_kptr[1] = bulk_stage(kp, a.tb.key_thr + kb, 8 * (size_t)nk, &s_bar, &tx);
+        kp += bulk_span(8 * (size_t)nk);
+        s_kptr[2] = bulk_stage(kp, a.tb.key_var + kb, 4 * (size_t)nk, &s_bar, &tx);
+        kp += bulk_span(4 * (size_t)nk);
+        s_kptr[3] = bulk_stage(kp, a.tb.key_cost + kb, 4 * (size_t)nk, &s_bar, &tx);
+      }
+      if (ways_sm) {
+        unsigned char* wp = wreg;
+        for (int d = d0; d < d1; ++d) {
+          const GenDesc& Dd = a.desc[d];
+          if (Dd.mode != 0) continue;
+          const size_t bytes = 4 * (size_t)(Dd.n_tuples + 1) * (a.S + 1);
+          s_wptr[d - d0] = static_cast<const unsigned*>(bulk_stage(wp, a.ways + Dd.w_off, bytes, &s_bar, &tx));
+          wp += bulk_span(bytes);
+        }
+      }
+      // (arrive with the transaction count after issuing: the phase completes when
+      // every byte has landed)
+      mbar_expect_tx(&s_bar, tx);
+    } else {
+      unsigned char* kp = kreg;
+      s_kptr[0] = kp; kp += bulk_span(8 * (size_t)nk);
+      s_kptr[1] = kp; kp += bulk_span(8 * (size_t)nk);
+      s_kptr[2] = kp; kp += bulk_span(4 * (size_t)nk);
+      s_kptr[3] = kp;
+      unsigned char* wp = wreg;
+      for (int d = d0; d < d1; ++d) {
+        if (a.desc[d].mode != 0) continue;
+        s_wptr[d - d0] = reinterpret_cast<const unsigned*>(wp);
+        wp += bulk_span(4 * (size_t)(a.desc[d].n_tuples + 1) * (a.S + 1));
+      }
     }
   }
-  (void)st_i;
+  __syncthreads();
+  double* k_lat = static_cast<double*>(s_kptr[0]);
+  double* k_thr = static_cast<double*>(s_kptr[1]);
+  int* k_var = static_cast<int*>(s_kptr[2]);
+  int* k_cost = static_cast<int*>(s_kptr[3]);
+  if (a.tma) {
+    if (keys_sm || ways_sm) mbar_wait(&s_bar, 0);
+  } else {
+    if (keys_sm)
+      for (int k = tid; k < nk; k += S1F_THREADS) {
+        k_lat[k] = a.tb.key_lat[kb + k];
+        k_thr[k] = a.tb.key_thr[kb + k];
+        k_var[k] = a.tb.key_var[kb + k];
+        k_cost[k] = a.tb.key_cost[kb + k];
+      }
+    if (ways_sm)
+      for (int d = d0; d < d1; ++d) {
+        const GenDesc& Dd = a.desc[d];
+        if (Dd.mode != 0) continue;
+        const int m = (Dd.n_tuples + 1) * (a.S + 1);
+        unsigned* w = const_cast<unsigned*>(s_wptr[d - d0]);
+        for (int i = tid; i < m; i += S1F_THREADS) w[i] = a.ways[Dd.w_off + i];
+      }
+  }
   __syncthreads();
   // ---- A: enumeration units of this task's descriptors (_candidate_pool's union)
   int u_tot = 0;
@@ -1151,12 +1208,9 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
     o.n = 0;
     o.key1 = -1;
     if (u < u_tot) {
-      int d = a.desc_t0[t], lu = u, wo = 0;
-      while (lu >= a.desc[d].n_units) {
-        if (a.desc[d].mode == 0) wo += (a.desc[d].n_tuples + 1) * (a.S + 1);
-        lu -= a.desc[d++].n_units;
-      }
-      gen_unit(a, probe, a.desc[d], lu, o, ways_sm ? w_sm + wo : a.ways + a.desc[d].w_off);
+      int d = a.desc_t0[t], lu = u;
+      while (lu >= a.desc[d].n_units) lu -= a.desc[d++].n_units;
+      gen_unit(a, probe, a.desc[d], lu, o, ways_sm ? s_wptr[d - d0] : a.ways + a.desc[d].w_off);
     }
     // warp-aggregated slot reservation
     int incl = o.m;
@@ -1182,16 +1236,6 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   const int n = min(s_n, (int)a.task_cap[t]);
   S1_STAMP(1);
   if (tid == 0) a.cnt[job] = s_n;
-  if (keys_sm) {
-    const int kb = g.key_off[t];
-    for (int k = tid; k < nk; k += S1F_THREADS) {
-      k_lat[k] = a.tb.key_lat[kb + k];
-      k_thr[k] = a.tb.key_thr[kb + k];
-      k_var[k] = a.tb.key_var[kb + k];
-      k_cost[k] = a.tb.key_cost[kb + k];
-    }
-    __syncthreads();
-  }
   const bool fits = n <= ncap;
   int* front = fits ? reinterpret_cast<int*>(pcand) : a.front + base;
   int* ord = fits ? front + ncap : a.order + base;
