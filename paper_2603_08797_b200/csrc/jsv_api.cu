@@ -1399,7 +1399,11 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   if (nx == 0) return JSV_OK;
   JSV_T("exh: probes planned");
   // every probe's prefix range, concatenated (k_x_live); live lists at the same offsets
-  const int n_slots = x_slots(p.P);
+  // prefixes per round: short rounds for small batches (their live prefixes spread over
+  // more warps; JSV_XROUND overrides)
+  int n_slots = x_slots(p.P);
+  if (nx <= 8) n_slots = std::min(n_slots, 8);
+  if (const char* e = getenv("JSV_XROUND")) n_slots = std::max(1, std::min(x_slots(p.P), atoi(e)));
   // k_x_live's work units: upper prefixes (all prefix digits but the fastest)
   std::vector<long long> uoff(n + 1, 0);
   long long n_pref = 0, n_upper = 0, max_rounds = 0;
@@ -1451,6 +1455,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   }
   a.max_pn_last = max_pn_last;
   a.rpl = reg;
+  a.round = n_slots;
   if (a.fast) {
     CK(B[B_XSACC].ensure(sizeof(double) * (size_t)n * W));
     CK(B[B_XSCAP].ensure(sizeof(double) * (size_t)n * W));
@@ -1598,6 +1603,7 @@ static int run_exhaustive_dev(jsv_problem& p, BatchState& bs, bool want_config, 
   }
   a.max_pn_last = W;
   a.rpl = 1;
+  a.round = n_slots;  // (device-planned batches keep full rounds)
   a.prune = getenv("JSV_NO_PRUNE") ? 0 : 1;
   if (a.mode == LEAF_FULL) {
     a.mkey = (T <= 5 && (long long)W * bs.s1.maxi <= 4096 && !getenv("JSV_NO_MKEY")) ? 1 : 0;

@@ -760,9 +760,11 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? JSV_XMINB : 1)
         for (int p = 0; p < PM; ++p) cx.frac[p] = frac[p];
       }
       // ---- one live prefix per lane -> the warp state in shared memory
+      // (a round is a.round prefixes <= NS: small batches use short rounds so their few
+      // live prefixes spread over more warps)
       if (lane < NS) {
-        const long long qi = (rd - a.roff[probe]) * NS + lane;
-        if (qi < a.live_cnt[probe])
+        const long long qi = (rd - a.roff[probe]) * a.round + lane;
+        if (lane < a.round && qi < a.live_cnt[probe])
           x_prefix<PM, NS, RANK>(s, g, xp, pr, probe, xp.q0 + a.live[xp.loff + qi], frac, thru,
                                  lane, a.lat2_max, rv, ws, a.mkey);
         else {
@@ -1663,7 +1665,7 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
     k_x_live<<<(unsigned)blocks, 256, 0, st>>>(a, n_upper);
     ++launches;
   }
-  k_x_sched<<<1, 1024, 0, st>>>(a, x_slots(P));
+  k_x_sched<<<1, 1024, 0, st>>>(a, a.round);
   PROF_END();
   cudaStreamWaitEvent(st, join, 0);
   PROF_BEGIN(K_S2_EXH);

@@ -283,6 +283,7 @@ struct XArgs {
   int mkey;               // full plans, T <= 5: m tie-breaks compare packed 55-bit keys
   int* xr_done;           // [n_probes] column blocks of k_x_rank finished
   const long long* dev_totals;  // device-planned batches (k_x_plan): [0] upper prefixes
+  int round;              // prefixes per round (<= x_slots(P))
 };
 
 // k_x_plan: XProbe construction on the device (no host round trip between Stage 1
