@@ -313,12 +313,27 @@ __global__ void __launch_bounds__(JOB_BS, 2) k_bucket(const __grid_constant__ S1
   for (int i = threadIdx.x; i < n; i += blockDim.x)
     atomicAdd(&hist[(int)a.arr[base + i] + 1], 1);  // arr[0] = slices
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int acc = 0;
-    for (int s = 0; s < NB; ++s) {
-      acc += hist[s];
-      hist[s] = acc;
-      bst[s] = acc;
+  {
+    // inclusive block scan of the bucket counts, JOB_BS buckets per step (840-slice
+    // budgets: 842 buckets -- a thread-0 loop was most of this kernel there)
+    typedef cub::BlockScan<int, JOB_BS> BScan;
+    __shared__ typename BScan::TempStorage btmp;
+    __shared__ int bcarry;
+    if (threadIdx.x == 0) bcarry = 0;
+    __syncthreads();
+    for (int s0 = 0; s0 < NB; s0 += JOB_BS) {
+      const int s = s0 + threadIdx.x;
+      const int v = s < NB ? hist[s] : 0;
+      int inc, total;
+      BScan(btmp).InclusiveSum(v, inc, total);
+      const int c0 = bcarry;
+      if (s < NB) {
+        hist[s] = c0 + inc;
+        bst[s] = c0 + inc;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) bcarry = c0 + total;
+      __syncthreads();
     }
   }
   // same-bucket pass items: j chunks of 1024 (a tile's bucket range can be long)
