@@ -92,7 +92,8 @@ enum BufId {
   B_PWIDTH, B_PFLAG, B_PR, B_PUSED, B_PLATS, B_PACCS, B_PTOT, B_PSTART, B_XPROBE, B_XBOFF,
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
   B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_ARRF,
-  B_BFKEY, B_BFWAYS, B_BFPART, B_BFOUT, B_COUNT
+  B_BFKEY, B_BFWAYS, B_BFPART, B_BFOUT, B_SRT_KTMP, B_SRT_KOUT, B_SRT_PERM, B_SRT_PERMO,
+  B_SRT_TMP, B_SRT_ROWS, B_SRT_SEGE, B_COUNT
 };
 
 struct jsv_context {
@@ -113,7 +114,7 @@ struct jsv_context {
   long long exh_limit = 1LL << 31;
   // branch-and-bound per-level frontier / live-count buffers (reused call to call:
   // cudaMalloc / cudaFree per call would serialise the device)
-  std::vector<std::unique_ptr<DevBuf>> bb_fr, bb_cnt;
+  std::vector<std::unique_ptr<DevBuf>> bb_fr, bb_cnt, bb_key;
   int shard_rank = 0, shard_world = 1;
   // pinned host staging for per-solve tables (one async copy instead of several
   // pageable ones); reused call to call -- every call synchronises before returning
@@ -903,6 +904,10 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
       fprintf(stderr, "[jsv s1] jobs %d span %.1f us; mean us per phase:", n_s1 * T, (t1 - t0) / 1e3);
       for (int k = 0; k < 8; ++k) fprintf(stderr, " %.1f", acc[k] / (n_s1 * T) / 1e3);
       fprintf(stderr, "\n");
+      if (atoi(getenv("JSV_S1_PHASES")) > 1)  // per job: task, start and end (us from t0)
+        for (size_t j = 0; j < (size_t)n_s1 * T; ++j)
+          fprintf(stderr, "[jsv s1 job] %zu %zu %.1f %.1f\n", j, j % T, (h[j * 10] - t0) / 1e3,
+                  (h[j * 10 + 8] - t0) / 1e3);
       a.stamps = nullptr;
     }
   } else {
@@ -1014,7 +1019,7 @@ struct BBState {
 };
 
 static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vector<long long>& foff,
-                    const std::vector<long long>& fcap) {
+                    const std::vector<long long>& fcap, DevBuf* ckey = nullptr) {
   jsv_problem& p = *S.p;
   BatchState& bs = *S.bs;
   jsv_context& c = *p.ctx;
@@ -1028,7 +1033,7 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
   std::vector<long long> pstart(n), nxt_off(n), nxt_cap(n), boff(n + 1);
   std::vector<unsigned long long> ptot(n), fcnt(n);
   JSV_T("s2 level begin");
-  if (timing_on()) fprintf(stderr, "[jsv t] level %d slots %lld\n", L, n_slots);
+  if (timing_on()) fprintf(stderr, "[jsv t] level %d slots %lld n %d\n", L, n_slots, n);
   const bool last = (L == T - 1);
   const size_t S1 = (size_t)std::max<long long>(1, n_slots);
   CK(B[B_FOFF].ensure(sizeof(long long) * n));
@@ -1092,6 +1097,35 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
     for (int i = 0; i < n; ++i) can = can || fcnt[i] >= 2;
     if (can) {
       if (timing_on()) fprintf(stderr, "[jsv t] level %d split (%lld children)\n", L, total);
+      if (ckey) {
+        // best-first: the frontier ordered by its children's objective bound (the
+        // halves below are copied from the sorted rows and stay sorted: ckey = null)
+        std::vector<long long> sege(n);
+        long long max_cap = 0;
+        for (int i = 0; i < n; ++i) {
+          sege[i] = foff[i] + fcap[i];
+          max_cap = std::max(max_cap, fcap[i]);
+        }
+        CK(B[B_SRT_SEGE].ensure(sizeof(long long) * n));
+        CK(cudaMemcpyAsync(B[B_SRT_SEGE].p, sege.data(), sizeof(long long) * n, cudaMemcpyHostToDevice, st));
+        CK(B[B_SRT_KTMP].ensure(sizeof(double) * S1));
+        CK(B[B_SRT_KOUT].ensure(sizeof(double) * S1));
+        CK(B[B_SRT_PERM].ensure(sizeof(int) * S1));
+        CK(B[B_SRT_PERMO].ensure(sizeof(int) * S1));
+        CK(B[B_SRT_ROWS].ensure(sizeof(uint16_t) * S1 * T));
+        size_t sb = 0;
+        CK((cudaError_t)launch_frontier_best_first(nullptr, nullptr, nullptr, B[B_SRT_KTMP].as<double>(),
+                                                   B[B_SRT_KOUT].as<double>(), B[B_SRT_PERM].as<int>(),
+                                                   B[B_SRT_PERMO].as<int>(), nullptr, &sb, a.foff, a.fcap,
+                                                   B[B_SRT_SEGE].as<long long>(), a.fcnt, n, n_slots,
+                                                   max_cap, T, st));
+        CK(B[B_SRT_TMP].ensure(std::max<size_t>(sb, 16)));
+        CK((cudaError_t)launch_frontier_best_first(
+            ckey->as<double>(), cur->as<uint16_t>(), B[B_SRT_ROWS].as<uint16_t>(), B[B_SRT_KTMP].as<double>(),
+            B[B_SRT_KOUT].as<double>(), B[B_SRT_PERM].as<int>(), B[B_SRT_PERMO].as<int>(), B[B_SRT_TMP].p,
+            &sb, a.foff, a.fcap, B[B_SRT_SEGE].as<long long>(), a.fcnt, n, n_slots, max_cap, T, st));
+        c.stats.kernel_launches += 3;
+      }
       for (int half = 0; half < 2; ++half) {
         std::vector<long long> hoff(n), hcap(n);
         std::vector<unsigned long long> hcnt(n);
@@ -1130,6 +1164,7 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
   if (last && !diag) c.stats.leaf_work += total;
   DevBuf* nxt = nullptr;
   DevBuf* ncnt = nullptr;
+  DevBuf* nkey = nullptr;
   std::vector<long long> noff(n), ncap(n);
   if (total > 0) {
     CK(B[B_PSTART].ensure(sizeof(long long) * n));
@@ -1165,6 +1200,12 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
         c.bb_fr[L + 1] = std::make_unique<DevBuf>();
         c.bb_cnt[L + 1] = std::make_unique<DevBuf>();
       }
+      if ((int)c.bb_key.size() <= L + 1) c.bb_key.resize(L + 2);
+      if (!c.bb_key[L + 1]) c.bb_key[L + 1] = std::make_unique<DevBuf>();
+      // children's objective bounds (full plans only: the order a later split uses)
+      nkey = (a.mode == LEAF_FULL && !diag) ? c.bb_key[L + 1].get() : nullptr;
+      if (nkey) CK(nkey->ensure(sizeof(double) * std::max<long long>(1, NO)));
+      a.nxt_key = nkey ? nkey->as<double>() : nullptr;
       nxt = c.bb_fr[L + 1].get();
       ncnt = c.bb_cnt[L + 1].get();
       CK(B[B_NXTOFF].ensure(sizeof(long long) * n));
@@ -1187,7 +1228,7 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
   if (diag) c.stats.kernel_launches += launch_stage2_blocked(a, st);
   if (last || total == 0) return JSV_OK;
   // next frontier: slots [nxt_off, nxt_off + nxt_cap) per probe, live counts on the device
-  return bb_level(S, L + 1, nxt, ncnt, nxt_off, nxt_cap);
+  return bb_level(S, L + 1, nxt, ncnt, nxt_off, nxt_cap, nkey);
 }
 
 static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_config,
@@ -1207,6 +1248,9 @@ static int run_stage2(jsv_problem& p, BatchState& bs, bool diag, bool want_confi
   // Shallow graphs and feasibility probes keep wide levels (fewer round trips).
   S.max_slots = (!bs.feasible_only && T >= 6) ? (1LL << 16) : (1LL << 25);
   if (const char* e = getenv("JSV_BB_MAX_SLOTS")) S.max_slots = std::max(1LL, atoll(e));
+  if (timing_on())
+    fprintf(stderr, "[jsv t] bb run n %d T %d fonly %d diag %d max_slots %lld\n", n, T, bs.feasible_only, (int)diag,
+            S.max_slots);
   S2Args& a = S.a;
   s2_base(p, bs, a);
   a.diag = diag ? 1 : 0;

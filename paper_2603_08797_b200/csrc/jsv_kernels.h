@@ -199,6 +199,8 @@ struct S2Args {
   long long* pfx;               // [n_slots + 1] exclusive scan of pr_width
   const long long* pstart;      // [n_probes] first work item of each probe
   uint16_t* nxt;
+  double* nxt_key;              // [slot of nxt] objective upper bound of the child (LEAF_FULL;
+                                // orders a frontier best-first before it is split)
   unsigned long long* nxt_cnt;  // [n_probes]
   const long long* nxt_off;     // [n_probes]
   const long long* nxt_cap;     // [n_probes]
@@ -367,6 +369,13 @@ int launch_stage2_prep(const S2Args& a, double* min_lat2, int* min_sl, double* a
 int launch_stage2_prefix(const S2Args& a, cudaStream_t st);
 int launch_stage2_level(const S2Args& a, long long total, cudaStream_t st);
 int launch_stage2_blocked(const S2Args& a, cudaStream_t st);
+// order each probe's frontier rows by the children's objective bound, descending
+// (sort_tmp == nullptr: *sort_bytes <- the scratch size; returns a cudaError_t)
+int launch_frontier_best_first(const double* key, uint16_t* rows, uint16_t* rows_tmp, double* k_tmp,
+                               double* k_out, int* perm, int* perm_out, void* sort_tmp,
+                               size_t* sort_bytes, const long long* foff, const long long* fcap,
+                               const long long* seg_end, const unsigned long long* fcnt, int n,
+                               long long n_slots, long long max_cap, int T, cudaStream_t st);
 
 struct FinArgs {
   const DGraph* g;

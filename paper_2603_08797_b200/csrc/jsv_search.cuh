@@ -229,6 +229,12 @@ __global__ void __launch_bounds__(256) k_s2_level(const __grid_constant__ S2Args
       atomicExch(a.err, 3);
       continue;
     }
+    if (a.nxt_key) {
+      const DProbe& pr = a.probes[probe];
+      const int used = a.pr_used[s] + (rpos ? a.p_sl[(long long)(probe * T + a.g->topo[L]) * a.W + b] : 0);
+      const int fut = a.future[probe * (T + 1) + L + 1];
+      a.nxt_key[a.nxt_off[probe] + (long long)pos] = pr.alpha * ub - pr.beta * (double)(used + fut);
+    }
     uint16_t* dst = a.nxt + (a.nxt_off[probe] + (long long)pos) * T;
     for (int k = 0; k < L; ++k) dst[k] = a.cur[s * T + k];
     dst[L] = rpos ? (uint16_t)b : (uint16_t)NONE16;
@@ -522,6 +528,59 @@ int launch_stage2_level(const S2Args& a, long long total, cudaStream_t st) {
   k_s2_level<<<(unsigned)blocks, 256, 0, st>>>(a);
   PROF_END();
   return 1;
+}
+
+// ---------------------------------------------------------------- best-first
+// A frontier about to be split into depth-first halves is first ordered by its
+// children's objective upper bound (descending, per probe): the first half then
+// holds the most promising prefixes, its leaves set an incumbent early and the
+// bound prunes every later chunk.  The order changes only the traversal (every
+// filter is admissible and the chunk merges are order-free), never a result; it
+// also makes the traversal independent of the atomic slot order of k_s2_level.
+
+__global__ void k_fr_keys(const double* key, double* kout, int* perm, const long long* foff,
+                          const long long* fcap, const unsigned long long* fcnt) {
+  const int i = blockIdx.y;
+  const long long cap = fcap[i];
+  const long long m = min((long long)fcnt[i], cap);
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < cap;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long s = foff[i] + k;
+    kout[s] = k < m ? key[s] : -INFINITY;
+    perm[s] = (int)s;
+  }
+}
+
+__global__ void k_fr_gather(const uint16_t* src, uint16_t* dst, const int* perm, const long long* foff,
+                            const long long* fcap, int T) {
+  const int i = blockIdx.y;
+  const long long cap = fcap[i];
+  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < cap;
+       k += (long long)gridDim.x * blockDim.x) {
+    const long long s = foff[i] + k;
+    const long long f = perm[s];
+    for (int q = 0; q < T; ++q) dst[s * T + q] = src[f * T + q];
+  }
+}
+
+int launch_frontier_best_first(const double* key, uint16_t* rows, uint16_t* rows_tmp, double* k_tmp,
+                               double* k_out, int* perm, int* perm_out, void* sort_tmp,
+                               size_t* sort_bytes, const long long* foff, const long long* fcap,
+                               const long long* seg_end, const unsigned long long* fcnt, int n,
+                               long long n_slots, long long max_cap, int T, cudaStream_t st) {
+  // sort_tmp == nullptr: only report the scratch the segmented sort needs
+  if (!sort_tmp) {
+    return (int)cub::DeviceSegmentedRadixSort::SortPairsDescending(
+        nullptr, *sort_bytes, k_tmp, k_out, perm, perm_out, (int)n_slots, n, foff, seg_end, 0, 64, st);
+  }
+  const dim3 grid((unsigned)std::min<long long>(64, (max_cap + 255) / 256), (unsigned)n);
+  k_fr_keys<<<grid, 256, 0, st>>>(key, k_tmp, perm, foff, fcap, fcnt);
+  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+      sort_tmp, *sort_bytes, k_tmp, k_out, perm, perm_out, (int)n_slots, n, foff, seg_end, 0, 64, st);
+  if (e != cudaSuccess) return (int)e;
+  k_fr_gather<<<grid, 256, 0, st>>>(rows, rows_tmp, perm_out, foff, fcap, T);
+  return (int)cudaMemcpyAsync(rows, rows_tmp, sizeof(uint16_t) * (size_t)n_slots * T,
+                              cudaMemcpyDeviceToDevice, st);
 }
 
 int launch_stage2_leaf(const S2Args& a, long long n_blocks, cudaStream_t st) {

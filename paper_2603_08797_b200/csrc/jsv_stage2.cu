@@ -18,6 +18,8 @@
 // order-independent and the diagnostic re-run reproduces the reference's kill
 // counts, deepest blocked level and last failed leaf (H5).
 #include <cub/block/block_scan.cuh>
+#include <cub/device/device_segmented_radix_sort.cuh>
+#include <algorithm>
 #include "jsv_internal.cuh"
 #include "jsv_kernels.h"
 
