@@ -93,7 +93,7 @@ enum BufId {
   B_XPART, B_XSACC, B_XRANK, B_XSCAP, B_XSLAT, B_XPACK, B_FOACT,
   B_FOCLS, B_FONCLS, B_FOF, B_FOB0, B_FOTAU, B_FOCAND, B_FONCAND, B_FOOVF, B_SURV, B_PCNT, B_SBST, B_SCNT, B_WL0, B_WL1, B_WL2, B_WN, B_ARRL, B_REP, B_FSORT, B_ARRF,
   B_BFKEY, B_BFWAYS, B_BFPART, B_BFOUT, B_SRT_KTMP, B_SRT_KOUT, B_SRT_PERM, B_SRT_PERMO,
-  B_SRT_TMP, B_SRT_ROWS, B_SRT_SEGE, B_COUNT
+  B_SRT_TMP, B_SRT_ROWS, B_SRT_SEGE, B_JOBMAP, B_COUNT
 };
 
 struct jsv_context {
@@ -713,6 +713,30 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_WAYS].ensure(sizeof(unsigned) * std::max<size_t>(1, pl.ways.size())));
   CK(B[B_TILE_TASK].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_task.size())));
   CK(B[B_TILE_START].ensure(sizeof(int) * std::max<size_t>(1, pl.tile_start.size())));
+  // fused Stage 1 with more jobs than SMs but fewer than two per SM: every job on a
+  // whole SM (1024 threads), the largest demands (the most candidates) first, so the
+  // second wave holds the smallest jobs (measured: 192 XR jobs 346 -> ~200 us against
+  // 512 threads two per SM; JSV_S1_SPLIT: the largest on 1024 threads and the rest
+  // two per SM at 512, one wave -- 265 us)
+  int n_sm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long jobs1 = (long long)n_s1 * T;
+  std::vector<int> jmap;
+  int n_heavy = 0;
+  // (up to three jobs per SM: 384 XR jobs 0.525 -> 0.478 ms; at 768 the 512-thread
+  // pairs are 2% faster)
+  if (jobs1 > n_sm && jobs1 < 3LL * n_sm && !getenv("JSV_NO_S1SPLIT")) {
+    n_heavy = getenv("JSV_S1_SPLIT") ? (int)(2LL * n_sm - jobs1) : (int)jobs1;
+    jmap.resize((size_t)jobs1);
+    for (int j = 0; j < (int)jobs1; ++j) jmap[j] = j;
+    std::stable_sort(jmap.begin(), jmap.end(),
+                     [&](int x, int y) { return probes[x / T].demand > probes[y / T].demand; });
+  }
+  CK(B[B_JOBMAP].ensure(sizeof(int) * std::max<size_t>(1, jmap.size())));
   {
     // the batch's inputs staged in pinned memory: truly asynchronous copies
     // (pageable sources would each be a staged, host-blocking transfer)
@@ -722,7 +746,8 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
                       {B[B_DESC].p, pl.desc.data(), sizeof(GenDesc) * pl.desc.size()},
                       {B[B_WAYS].p, pl.ways.data(), sizeof(unsigned) * pl.ways.size()},
                       {B[B_TILE_TASK].p, pl.tile_task.data(), sizeof(int) * pl.tile_task.size()},
-                      {B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size()}};
+                      {B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size()},
+                      {B[B_JOBMAP].p, jmap.data(), sizeof(int) * jmap.size()}};
     size_t total = 0;
     for (const Up& u : ups) total += (u.bytes + 15) & ~size_t(15);
     char* h = static_cast<char*>(c.pinned(total));
@@ -887,7 +912,10 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     CK(cudaMemsetAsync(B[B_S1TESTS].p, 0, 2 * sizeof(unsigned long long), st));
     a.tests = B[B_S1TESTS].as<unsigned long long>();
     a.tma = getenv("JSV_NO_TMA") ? 0 : 1;
-    c.stats.kernel_launches += launch_stage1_fused(a, smem, st);
+    a.job_map = n_heavy ? B[B_JOBMAP].as<int>() : nullptr;
+    a.job_off = 0;
+    c.stats.kernel_launches += launch_stage1_fused(a, smem, n_heavy, st, c.st2, c.fork, c.join);
+    a.job_map = nullptr;
     if (phases) {
       // mean phase durations over the jobs (diagnostics on stderr)
       std::vector<unsigned long long> h(10 * (size_t)n_s1 * T);

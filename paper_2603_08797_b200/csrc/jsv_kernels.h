@@ -125,6 +125,11 @@ struct S1Args {
   unsigned long long* stamps;  // JSV_S1_PHASES: [jobs x 10] phase timestamps (else null)
   unsigned long long* tests;   // fused Stage 1: [2] skyline pair tests (float shadow, exact)
   int tma;        // fused Stage 1: stage the task's tables with cp.async.bulk (JSV_NO_TMA: loops)
+  // fused Stage 1 split launch: block b of the launch runs job job_map[job_off + b]
+  // (null: job = b).  Heavy jobs (largest demand) get a whole SM of 1024 threads,
+  // the rest share SMs two by two at 512 threads, all in one wave.
+  const int* job_map;
+  int job_off;
 };
 
 struct S1Launch {
@@ -141,7 +146,8 @@ int stage1_padded_dims(int D);
 int launch_stage1(const S1Args& a, const S1Launch& L, cudaStream_t st);
 int launch_stage1_expand(const S1Args& a, const int* rep, int n_s1, int n, cudaStream_t st);
 size_t s1_fused_smem(int D, int NB, int cap);
-int launch_stage1_fused(const S1Args& a, size_t smem, cudaStream_t st);
+int launch_stage1_fused(const S1Args& a, size_t smem, int n_heavy, cudaStream_t st, cudaStream_t st2,
+                        cudaEvent_t fork, cudaEvent_t join);
 
 // ------------------------------------------------------------------ stage 2
 

@@ -291,7 +291,7 @@ __device__ void push_items(const S1Args& a, int k, int job, int n, int jchunk, b
 #define JOB_BS 512
 __global__ void __launch_bounds__(JOB_BS, 2) k_bucket(const __grid_constant__ S1Args a) {
   extern __shared__ int hist[];
-  const int job = blockIdx.x;
+  const int job = a.job_map ? a.job_map[a.job_off + blockIdx.x] : blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const int n = a.cnt[job];
   const int NB = a.S + 2;
@@ -1091,7 +1091,7 @@ __device__ __forceinline__ void s1_scan_inplace(typename Scan::TempStorage& tmp,
     if (a.stamps && threadIdx.x == 0) {                                        \
       unsigned long long t_;                                                   \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
-      a.stamps[blockIdx.x * 10 + (k)] = t_;                                    \
+      a.stamps[job * 10 + (k)] = t_;                                    \
     }                                                                          \
   } while (0)
 // S1F_THREADS: 1024 (one block per SM, small batches: the most threads per job) or
@@ -1102,6 +1102,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   typedef cub::BlockScan<int, S1F_THREADS> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_n, s_carry, s_ok;
+  __shared__ unsigned s_tests[2];  // float-shadow / exact pair tests of the job
   __shared__ int s_work[3];  // dynamic work counters: units (A), list positions (D), survivors (F)
   __shared__ __align__(8) unsigned long long s_bar;  // TMA staging of the task's tables
   __shared__ void* s_kptr[4];                        // staged key tables (lat, thr, var, cost)
@@ -1109,7 +1110,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   __shared__ double s_rd[32];
   __shared__ int s_ri[32];
   __shared__ double s_ra[32];
-  const int job = blockIdx.x;
+  const int job = a.job_map ? a.job_map[a.job_off + blockIdx.x] : (int)blockIdx.x;
   const int probe = job / a.T, t = job % a.T;
   const long long tot = (long long)a.n_probes * a.C_probe;
   const long long base = job_base(a, probe, t);
@@ -1122,6 +1123,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   if (tid == 0) {
     s_n = 0;
     s_work[0] = s_work[1] = s_work[2] = 0;
+    s_tests[0] = s_tests[1] = 0;
   }
   S1_STAMP(0);
   __syncthreads();
@@ -1416,8 +1418,8 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
     if (lane == 0) k0 = atomicAdd(&s_work[2], 32);
     k0 = __shfl_sync(0xffffffffu, k0, 0);
     if (k0 >= ns) break;
-    const int k = k0 + lane;
-    if (k >= ns) continue;
+    if (k0 + lane >= ns) continue;
+    const int k = ns - 1 - (k0 + lane);  // (the most slices -- the longest scans -- first)
     const int ci = ord[survp[k]];
     double xi[D];
 #pragma unroll
@@ -1447,15 +1449,16 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   }
   __syncthreads();
   S1_STAMP(5);
+  // pair-test counters: warp sums into shared memory, one global add per job at the end
   if (a.tests) {
-    unsigned long long sh = n_sh, ex = n_ex;
+    unsigned sh = n_sh, ex = n_ex;
     for (int d = 16; d > 0; d >>= 1) {
       sh += __shfl_down_sync(0xffffffffu, sh, d);
       ex += __shfl_down_sync(0xffffffffu, ex, d);
     }
     if (lane == 0) {
-      atomicAdd(&a.tests[0], sh);
-      atomicAdd(&a.tests[1], ex);
+      atomicAdd(&s_tests[0], sh);
+      atomicAdd(&s_tests[1], ex);
     }
   }
   // ---- G: the frontier in candidate order
@@ -1664,6 +1667,10 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
     msl = min(msl, s_ri[0]);
     macc = fmax(macc, s_ra[0]);
     a.pool_n[job] = P;
+    if (a.tests) {
+      atomicAdd(&a.tests[0], (unsigned long long)s_tests[0]);
+      atomicAdd(&a.tests[1], (unsigned long long)s_tests[1]);
+    }
     a.pool_min_lat2[job] = mlat;
     a.pool_min_sl[job] = msl;
     a.pool_acc_ub[job] = macc;
@@ -1682,35 +1689,54 @@ size_t s1_fused_smem(int D, int NB, int cap) {
   return fixed + std::max(lists, sort);
 }
 
-int launch_stage1_fused(const S1Args& a, size_t smem, cudaStream_t st) {
+int launch_stage1_fused(const S1Args& a, size_t smem, int n_heavy, cudaStream_t st, cudaStream_t st2,
+                        cudaEvent_t fork, cudaEvent_t join) {
   const long long jobs = (long long)a.n_probes * a.T;
   int dev = 0, n_sm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-#define JSV_S1F(DV, NT)                                                                              \
-  do {                                                                                               \
-    jsv_smem_attr((const void*)k_s1_job<DV, NT>, smem);                                    \
-    k_s1_job<DV, NT><<<(unsigned)jobs, NT, smem, st>>>(a);                                           \
+#define JSV_S1F(DV, NT, GRID, ARGS, STREAM)                                        \
+  do {                                                                             \
+    jsv_smem_attr((const void*)k_s1_job<DV, NT>, smem);                            \
+    k_s1_job<DV, NT><<<(unsigned)(GRID), NT, smem, STREAM>>>(ARGS);                \
   } while (0)
-#define JSV_S1FD(NT)                  \
-  switch (a.D) {                      \
-    case 4: JSV_S1F(4, NT); break;    \
-    case 5: JSV_S1F(5, NT); break;    \
-    case 6: JSV_S1F(6, NT); break;    \
-    case 8: JSV_S1F(8, NT); break;    \
-    case 12: JSV_S1F(12, NT); break;  \
-    default: JSV_S1F(16, NT); break;  \
+#define JSV_S1FD(NT, GRID, ARGS, STREAM)             \
+  switch (a.D) {                                     \
+    case 4: JSV_S1F(4, NT, GRID, ARGS, STREAM); break;   \
+    case 5: JSV_S1F(5, NT, GRID, ARGS, STREAM); break;   \
+    case 6: JSV_S1F(6, NT, GRID, ARGS, STREAM); break;   \
+    case 8: JSV_S1F(8, NT, GRID, ARGS, STREAM); break;   \
+    case 12: JSV_S1F(12, NT, GRID, ARGS, STREAM); break; \
+    default: JSV_S1F(16, NT, GRID, ARGS, STREAM); break; \
   }
   PROF_BEGIN(K_GENERATE);
-  if (jobs <= n_sm) {
-    JSV_S1FD(1024);
+  int launches = 1;
+  if (a.job_map && n_heavy >= jobs) {
+    // every job on 1024 threads in job_map's order (largest first: the second
+    // wave's jobs are the smallest and start as the first SMs free up)
+    JSV_S1FD(1024, jobs, a, st);
+  } else if (a.job_map && n_heavy > 0) {
+    // one wave: the n_heavy jobs of job_map's head on 1024 threads (one per SM) on
+    // st, the rest at 512 threads two per SM on st2 (joined back into st)
+    S1Args h = a, l = a;
+    h.job_off = 0;
+    l.job_off = n_heavy;
+    cudaEventRecord(fork, st);
+    cudaStreamWaitEvent(st2, fork, 0);
+    JSV_S1FD(1024, n_heavy, h, st);
+    JSV_S1FD(512, jobs - n_heavy, l, st2);
+    cudaEventRecord(join, st2);
+    cudaStreamWaitEvent(st, join, 0);
+    launches = 2;
+  } else if (jobs <= n_sm) {
+    JSV_S1FD(1024, jobs, a, st);
   } else {
-    JSV_S1FD(512);
+    JSV_S1FD(512, jobs, a, st);
   }
   PROF_END();
 #undef JSV_S1FD
 #undef JSV_S1F
-  return 1;
+  return launches;
 }
 
 // ------------------------------------------------------------------ launchers
