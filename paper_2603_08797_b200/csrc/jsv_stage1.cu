@@ -1505,8 +1505,15 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   if (s_ok) {
     // sort 1: rows, lexicographic (distinct rows: the sorted rank is the count of
     // smaller rows; padding rows +inf, ties by index)
+    // (a stage with j <= 32 pairs elements inside one 64-element block, and the 32
+    // consecutive h of a warp cover whole blocks: such a stage needs only the warp's
+    // own earlier writes -- __syncwarp -- unless the stage before it crossed warps)
+    int pj = F2;
     for (int kk = 2; kk <= F2; kk <<= 1) {
       for (int j = kk >> 1; j > 0; j >>= 1) {
+        if (j >= 64 || pj >= 64) __syncthreads();
+        else __syncwarp();
+        pj = j;
         for (int h = tid; h < (F2 >> 1); h += S1F_THREADS) {
           const int i = ((h & ~(j - 1)) << 1) | (h & (j - 1)), l = i | j;
           const int x = ix[i], y = ix[l];
@@ -1524,17 +1531,21 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
             ix[l] = x;
           }
         }
-        __syncthreads();
       }
     }
+    __syncthreads();
     for (int r = tid; r < F; r += S1F_THREADS) fpos[ix[r]] = r;
     if (F > a.W) {
       __syncthreads();
       for (int k = tid; k < F2; k += S1F_THREADS) ix[k] = k;
       __syncthreads();
       // sort 2: (-capacity, slices, items); padding -capacity = +inf
+      pj = F2;
       for (int kk = 2; kk <= F2; kk <<= 1) {
         for (int j = kk >> 1; j > 0; j >>= 1) {
+          if (j >= 64 || pj >= 64) __syncthreads();
+          else __syncwarp();
+          pj = j;
           for (int h = tid; h < (F2 >> 1); h += S1F_THREADS) {
             const int i = ((h & ~(j - 1)) << 1) | (h & (j - 1)), l = i | j;
             const int x = ix[i], y = ix[l];
@@ -1550,9 +1561,9 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
               ix[l] = x;
             }
           }
-          __syncthreads();
         }
       }
+      __syncthreads();
       for (int r = tid; r < F; r += S1F_THREADS) fcr[ix[r]] = r;
     }
   } else {
