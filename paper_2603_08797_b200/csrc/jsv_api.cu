@@ -953,13 +953,18 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   // stage1_collect after the caller's next synchronisation (Stage 2 of exhaustive
   // probes is planned on the device, so no host round trip sits between the stages)
   {
-    const size_t bytes = sizeof(long long) * 3 + sizeof(int) * (size_t)jobs;
+    // (+ the generated and frontier counts per job: the batch statistics, read here
+    // instead of by two synchronous copies after the batch)
+    const size_t bytes = sizeof(long long) * 3 + 3 * sizeof(int) * (size_t)jobs;
     char* h = static_cast<char*>(c.pinned(bytes, 2));
     if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
     memset(h, 0, sizeof(long long) * 3);
     if (a.tests) CK(cudaMemcpyAsync(h, a.tests, 2 * sizeof(long long), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h + 2 * sizeof(long long), a.err, sizeof(int), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h + 3 * sizeof(long long), a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost,
+    char* hp = h + 3 * sizeof(long long);
+    CK(cudaMemcpyAsync(hp, a.pool_n, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + sizeof(int) * jobs, a.cnt, sizeof(int) * jobs, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hp + 2 * sizeof(int) * jobs, a.fcnt, sizeof(int) * jobs, cudaMemcpyDeviceToHost,
                        st));
   }
   bs.s1_pending = true;
@@ -982,6 +987,18 @@ static int stage1_collect(jsv_problem& p, BatchState& bs) {
   memcpy(bs.pool_n.data(), h + 3 * sizeof(long long), sizeof(int) * jobs);
   c.stats.s1_shadow_tests += (long long)tests[0];
   c.stats.s1_exact_tests += (long long)tests[1];
+  {
+    const int* cnt = reinterpret_cast<const int*>(h + 3 * sizeof(long long)) + jobs;
+    const int* fc = cnt + jobs;
+    long long gen = 0;
+    for (size_t i = 0; i < jobs; ++i) {
+      gen += cnt[i];
+      c.stats.pair_tests_a += (long long)cnt[i] * cnt[i];
+      c.stats.pair_tests_b += (long long)fc[i] * fc[i];
+    }
+    c.stats.candidates_generated += gen;
+    c.stats.dims = bs.s1.D;
+  }
   if (err) return fail(JSV_ERR_CAPACITY, "stage-1 candidate capacity exceeded (code " +
                                              std::to_string(err) + ")");
   bs.dead.assign(n, 0);
@@ -2050,19 +2067,6 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   c.stats.ms_stage1 += ms1;
   c.stats.ms_stage2 += ms2;
   c.stats.ms_total += mst;
-  long long gen = 0;
-  {
-    std::vector<int> cnt((size_t)n * p.T), fc((size_t)n * p.T);
-    CK(cudaMemcpy(cnt.data(), bs.s1.cnt, sizeof(int) * cnt.size(), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(fc.data(), bs.s1.fcnt, sizeof(int) * fc.size(), cudaMemcpyDeviceToHost));
-    for (size_t i = 0; i < cnt.size(); ++i) {
-      gen += cnt[i];
-      c.stats.pair_tests_a += (long long)cnt[i] * cnt[i];
-      c.stats.pair_tests_b += (long long)fc[i] * fc[i];
-    }
-    c.stats.dims = bs.s1.D;
-  }
-  c.stats.candidates_generated += gen;
   return JSV_OK;
 }
 
