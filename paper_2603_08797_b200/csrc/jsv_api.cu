@@ -491,8 +491,27 @@ static void acc_threshold(double a_max, double s, double& thr, int& ok) {
   ok = 1;
 }
 
+// The factor products of a request (independent of demand): computed once per batch
+struct ProbeFactors {
+  double up[2][MAXE];  // _demand_upper_bound, A' off / on
+  double cz[MAXE];     // could_zero (the request's own A)
+  double uni[MAXE];    // plan_uninformed (A off, upper)
+};
+
+static void probe_factors(const jsv_problem& p, const jsv_request& rq, ProbeFactors& f) {
+  host_factors(p, rq, false, true, f.up[0]);
+  host_factors(p, rq, true, true, f.up[1]);
+  host_factors(p, rq, (rq.space & JSV_SPACE_A) != 0, false, f.cz);
+  host_factors(p, rq, false, true, f.uni);
+}
+
 static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_probe& in,
-                       DProbe& o) {
+                       DProbe& o, const ProbeFactors* pf = nullptr) {
+  ProbeFactors own;
+  if (!pf) {
+    probe_factors(p, rq, own);
+    pf = &own;
+  }
   memset(&o, 0, sizeof(o));
   o.demand = in.demand;
   o.slo_eff = in.slo_eff;
@@ -511,14 +530,12 @@ static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_pr
     o.acc_thr = c_thr;
     o.acc_thr_ok = c_ok;
   }
-  double fac[MAXE], r[MAXT];
+  double r[MAXT];
   for (int a = 0; a < 2; ++a) {
-    host_factors(p, rq, a == 1, true, fac);
-    host_rates(p, in.demand, fac, r);
+    host_rates(p, in.demand, pf->up[a], r);
     for (int t = 0; t < p.T; ++t) o.r_upper[a][t] = r[t];
   }
-  host_factors(p, rq, (rq.space & JSV_SPACE_A) != 0, false, fac);
-  host_rates(p, in.demand, fac, r);
+  host_rates(p, in.demand, pf->cz, r);
   o.could_zero = 0;
   for (int t = 0; t < p.T; ++t)
     if (r[t] == 0.0) o.could_zero |= 1u << t;
@@ -532,8 +549,7 @@ static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_pr
   }
   if (!(rq.space & JSV_SPACE_T)) {
     // plan_uninformed demand-dependent budgets (planner.py:1014-1037)
-    host_factors(p, rq, false, true, fac);
-    host_rates(p, in.demand, fac, r);
+    host_rates(p, in.demand, pf->uni, r);
     double est[MAXT], est_decl[MAXT];
     for (int t = 0; t < p.T; ++t) {
       o.star[t] = r[t];
@@ -1904,7 +1920,9 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   // back at the end.
   JSV_T("batch entry");
   std::vector<DProbe> fp(n);
-  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i]);
+  ProbeFactors pf;
+  probe_factors(p, rq, pf);
+  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i], &pf);
   JSV_T("probes filled");
   std::vector<int> perm;  // batch slot -> caller index
   std::vector<int> rep;   // batch slot -> slot whose Stage-1 pools it shares

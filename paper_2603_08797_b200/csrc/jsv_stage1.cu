@@ -1066,6 +1066,47 @@ __device__ __forceinline__ int s1_compact_slot(typename Scan::TempStorage& tmp, 
   return keep ? base + off : -1;
 }
 
+// stable block-wide compaction of [0, n) with two block barriers: warp w owns one
+// contiguous chunk, counts its kept entries by ballots, takes its base from the
+// per-warp counts and emits (slot, index) in order.  keep(i) is evaluated twice
+// (it must be a pure read); emit(k, i) is called for the k-th kept i.  Returns the
+// kept count (every thread).
+template <int NT, class Keep, class Emit>
+__device__ __forceinline__ int s1_compact_warps(int n, int* s_wcnt, Keep keep, Emit emit) {
+  constexpr int NW = NT / 32;
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int chunk = (((n + NW - 1) / NW) + 31) & ~31;
+  const int c0 = min(n, w * chunk), c1 = min(n, c0 + chunk);
+  int cnt = 0;
+  for (int b = c0; b < c1; b += 32) {
+    const int i = b + lane;
+    cnt += __popc(__ballot_sync(FULL, i < c1 && keep(i)));
+  }
+  if (lane == 0) s_wcnt[w] = cnt;
+  __syncthreads();
+  int before = 0, total = 0;
+  for (int x = lane; x < NW; x += 32) {
+    const int v = s_wcnt[x];
+    total += v;
+    if (x < w) before += v;
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    before += __shfl_xor_sync(FULL, before, d);
+    total += __shfl_xor_sync(FULL, total, d);
+  }
+  for (int b = c0; b < c1; b += 32) {
+    const int i = b + lane;
+    const bool k = i < c1 && keep(i);
+    const unsigned m = __ballot_sync(FULL, k);
+    if (k) emit(before + __popc(m & ((1u << lane) - 1u)), i);
+    before += __popc(m);
+  }
+  __syncthreads();  // (s_wcnt reusable, every emit visible)
+  return total;
+}
+
 // exclusive bucket starts in place over h[0 .. nb) (h[i] holds the count of i - 1)
 template <class Scan, int S1F_THREADS>
 __device__ __forceinline__ void s1_scan_inplace(typename Scan::TempStorage& tmp, int* h, int nb,
@@ -1103,6 +1144,7 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int s_n, s_carry, s_ok;
   __shared__ unsigned s_tests[2];  // float-shadow / exact pair tests of the job
+  __shared__ int s_wcnt[S1F_THREADS / 32];  // per-warp counts of s1_compact_warps
   __shared__ int s_work[3];  // dynamic work counters: units (A), list positions (D), survivors (F)
   __shared__ __align__(8) unsigned long long s_bar;  // TMA staging of the task's tables
   __shared__ void* s_kptr[4];                        // staged key tables (lat, thr, var, cost)
@@ -1396,22 +1438,15 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
   __syncthreads();
   S1_STAMP(4);
   // ---- E: survivors in list order and their bucket starts
-  if (tid == 0) s_carry = 0;
   for (int s0 = tid; s0 < NB; s0 += S1F_THREADS) sbst[s0] = 0;
   __syncthreads();
-  for (int p0 = 0; p0 < nl; p0 += S1F_THREADS) {
-    const int p = p0 + tid;
-    const bool keep = p < nl && !dead[ord[p]];
-    const int k = s1_compact_slot<Scan>(tmp, &s_carry, keep);
-    if (k >= 0) {
-      survp[k] = p;
-      sslp[k] = slp[p];
-      atomicAdd(&sbst[slp[p] + 1], 1);
-    }
-  }
-  __syncthreads();
-  const int ns = s_carry;
-  __syncthreads();  // (every thread has read the count before the scan reuses s_carry)
+  const int ns = s1_compact_warps<S1F_THREADS>(
+      nl, s_wcnt, [&](int p) { return !dead[ord[p]]; },
+      [&](int k, int p) {
+        survp[k] = p;
+        sslp[k] = slp[p];
+        atomicAdd(&sbst[slp[p] + 1], 1);
+      });
   s1_scan_inplace<Scan, S1F_THREADS>(tmp, sbst, NB, &s_carry);
   // ---- F: survivors against the survivors with fewer slices
   for (int k0 = 0;;) {
@@ -1462,15 +1497,8 @@ __global__ void __launch_bounds__(S1F_THREADS, 2048 / S1F_THREADS / 2) k_s1_job(
     }
   }
   // ---- G: the frontier in candidate order
-  if (tid == 0) s_carry = 0;
-  __syncthreads();
-  for (int c0 = 0; c0 < n; c0 += S1F_THREADS) {
-    const int c = c0 + tid;
-    const int k = s1_compact_slot<Scan>(tmp, &s_carry, c < n && !dead[c]);
-    if (k >= 0) front[k] = c;
-  }
-  __syncthreads();
-  const int F = s_carry;
+  const int F = s1_compact_warps<S1F_THREADS>(
+      n, s_wcnt, [&](int c) { return !dead[c]; }, [&](int k, int c) { front[k] = c; });
   if (tid == 0) a.fcnt[job] = F;
 
   S1_STAMP(6);

@@ -133,6 +133,30 @@ def test_alternative_kernel_paths_match_reference(env, monkeypatch):
         planner.set_strategy("auto")
 
 
+@pytest.mark.parametrize("env", [{}, {"JSV_S1_SPLIT": "1"}, {"JSV_NO_S1SPLIT": "1"},
+                                 {"JSV_NO_S1DEDUP": "1"}, {"JSV_NO_S1DEDUP": "1", "JSV_NO_S1SPLIT": "1"}])
+def test_stage1_job_scheduling_matches_reference(env, monkeypatch):
+    """Fused Stage-1 job scheduling -- 1,024-thread blocks in largest-demand-first order
+    for 148..443 jobs (default), the one-wave split of 1,024- and 512-thread blocks
+    (JSV_S1_SPLIT), 512-thread pairs (JSV_NO_S1SPLIT) -- changes no result: the bench's
+    64 solves (192 jobs) twice in one batch (192 jobs after Stage-1 dedup, 384 without)."""
+    from paper_2603_08797_b200 import planner, workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    app, table = workloads.xr()
+    rows = load("bench_xr64.json")["solves"]
+    reqs = [PlanRequest(r["demand"], 28, SearchSpace(True, True, True)) for r in rows]
+    planner.set_strategy("exhaustive", EXH_LIMIT)
+    try:
+        got = planner.plan_batch(app, table, reqs + reqs)
+    finally:
+        planner.set_strategy("auto")
+    for r, res in zip(rows + rows, got):
+        assert result_dict(res) == r["result"], r["demand"]
+
+
 def _check_md(P, doc):
     from paper_2603_08797_b200.model import app_from_dict
     from paper_2603_08797_b200.plan_types import SearchSpace
