@@ -512,14 +512,22 @@ __device__ __forceinline__ bool x_take(const XArgs& a, int probe, int tl, long l
   cb.sl = sl_pre + sl;
   cb.obj = alpha * (Wx / a_max) - beta * (double)cb.sl;
   cb.idx = qp * R + b;
-  cb.mk = a.mkey ? (pk | x_mk_task(a.s, probe, tl, bc, later)) : 0ull;
-  bool take;
+  // (the packed m key -- a dependent global load -- only when it decides a tie or
+  // the candidate is taken: most feasible leaves lose on the objective)
+  cb.mk = 0ull;
+  bool take, have_mk = false;
   if (!rb.has || a.mode != LEAF_FULL) take = !rb.has;
   else if (cb.obj != rb.obj) take = cb.obj > rb.obj;
   else if (cb.sl != rb.sl) take = cb.sl < rb.sl;
-  else if (a.mkey) take = cb.mk < rb.mk;
-  else take = x_sink_cmp(a.s, probe, tl, b, (int)(rb.idx - qp * R), later) < 0;
-  if (take) rb = cb;
+  else if (a.mkey) {
+    cb.mk = pk | x_mk_task(a.s, probe, tl, bc, later);
+    have_mk = true;
+    take = cb.mk < rb.mk;
+  } else take = x_sink_cmp(a.s, probe, tl, b, (int)(rb.idx - qp * R), later) < 0;
+  if (take) {
+    if (a.mkey && !have_mk) cb.mk = pk | x_mk_task(a.s, probe, tl, bc, later);
+    rb = cb;
+  }
   return a.mode != LEAF_FULL;  // feasible-only: first feasible of this lane (b ascending)
 }
 
