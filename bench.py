@@ -572,7 +572,9 @@ def main() -> None:
         dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
-    N.profile(ctx, True)
+    # (events only around the two roofline kernels: an event pair around every launch
+    # of the step would add ~8% of host gaps to the device time it measures)
+    N.profile(ctx, True, ("generate", "s2_exh"))
     dev_ms = e2e_ms = 0.0
     launches = 0
     tot = {"exh_candidates": 0, "leaves": 0, "swept": 0, "live_prefixes": 0, "ms_total": 0.0,

@@ -288,8 +288,9 @@ int jsv_plan_batch_shard(jsv_context* ctx, const jsv_problem* prob, const jsv_re
                          jsv_plan_out* out);
 
 /* Per-kernel CUDA-event timing on the library stream (bench roofline).
- * jsv_profile(on) resets the accumulators; jsv_kernel_times fills ms[k] /
- * count[k] for kernel ids 0..n-1 (see JSV_KERNEL_NAMES) and returns the id count. */
+ * jsv_profile(on) resets the accumulators; on = 0 off, 1 every kernel, or
+ * (1 << 30) | mask for only the kernels whose id bit is set.  jsv_kernel_times fills
+ * ms[k] / count[k] for kernel ids 0..n-1 (see JSV_KERNEL_NAMES) and returns the id count. */
 int jsv_profile(jsv_context* ctx, int on);
 int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* count);
 #define JSV_KERNEL_NAMES \

@@ -151,8 +151,12 @@ def set_shard(ctx, rank: int, world: int) -> None:
     check(load_library().jsv_set_shard(ctx, int(rank), int(world)))
 
 
-def profile(ctx, on: bool) -> None:
-    check(load_library().jsv_profile(ctx, 1 if on else 0))
+def profile(ctx, on: bool, kernels=None) -> None:
+    """Per-kernel CUDA events on/off; ``kernels`` (names of KERNEL_NAMES) limits them."""
+    arg = 1 if on else 0
+    if on and kernels is not None:
+        arg = (1 << 30) | sum(1 << KERNEL_NAMES.index(k) for k in kernels)
+    check(load_library().jsv_profile(ctx, arg))
 
 
 def kernel_times(ctx) -> dict:

@@ -161,7 +161,10 @@ struct ProfScope {
 extern "C" int jsv_profile(jsv_context* ctx, int on) {
   if (!ctx) return fail(JSV_ERR_ARG, "null argument");
   std::lock_guard<std::recursive_mutex> lock_(ctx->mu);
+  // on: 0 off, 1 every kernel, or (1 << 30) | mask -- only the kernels whose K_ id
+  // bit is set (fewer event records inside a timed region)
   ctx->prof.on = on != 0;
+  ctx->prof.mask = (on & (1 << 30)) ? (unsigned)(on & ((1 << 30) - 1)) : ~0u;
   ctx->prof.st = ctx->st;
   for (int k = 0; k < K_COUNT_; ++k) {
     ctx->kms[k] = 0.0;
@@ -1928,20 +1931,44 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   std::vector<int> rep;   // batch slot -> slot whose Stage-1 pools it shares
   int n_s1 = n;
   {
-    std::unordered_map<std::string, int> seen;
-    seen.reserve(2 * (size_t)n);
+    // probes whose Stage-1 inputs (both r_upper rows) are bit-identical share one
+    // Stage 1: a 64-bit hash of the rows per probe, the hash set verified by memcmp
     const bool no_dedup = getenv("JSV_NO_S1DEDUP") != nullptr;
+    const size_t row = sizeof(double) * p.T;
+    auto same = [&](int x, int y) {
+      return memcmp(fp[x].r_upper[0], fp[y].r_upper[0], row) == 0 &&
+             memcmp(fp[x].r_upper[1], fp[y].r_upper[1], row) == 0;
+    };
+    std::unordered_map<unsigned long long, int> seen;  // hash -> first slot (chained below)
+    seen.reserve(2 * (size_t)n);
+    std::vector<int> chain(n, -1);  // next probe index with the same hash
+    std::vector<int> slot_of(n, -1);
     std::vector<int> first, dups, dup_rep;
     for (int i = 0; i < n; ++i) {
-      std::string key(reinterpret_cast<const char*>(fp[i].r_upper[0]), sizeof(double) * p.T);
-      key.append(reinterpret_cast<const char*>(fp[i].r_upper[1]), sizeof(double) * p.T);
-      auto it = seen.find(key);
-      if (it == seen.end() || no_dedup) {
-        seen.emplace(key, (int)first.size());
+      unsigned long long h = 1469598103934665603ull;
+      for (int a = 0; a < 2; ++a) {
+        const unsigned char* b = reinterpret_cast<const unsigned char*>(fp[i].r_upper[a]);
+        for (size_t k = 0; k < row; ++k) h = (h ^ b[k]) * 1099511628211ull;
+      }
+      int match = -1;
+      auto it = seen.find(h);
+      if (it != seen.end() && !no_dedup)
+        for (int j = it->second; j >= 0; j = chain[j])
+          if (same(i, j)) {
+            match = j;
+            break;
+          }
+      if (match < 0) {
+        slot_of[i] = (int)first.size();
         first.push_back(i);
+        if (it == seen.end()) seen.emplace(h, i);
+        else {
+          chain[i] = it->second;
+          it->second = i;
+        }
       } else {
         dups.push_back(i);
-        dup_rep.push_back(it->second);
+        dup_rep.push_back(slot_of[match]);
       }
     }
     n_s1 = (int)first.size();

@@ -11,6 +11,8 @@ enum KernelId {
 
 struct Prof {
   bool on = false;
+  unsigned mask = ~0u;  // kernels (bit = K_ id) that get an event pair
+  bool cur = false;     // the open begin_on was recorded
   cudaStream_t st = nullptr;
   std::vector<cudaEvent_t> ev;
   std::vector<int> ids;
@@ -20,7 +22,8 @@ struct Prof {
   // events on the kernel's own stream (kernels of a side stream overlap the main one:
   // their times are their own, not a share of a serial step)
   void begin_on(int id, cudaStream_t s) {
-    if (!on) return;
+    cur = on && ((mask >> id) & 1u);
+    if (!cur) return;
     if (used + 2 > ev.size()) {
       for (int i = 0; i < 64; ++i) {
         cudaEvent_t e;
@@ -33,7 +36,8 @@ struct Prof {
     cudaEventRecord(ev[used], s);
   }
   void end_on(cudaStream_t s) {
-    if (!on) return;
+    if (!cur) return;
+    cur = false;
     cudaEventRecord(ev[used + 1], s);
     used += 2;
   }
