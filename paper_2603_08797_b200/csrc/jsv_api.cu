@@ -5,6 +5,7 @@
 // structured decision, plan_uninformed slice budgets) mirrors the reference's
 // Python float order exactly; the file is compiled with -ffp-contract=off so
 // no host expression is contracted into an FMA.
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -116,6 +117,10 @@ struct jsv_context {
   // cudaMalloc / cudaFree per call would serialise the device)
   std::vector<std::unique_ptr<DevBuf>> bb_fr, bb_cnt, bb_key;
   int shard_rank = 0, shard_world = 1;
+  // the Stage-1 plan whose descriptor / ways / tile tables are on the device now (and
+  // the buffers they were copied into): the next batch of the same plan skips them
+  unsigned long long s1_up_id = 0;
+  const void* s1_up_ptr[4] = {nullptr, nullptr, nullptr, nullptr};
   // pinned host staging for per-solve tables (one async copy instead of several
   // pageable ones); reused call to call -- every call synchronises before returning
   // (slot 1: the exhaustive probes' records, in flight together with slot 0's
@@ -184,6 +189,7 @@ extern "C" int jsv_kernel_times(jsv_context* ctx, int n, double* ms, int64_t* co
 }
 
 struct S1Plan {
+  unsigned long long id = 0;  // process-unique (the device copy of the tables is reused by id)
   std::vector<GenDesc> desc;
   std::vector<unsigned> ways;
   std::vector<long long> task_cap;
@@ -691,6 +697,8 @@ static int get_s1plan(jsv_problem& p, const jsv_request& rq, std::shared_ptr<S1P
     return JSV_OK;
   }
   auto pl = std::make_shared<S1Plan>();
+  static std::atomic<unsigned long long> next_id{1};
+  pl->id = next_id++;
   int rc = build_s1plan(p, rq, *pl);
   if (rc) return rc;
   p.s1cache[key] = pl;
@@ -760,13 +768,23 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     // the batch's inputs staged in pinned memory: truly asynchronous copies
     // (pageable sources would each be a staged, host-blocking transfer)
     struct Up { void* dst; const void* src; size_t bytes; };
+    // (the plan's tables only when another plan, or a reallocation, replaced them)
+    const bool plan_resident = c.s1_up_id == pl.id && c.s1_up_ptr[0] == B[B_DESC].p &&
+                               c.s1_up_ptr[1] == B[B_WAYS].p && c.s1_up_ptr[2] == B[B_TILE_TASK].p &&
+                               c.s1_up_ptr[3] == B[B_TILE_START].p && !getenv("JSV_NO_S1CACHE");
+    const size_t ps = plan_resident ? 0 : 1;
     const Up ups[] = {{B[B_REQ].p, &hreq, sizeof(DReq)},
                       {B[B_PROBES].p, probes, sizeof(DProbe) * n},
-                      {B[B_DESC].p, pl.desc.data(), sizeof(GenDesc) * pl.desc.size()},
-                      {B[B_WAYS].p, pl.ways.data(), sizeof(unsigned) * pl.ways.size()},
-                      {B[B_TILE_TASK].p, pl.tile_task.data(), sizeof(int) * pl.tile_task.size()},
-                      {B[B_TILE_START].p, pl.tile_start.data(), sizeof(int) * pl.tile_start.size()},
+                      {B[B_DESC].p, pl.desc.data(), ps * sizeof(GenDesc) * pl.desc.size()},
+                      {B[B_WAYS].p, pl.ways.data(), ps * sizeof(unsigned) * pl.ways.size()},
+                      {B[B_TILE_TASK].p, pl.tile_task.data(), ps * sizeof(int) * pl.tile_task.size()},
+                      {B[B_TILE_START].p, pl.tile_start.data(), ps * sizeof(int) * pl.tile_start.size()},
                       {B[B_JOBMAP].p, jmap.data(), sizeof(int) * jmap.size()}};
+    c.s1_up_id = pl.id;
+    c.s1_up_ptr[0] = B[B_DESC].p;
+    c.s1_up_ptr[1] = B[B_WAYS].p;
+    c.s1_up_ptr[2] = B[B_TILE_TASK].p;
+    c.s1_up_ptr[3] = B[B_TILE_START].p;
     size_t total = 0;
     for (const Up& u : ups) total += (u.bytes + 15) & ~size_t(15);
     char* h = static_cast<char*>(c.pinned(total));

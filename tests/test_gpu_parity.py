@@ -104,7 +104,7 @@ def test_bench_batch_strategies_agree_at_full_size():
                                  {"JSV_NO_PRUNE": "1"}, {"JSV_NO_MKEY": "1"}, {"JSV_NO_SIDE": "1"},
                                  {"JSV_NO_FANOUT": "1"}, {"JSV_DEVICE_PLAN": "1"},
                                  {"JSV_XROUND": "1"}, {"JSV_XROUND": "32"},
-                                 {"JSV_DEVICE_PLAN": "1", "JSV_NO_PRUNE": "1"}])
+                                 {"JSV_DEVICE_PLAN": "1", "JSV_NO_PRUNE": "1"}, {"JSV_NO_S1CACHE": "1"}])
 def test_alternative_kernel_paths_match_reference(env, monkeypatch):
     """Every kernel variant the library can pick (frontier ranks by counting vs by
     sorting, tiled vs barrier-free skyline passes, register vs looped sweep, TMA
