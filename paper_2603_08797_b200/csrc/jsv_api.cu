@@ -828,7 +828,10 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_S1SL].ensure(sizeof(int) * jobs));
   CK(B[B_S1ACC].ensure(sizeof(double) * jobs));
   CK(B[B_ERR].ensure(sizeof(int)));
-  CK(cudaMemsetAsync(B[B_CNT].p, 0, sizeof(int) * jobs, st));
+  // (the fused kernel stores every job's count itself: the zeroing is needed by the
+  // chain's atomic counters and by duplicate probes only)
+  const bool fused_path = D <= 8 && rq.budget + 2 <= 130 && !getenv("JSV_S1_LEGACY");
+  if (!fused_path || n_s1 < n) CK(cudaMemsetAsync(B[B_CNT].p, 0, sizeof(int) * jobs, st));
   CK(cudaMemsetAsync(B[B_ERR].p, 0, sizeof(int), st));
   S1Args& a = bs.s1;
   memset(&a, 0, sizeof(a));
@@ -893,7 +896,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   CK(B[B_WL1].ensure(sizeof(int4) * max_items));
   CK(B[B_WL2].ensure(sizeof(int4) * max_items));
   CK(B[B_WN].ensure(sizeof(int) * 4));
-  CK(cudaMemsetAsync(B[B_WN].p, 0, sizeof(int) * 4, st));
+  if (!fused_path) CK(cudaMemsetAsync(B[B_WN].p, 0, sizeof(int) * 4, st));
   a.wl[0] = B[B_WL0].as<int4>();
   a.wl[1] = B[B_WL1].as<int4>();
   a.wl[2] = B[B_WL2].as<int4>();
@@ -930,7 +933,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   const int NB = rq.budget + 2;
   // (measured: wide rows -- fan-out hubs -- and large budgets, whose jobs outgrow the
   // shared-memory lists, run faster through the multi-kernel chain)
-  const bool fused = D <= 8 && NB <= 130 && !getenv("JSV_S1_LEGACY");
+  const bool fused = fused_path;
   if (fused) {
     const size_t smax = 100 * 1024;  // two blocks per SM (with the static shared memory)
     long long cap = pl.max_cap;

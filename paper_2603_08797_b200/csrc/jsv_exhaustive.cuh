@@ -1655,16 +1655,9 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
                              long long n_upper) {
   if (grid <= 0) return 0;
   int launches = 0;
+  // (the main stream's chain is issued first: the side stream's launches do not
+  // delay the live pass, which is the critical path)
   cudaEventRecord(fork, st);
-  cudaStreamWaitEvent(st2, fork, 0);
-  launches += launch_x_rank(a, st2);
-  if (a.mode == LEAF_FULL) {
-    PROF_BEGIN_ON(K_MRANK, st2);
-    k_m_rank<<<a.s.n_probes * a.s.T, 512, 0, st2>>>(a);
-    PROF_END_ON(st2);
-    ++launches;
-  }
-  cudaEventRecord(join, st2);
   PROF_BEGIN(K_X_LIVE);
   if (n_upper != 0) {
     // one warp per upper prefix (n_upper < 0: counted on the device, grid-stride)
@@ -1675,6 +1668,15 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
   }
   k_x_sched<<<1, 1024, 0, st>>>(a, a.round);
   PROF_END();
+  cudaStreamWaitEvent(st2, fork, 0);
+  launches += launch_x_rank(a, st2);
+  if (a.mode == LEAF_FULL) {
+    PROF_BEGIN_ON(K_MRANK, st2);
+    k_m_rank<<<a.s.n_probes * a.s.T, 512, 0, st2>>>(a);
+    PROF_END_ON(st2);
+    ++launches;
+  }
+  cudaEventRecord(join, st2);
   cudaStreamWaitEvent(st, join, 0);
   PROF_BEGIN(K_S2_EXH);
   JSV_XDISPATCH(JSV_XLAUNCH);
