@@ -105,6 +105,8 @@ struct jsv_context {
   cudaStream_t st = nullptr;
   cudaStream_t st2 = nullptr;               // side stream for independent kernels of a call
   cudaEvent_t fork = nullptr, join = nullptr;  // st -> st2 -> st ordering (no timing)
+  cudaStream_t st3 = nullptr;                  // second side stream (exhaustive m keys)
+  cudaEvent_t join2 = nullptr;
   cudaEvent_t ev[4] = {};
   DevBuf buf[B_COUNT];
   jsv_stats stats{};
@@ -261,6 +263,8 @@ extern "C" int jsv_context_create(int device, jsv_context** out) {
   CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming));
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
   *out = c;
   return JSV_OK;
@@ -274,6 +278,8 @@ extern "C" void jsv_context_destroy(jsv_context* ctx) {
   if (ctx->fork) cudaEventDestroy(ctx->fork);
   if (ctx->join) cudaEventDestroy(ctx->join);
   if (ctx->st2) cudaStreamDestroy(ctx->st2);
+  if (ctx->join2) cudaEventDestroy(ctx->join2);
+  if (ctx->st3) cudaStreamDestroy(ctx->st3);
   if (ctx->st) cudaStreamDestroy(ctx->st);
   for (void* h : ctx->hpin)
     if (h) cudaFreeHost(h);
@@ -1648,7 +1654,7 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   JSV_T("exh: before launch");
   c.stats.kernel_launches +=
       launch_stage2_exhaustive(a, grid, p.P, smem, st, getenv("JSV_NO_SIDE") ? st : c.st2, c.fork,
-                               c.join, n_upper);
+                               c.join, n_upper, getenv("JSV_NO_SIDE") ? nullptr : c.st3, c.join2);
   CK(cudaGetLastError());
   bool any_trunc = false;
   for (int i = 0; i < n; ++i) any_trunc = any_trunc || truncated[i];
@@ -1783,7 +1789,7 @@ static int run_exhaustive_dev(jsv_problem& p, BatchState& bs, bool want_config, 
   const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
   c.stats.kernel_launches +=
       launch_stage2_exhaustive(a, G, p.P, smem, st, getenv("JSV_NO_SIDE") ? st : c.st2, c.fork,
-                               c.join, -1);
+                               c.join, -1, getenv("JSV_NO_SIDE") ? nullptr : c.st3, c.join2);
   CK(cudaGetLastError());
   // readbacks for the caller's sync: handled / truncated flags and the totals
   char* h = static_cast<char*>(c.pinned(sizeof(long long) * 4 + sizeof(int) * 2 * (size_t)n, 1));

@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(XBLOCK, (RANK && REG) ? JSV_XMINB : 1)
 // so it is decided here; the others (every leaf prefix when pruning is off) are
 // appended to the probe's live list for the full derivation + sweep (k_s2_exh).
 // BestRec.leaves ends equal to the probe's whole cross-product of leaves.
-__global__ void __launch_bounds__(256) k_x_live(const __grid_constant__ XArgs a, long long total_arg) {
+__global__ void __launch_bounds__(256, 3) k_x_live(const __grid_constant__ XArgs a, long long total_arg) {
   __shared__ __align__(16) DGraph s_g;
   const S2Args& s = a.s;
   {
@@ -1652,7 +1652,7 @@ int launch_x_rank(const XArgs& a, cudaStream_t st) {
 // the sweep and the per-probe fold.
 int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem, cudaStream_t st,
                              cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join,
-                             long long n_upper) {
+                             long long n_upper, cudaStream_t st3, cudaEvent_t join2) {
   if (grid <= 0) return 0;
   int launches = 0;
   // (the main stream's chain is issued first: the side stream's launches do not
@@ -1670,14 +1670,23 @@ int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem,
   PROF_END();
   cudaStreamWaitEvent(st2, fork, 0);
   launches += launch_x_rank(a, st2);
+  // (the m keys on a third stream when there is one: the rank tables and the m keys
+  // are independent, and the two side kernels in series outlast the live pass)
+  const bool third = st3 && join2 && a.mode == LEAF_FULL;
+  if (third) cudaStreamWaitEvent(st3, fork, 0);
   if (a.mode == LEAF_FULL) {
-    PROF_BEGIN_ON(K_MRANK, st2);
-    k_m_rank<<<a.s.n_probes * a.s.T, 512, 0, st2>>>(a);
-    PROF_END_ON(st2);
+    cudaStream_t sm = third ? st3 : st2;
+    PROF_BEGIN_ON(K_MRANK, sm);
+    k_m_rank<<<a.s.n_probes * a.s.T, 512, 0, sm>>>(a);
+    PROF_END_ON(sm);
     ++launches;
   }
   cudaEventRecord(join, st2);
   cudaStreamWaitEvent(st, join, 0);
+  if (third) {
+    cudaEventRecord(join2, st3);
+    cudaStreamWaitEvent(st, join2, 0);
+  }
   PROF_BEGIN(K_S2_EXH);
   JSV_XDISPATCH(JSV_XLAUNCH);
   PROF_END();

@@ -329,7 +329,8 @@ long long x_resident_blocks(const XArgs& a, int P, size_t smem);
 int launch_x_rank(const XArgs& a, cudaStream_t st);
 int launch_stage2_exhaustive(const XArgs& a, long long grid, int P, size_t smem, cudaStream_t st,
                              cudaStream_t st2, cudaEvent_t fork, cudaEvent_t join,
-                             long long n_upper);
+                             long long n_upper, cudaStream_t st3 = nullptr,
+                             cudaEvent_t join2 = nullptr);
 
 // fan-out graphs (jsv_fanout.cuh)
 #define FO_DELTA_W 1e-9   // slack on real-valued accuracy sums (>> float error)
