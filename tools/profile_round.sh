@@ -1,5 +1,6 @@
 #!/bin/bash
 # The round's measurement set (run under gpurun):  bash tools/profile_round.sh r02
+#   (then here: bash tools/summarize_round.sh r02 -> profiles/)
 #   bench JSON (N=1) and the reference arm; the per-launch list of one bench run
 #   (ncu gpu__time_duration, cold and serialised: compare SHARES); one
 #   ncu --set full capture of the step's top kernels (k_s2_exh, k_s1_job, k_x_live,
@@ -16,3 +17,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on \
   -k regex:'k_s2_exh|k_s1_job|k_x_live|k_m_rank' -s 12 -c 4 -o gpurun_out/${tag}_full \
   python bench.py --steps 2 --warmup 3 --no-extras --no-cpu-baseline > gpurun_out/${tag}_full_run.log 2>&1
 echo "ncu full rc=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv \
+  --log-file gpurun_out/${tag}_sweep_launches.csv python tools/sweep_run.py > gpurun_out/${tag}_sweep_launch_run.log 2>&1
+echo "sweep launch list rc=$?"
+timeout 300 python tools/single_latency.py > gpurun_out/${tag}_single.log 2>&1; echo "single rc=$?"
