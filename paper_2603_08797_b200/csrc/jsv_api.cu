@@ -804,6 +804,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     }
   }
   const size_t C1 = (size_t)std::max<long long>(1, Ctot);
+  JSV_T("s1: uploads issued");
   CK(B[B_ITEMS].ensure(sizeof(uint32_t) * C1 * pl.maxi));
   CK(B[B_NITEMS].ensure(sizeof(int) * C1));
   CK(B[B_ARR].ensure(sizeof(double) * C1 * D));
@@ -839,6 +840,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   const bool fused_path = D <= 8 && rq.budget + 2 <= 130 && !getenv("JSV_S1_LEGACY");
   if (!fused_path || n_s1 < n) CK(cudaMemsetAsync(B[B_CNT].p, 0, sizeof(int) * jobs, st));
   CK(cudaMemsetAsync(B[B_ERR].p, 0, sizeof(int), st));
+  JSV_T("s1: memsets done");
   S1Args& a = bs.s1;
   memset(&a, 0, sizeof(a));
   a.g = p.dgraph.as<DGraph>();
@@ -913,6 +915,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   a.fsorted = B[B_FSORT].as<int>();
   CK(B[B_ARRF].ensure(sizeof(float4) * C1));
   a.arrf = B[B_ARRF].as<float4>();
+  JSV_T("s1: args filled");
   S1Launch L{};
   L.max_items = max_items;
   {
@@ -936,6 +939,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
       a.desc_t0[t] = d;
     }
   }
+  JSV_T("s1: before fused setup");
   const int NB = rq.budget + 2;
   // (measured: wide rows -- fan-out hubs -- and large budgets, whose jobs outgrow the
   // shared-memory lists, run faster through the multi-kernel chain)
@@ -961,6 +965,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
     a.job_map = n_heavy ? B[B_JOBMAP].as<int>() : nullptr;
     a.job_off = 0;
     c.stats.kernel_launches += launch_stage1_fused(a, smem, n_heavy, st, c.st2, c.fork, c.join);
+    JSV_T("s1: launched");
     a.job_map = nullptr;
     if (phases) {
       // mean phase durations over the jobs (diagnostics on stderr)
@@ -1014,6 +1019,7 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
                        st));
   }
   bs.s1_pending = true;
+  JSV_T("s1: readbacks issued");
   return JSV_OK;
 }
 
@@ -1562,22 +1568,32 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   for (int i = 0; i < n; ++i)
     if (xp[i].rounds > 0) xp[i].rpl = reg ? (xp[i].pn[T - 1] + 31) / 32 : 0;
   JSV_T("exh: before xprobe copy");
-  CK(B[B_XPROBE].ensure(sizeof(XProbe) * n));
+  // one staged upload for the sweep's per-batch inputs (a copy per array costs
+  // microseconds of host time each, on the path to the first Stage-2 kernel):
+  // [uoff n+1][roff n+1][work 1][live_cnt n][active n][xr_done n] pad [XProbe n]
+  // -- uoff and the probes from the host, everything else zero
+  const size_t x_ints = (size_t)(2 * (n + 1) + 1) * sizeof(long long) + 3 * sizeof(int) * (size_t)n;
+  const size_t x_head = (x_ints + 15) & ~(size_t)15;
+  const size_t x_bytes = x_head + sizeof(XProbe) * (size_t)n;
+  CK(B[B_XBOFF].ensure(x_bytes));
+  char* xb = B[B_XBOFF].as<char>();
   {
-    void* h = c.pinned(sizeof(XProbe) * n, 1);
+    char* h = static_cast<char*>(c.pinned(x_bytes, 1));
     if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
-    memcpy(h, xp.data(), sizeof(XProbe) * n);
-    CK(cudaMemcpyAsync(B[B_XPROBE].p, h, sizeof(XProbe) * n, cudaMemcpyHostToDevice, st));
+    memset(h, 0, x_head);
+    memcpy(h, uoff.data(), sizeof(long long) * (n + 1));
+    memcpy(h + x_head, xp.data(), sizeof(XProbe) * n);
+    CK(cudaMemcpyAsync(xb, h, x_bytes, cudaMemcpyHostToDevice, st));
   }
-  CK(B[B_ACTIVE].ensure(sizeof(int) * n));
-  CK(cudaMemsetAsync(B[B_ACTIVE].p, 0, sizeof(int) * n, st));
+  long long* xL = reinterpret_cast<long long*>(xb);
+  int* xI = reinterpret_cast<int*>(xL + 2 * (n + 1) + 1);
   XArgs a;
   memset(&a, 0, sizeof(a));
   s2_base(p, bs, a.s);
-  a.s.active = B[B_ACTIVE].as<int>();
+  a.s.active = xI + n;
   const bool fonly = bs.feasible_only != 0;
   a.mode = fonly ? (want_config ? LEAF_FIRST : LEAF_ANY) : LEAF_FULL;
-  a.xp = B[B_XPROBE].as<XProbe>();
+  a.xp = reinterpret_cast<XProbe*>(xb + x_head);
   a.tma = (W % 4 == 0) ? 1 : 0;
   a.fast = p.lat_fast ? 1 : 0;
   for (int i = 0; i < n; ++i)
@@ -1630,25 +1646,15 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   const size_t smem = x_smem_bytes(max_pn_last, p.P, a.fast != 0);
   const long long G = std::max<long long>(1, x_resident_blocks(a, p.P, smem));
   CK(B[B_XLIVE].ensure(sizeof(unsigned) * (size_t)std::max<long long>(1, n_pref)));
-  CK(B[B_XBOFF].ensure(sizeof(long long) * (2 * (size_t)(n + 1) + 1) + sizeof(int) * (size_t)n));
   CK(B[B_XPART].ensure(sizeof(XPart) * (size_t)std::max<long long>(1, max_rounds)));
-  {
-    // upper-prefix offsets (pinned upload); round offsets, round counter, live counts zeroed
-    long long* h = static_cast<long long*>(c.pinned(sizeof(long long) * (n + 1)));
-    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
-    memcpy(h, uoff.data(), sizeof(long long) * (n + 1));
-    CK(cudaMemcpyAsync(B[B_XBOFF].p, h, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(B[B_XBOFF].as<long long>() + (n + 1), 0,
-                       sizeof(long long) * (n + 2) + sizeof(int) * n, st));
-  }
-  a.uoff = B[B_XBOFF].as<long long>();
-  a.roff = B[B_XBOFF].as<long long>() + (n + 1);
-  a.roff_w = B[B_XBOFF].as<long long>() + (n + 1);
-  a.work = reinterpret_cast<unsigned long long*>(B[B_XBOFF].as<long long>() + 2 * (n + 1));
-  a.live_cnt = reinterpret_cast<int*>(B[B_XBOFF].as<long long>() + 2 * (n + 1) + 1);
+  a.uoff = xL;
+  a.roff = xL + (n + 1);
+  a.roff_w = xL + (n + 1);
+  a.work = reinterpret_cast<unsigned long long*>(xL + 2 * (n + 1));
+  a.live_cnt = xI;
   a.live = B[B_XLIVE].as<unsigned>();
-  CK(B[B_XRDONE].ensure(sizeof(int) * (size_t)n));
-  a.xr_done = B[B_XRDONE].as<int>();
+  a.xr_done = xI + 2 * n;
+  a.xr_zeroed = 1;  // (uploaded as zeros above)
   const long long grid = std::min(G, std::max<long long>(1, (max_rounds + 7) / 8));
   a.part = B[B_XPART].as<XPart>();
   JSV_T("exh: before launch");

@@ -1639,7 +1639,7 @@ int launch_x_rank(const XArgs& a, cudaStream_t st) {
   while (n2 < a.max_pn_last) n2 <<= 1;
   const size_t sm2 = (sizeof(double) + sizeof(int)) * n2;
   if (sm2 > 48 * 1024) jsv_smem_attr((const void*)k_x_rank, sm2);
-  cudaMemsetAsync(a.xr_done, 0, sizeof(int) * a.s.n_probes, st);
+  if (!a.xr_zeroed) cudaMemsetAsync(a.xr_done, 0, sizeof(int) * a.s.n_probes, st);
   PROF_BEGIN_ON(K_S2_XSORT, st);
   k_x_rank<<<dim3(a.s.n_probes, 3), 512, sm2, st>>>(a, n2);
   PROF_END_ON(st);

@@ -294,6 +294,7 @@ struct XArgs {
   long long* roff_w;      // = roff, written by k_x_sched
   int mkey;               // full plans, T <= 5: m tie-breaks compare packed 55-bit keys
   int* xr_done;           // [n_probes] column blocks of k_x_rank finished
+  int xr_zeroed;          // xr_done arrives zeroed (else launch_x_rank clears it)
   const long long* dev_totals;  // device-planned batches (k_x_plan): [0] upper prefixes
   int round;              // prefixes per round (<= x_slots(P))
 };
