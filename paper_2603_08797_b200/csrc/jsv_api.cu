@@ -521,13 +521,13 @@ static void probe_factors(const jsv_problem& p, const jsv_request& rq, ProbeFact
 }
 
 static void fill_probe(const jsv_problem& p, const jsv_request& rq, const jsv_probe& in,
-                       DProbe& o, const ProbeFactors* pf = nullptr) {
+                       DProbe& o, const ProbeFactors* pf = nullptr, bool zeroed = false) {
   ProbeFactors own;
   if (!pf) {
     probe_factors(p, rq, own);
     pf = &own;
   }
-  memset(&o, 0, sizeof(o));
+  if (!zeroed) memset(&o, 0, sizeof(o));
   o.demand = in.demand;
   o.slo_eff = in.slo_eff;
   o.acc_slo = in.acc_slo;
@@ -1413,7 +1413,14 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
   auto& B = c.buf;
   const int n = bs.n;
   CK(B[B_DEAD].ensure(sizeof(int) * n));
-  CK(cudaMemcpyAsync(B[B_DEAD].p, bs.dead.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  {
+    // (through pinned staging slot 0: its Stage-1 uploads completed before the
+    // synchronisations behind us; a pageable source is a staged driver copy)
+    int* h = static_cast<int*>(c.pinned(sizeof(int) * n, 0));
+    if (!h) return fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    memcpy(h, bs.dead.data(), sizeof(int) * n);
+    CK(cudaMemcpyAsync(B[B_DEAD].p, h, sizeof(int) * n, cudaMemcpyHostToDevice, st));
+  }
   CK(B[B_OUT].ensure(sizeof(jsv_plan_out) * n));
   // (every byte of the records defined: k_finalize writes only the graph's tasks/paths)
   CK(cudaMemsetAsync(B[B_OUT].p, 0, sizeof(jsv_plan_out) * n, st));
@@ -1958,7 +1965,7 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
   std::vector<DProbe> fp(n);
   ProbeFactors pf;
   probe_factors(p, rq, pf);
-  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i], &pf);
+  for (int i = 0; i < n; ++i) fill_probe(p, rq, in[i], fp[i], &pf, true);  // (fp value-initialised)
   JSV_T("probes filled");
   std::vector<int> perm;  // batch slot -> caller index
   std::vector<int> rep;   // batch slot -> slot whose Stage-1 pools it shares
@@ -2017,11 +2024,11 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
     bs.probes.resize(n);
     for (int k = 0; k < n; ++k) bs.probes[k] = fp[perm[k]];
   }
-  std::vector<jsv_plan_out> pout;
+  std::unique_ptr<jsv_plan_out[]> pout;  // (uninitialised: every used record is written)
   jsv_plan_out* out_caller = out;
   if (n_s1 < n) {
-    pout.resize(n);
-    out = pout.data();
+    pout.reset(new jsv_plan_out[n]);
+    out = pout.get();
   }
   JSV_T("batch begin");
   if (timing_on()) fprintf(stderr, "[jsv t] probes %d (stage-1 distinct %d)\n", n, n_s1);
@@ -2106,9 +2113,10 @@ static int plan_batch_internal(jsv_problem& p, const jsv_request& rq, int n, con
       CK(cudaEventRecord(c.ev[2], st));
       CK(cudaEventRecord(c.ev[3], st));
       CK(cudaEventSynchronize(c.ev[3]));
+      // (only the verdict fields: this path serves max_demand's internal probes,
+      // which read nothing else -- zeroing ~5 KB per record cost more than the round)
       for (int k = 0; k < n; ++k) {
         jsv_plan_out& o = out_caller[perm[k]];
-        memset(&o, 0, sizeof(o));
         o.feasible = (!bs.dead[k] && best[k].has) ? 1 : 0;
         o.dead = bs.dead[k];
       }
@@ -2241,8 +2249,10 @@ extern "C" int jsv_max_demand_batch(jsv_context* ctx, const jsv_problem* prob,
       const size_t distinct = std::unique(dd.begin(), dd.end()) - dd.begin();
       fprintf(stderr, "[jsv dup] probes %zu distinct demands %zu\n", work.size(), distinct);
     }
-    std::vector<jsv_plan_out> res(work.size());
-    int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.data(), false, true);
+    // (verdict-only probes: plan_batch_internal writes just feasible/dead of each
+    // record, so the ~5 KB records are neither zeroed nor filled)
+    std::unique_ptr<jsv_plan_out[]> res(new jsv_plan_out[work.size()]);
+    int rc = plan_batch_internal(p, preq, (int)work.size(), pr.data(), res.get(), false, true);
     if (rc) return rc;
     feas.resize(work.size());
     for (size_t k = 0; k < work.size(); ++k) feas[k] = res[k].feasible;
