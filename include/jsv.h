@@ -255,6 +255,13 @@ int jsv_pool_dump(jsv_context* ctx, const jsv_problem* prob, const jsv_request* 
 
 int jsv_last_stats(jsv_context* ctx, jsv_stats* out);
 
+/* Page-locked host memory (cudaHostAlloc, portable).  An output array of
+ * jsv_plan_batch in such memory receives the device-to-host copy directly (no
+ * staging copy); any host memory works.  jsv_host_alloc returns NULL on failure
+ * (jsv_last_error).  No reference counterpart: a transfer-path knob. */
+void* jsv_host_alloc(size_t bytes);
+void jsv_host_free(void* p);
+
 /*
  * Stage-2 strategy of a context (no reference counterpart: the reference has
  * one CPU branch-and-bound, planner.py:731-912; every strategy returns its

@@ -120,6 +120,8 @@ EXPORTS = {
     "jsv_pool_dump": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(Request), C.POINTER(Probe),
                                 C.c_int32, C.c_int32, _I32P, _I32P, _U32P, _F64P, _I32P]),
     "jsv_last_stats": (C.c_int, [C.c_void_p, C.POINTER(Stats)]),
+    "jsv_host_alloc": (C.c_void_p, [C.c_size_t]),
+    "jsv_host_free": (None, [C.c_void_p]),
     "jsv_profile": (C.c_int, [C.c_void_p, C.c_int]),
     "jsv_set_strategy": (C.c_int, [C.c_void_p, C.c_int, C.c_int64]),
     "jsv_set_shard": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
@@ -217,3 +219,38 @@ def last_stats(ctx) -> Stats:
     s = Stats()
     check(load_library().jsv_last_stats(ctx, C.byref(s)))
     return s
+
+
+class _PinnedOut(threading.local):
+    """Per-thread page-locked array of PlanOut records for plan_batch's results (the
+    device-to-host copy lands in it directly; plan_batch decodes before returning,
+    so one buffer per thread is reused call after call)."""
+
+    def __init__(self):
+        self.ptr = None
+        self.cap = 0
+
+    def get(self, n: int):
+        if n > self.cap:
+            lib = load_library()
+            cap = max(n, 2 * self.cap, 64)
+            ptr = lib.jsv_host_alloc(C.sizeof(PlanOut) * cap)
+            if not ptr:
+                return None
+            if self.ptr:
+                lib.jsv_host_free(self.ptr)
+            self.ptr, self.cap = ptr, cap
+        return (PlanOut * n).from_address(self.ptr)
+
+    def __del__(self):
+        if self.ptr and _lib is not None:
+            _lib.jsv_host_free(self.ptr)
+            self.ptr = None
+
+
+_pinned_out = _PinnedOut()
+
+
+def pinned_outs(n: int):
+    """A PlanOut[n] view of this thread's page-locked result buffer (or None)."""
+    return _pinned_out.get(n)

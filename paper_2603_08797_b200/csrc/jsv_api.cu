@@ -1466,7 +1466,13 @@ static int finalize(jsv_problem& p, BatchState& bs, bool uninformed, jsv_plan_ou
   CK(cudaGetLastError());
   // results through the pinned staging buffer (a pageable copy of the ~5 KB
   // records is staged by the driver at a fraction of the link rate)
-  jsv_plan_out* h = static_cast<jsv_plan_out*>(c.pinned(sizeof(jsv_plan_out) * n));
+  // (a caller's page-locked buffer -- jsv_host_alloc -- takes the copy directly)
+  cudaPointerAttributes pa{};
+  const bool out_pinned = cudaPointerGetAttributes(&pa, out) == cudaSuccess &&
+                          pa.type == cudaMemoryTypeHost;
+  cudaGetLastError();  // (an unregistered pointer must not leave a sticky error)
+  jsv_plan_out* h =
+      out_pinned ? nullptr : static_cast<jsv_plan_out*>(c.pinned(sizeof(jsv_plan_out) * n));
   if (h) {
     CK(cudaMemcpyAsync(h, f.out, sizeof(jsv_plan_out) * n, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -2200,6 +2206,20 @@ extern "C" int jsv_set_shard(jsv_context* ctx, int rank, int world) {
   ctx->shard_rank = rank;
   ctx->shard_world = world;
   return JSV_OK;
+}
+
+extern "C" void* jsv_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    fail(JSV_ERR_CUDA, "cudaHostAlloc failed");
+    return nullptr;
+  }
+  return p;
+}
+
+extern "C" void jsv_host_free(void* p) {
+  if (p) cudaFreeHost(p);
 }
 
 extern "C" int jsv_last_stats(jsv_context* ctx, jsv_stats* out) {

@@ -381,7 +381,7 @@ def plan_batch(
     if not 1 <= w <= 32766:
         raise ConfigError(f"pareto_width {w} is outside the supported range 1..32766 "
                           "(0 only with a task-graph-informed space)")
-    outs, lw, apps = solve_records(app, profile, requests, options, apps, device)
+    outs, lw, apps = solve_records(app, profile, requests, options, apps, device, transient=True)
     wall = (time.perf_counter() - t0) * 1000.0
     return _results_from(outs, apps, lw, requests, wall)
 
@@ -399,11 +399,13 @@ def _zero_width_result(app, profile, request: PlanRequest, device=None) -> PlanR
 
 
 def solve_records(app, profile, requests: Sequence[PlanRequest], options=None, apps=None,
-                  device=None, shard: tuple[int, int] | None = None):
+                  device=None, shard: tuple[int, int] | None = None, transient: bool = False):
     """plan_batch without the decode: (jsv_plan_out array, lowering, apps).
 
     ``shard=(rank, world)`` sweeps only that block of every exhaustive
     candidate space (jsv_plan_batch_shard; shard.plan_sharded combines).
+    ``transient``: the records land in this thread's page-locked buffer, valid
+    until the thread's next transient call (plan_batch decodes them at once).
     """
     options = options or PlannerOptions()
     same_app = apps is None
@@ -439,7 +441,9 @@ def solve_records(app, profile, requests: Sequence[PlanRequest], options=None, a
             st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
             probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
     req, keep = LW.request_struct(lw, r0, options)
-    outs = (N.PlanOut * len(requests))()
+    outs = N.pinned_outs(len(requests)) if transient else None
+    if outs is None:
+        outs = (N.PlanOut * len(requests))()
     lib = N.load_library()
     if shard is None:
         N.check(lib.jsv_plan_batch(lw.ctx, lw.handle, C.byref(req), len(requests), probes, outs))
