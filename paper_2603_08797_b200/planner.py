@@ -435,10 +435,19 @@ def solve_records(app, profile, requests: Sequence[PlanRequest], options=None, a
         view[:] = np.frombuffer(proto, dtype=_PROBE_DTYPE)[0]
         view["demand"] = [float(r.demand_rps) for r in requests]
     else:
+        # plan_uninformed's static budgets depend on the app and the space, not on the
+        # demand: one computation per distinct app object (a day trace of 288 bins paid
+        # 288 Python passes over the profile otherwise)
+        statics = {}
         for i, (a, r) in enumerate(zip(apps, requests)):
             if a.graph is not app.graph and a.graph != app.graph:
                 raise ConfigError("plan_batch apps must share one task graph")
-            st = None if r.space.task_graph_informed else LW.uninformed_statics(a, profile, lw, r)
+            st = None
+            if not r.space.task_graph_informed:
+                key = (id(a), r.space.accuracy_scaling, r.space.spatial_partitioning)
+                st = statics.get(key)
+                if st is None:
+                    st = statics[key] = LW.uninformed_statics(a, profile, lw, r)
             probes[i] = LW.probe_struct(a, lw, r.demand_rps, st)
     req, keep = LW.request_struct(lw, r0, options)
     outs = N.pinned_outs(len(requests)) if transient else None
