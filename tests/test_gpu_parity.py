@@ -157,6 +157,39 @@ def test_stage1_job_scheduling_matches_reference(env, monkeypatch):
         assert result_dict(res) == r["result"], r["demand"]
 
 
+def test_concurrent_threads_match_reference():
+    """Four Python threads calling plan_batch / plan on one device at once (ctypes
+    releases the GIL; libjsv serialises calls per context, each thread decodes from
+    its own page-locked result buffer): every result equals the reference's."""
+    import threading
+
+    from paper_2603_08797_b200 import planner, workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest, SearchSpace
+
+    app, table = workloads.xr()
+    rows = load("bench_xr64.json")["solves"]
+    errors = []
+
+    def worker(k):
+        try:
+            mine = rows[k::4]
+            reqs = [PlanRequest(r["demand"], 28, SearchSpace(True, True, True)) for r in mine]
+            for _ in range(3):
+                for r, res in zip(mine, planner.plan_batch(app, table, reqs)):
+                    assert result_dict(res) == r["result"], r["demand"]
+                one = planner.plan(app, table, reqs[0])
+                assert result_dict(one) == mine[0]["result"]
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append(repr(e))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
+
+
 def _check_md(P, doc):
     from paper_2603_08797_b200.model import app_from_dict
     from paper_2603_08797_b200.plan_types import SearchSpace
