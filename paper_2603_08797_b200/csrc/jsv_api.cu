@@ -762,7 +762,9 @@ static int run_stage1(jsv_problem& p, const jsv_request& rq, int n, const DProbe
   int n_heavy = 0;
   // (up to three jobs per SM: 384 XR jobs 0.525 -> 0.478 ms; at 768 the 512-thread
   // pairs are 2% faster)
-  if (jobs1 > n_sm && jobs1 < 3LL * n_sm && !getenv("JSV_NO_S1SPLIT")) {
+  long long lpt_max = 3;  // (JSV_S1_LPT_MAX: the largest jobs-per-SM multiple scheduled LPT)
+  if (const char* e = getenv("JSV_S1_LPT_MAX")) lpt_max = atoll(e);
+  if (jobs1 > n_sm && jobs1 < lpt_max * n_sm && !getenv("JSV_NO_S1SPLIT")) {
     n_heavy = getenv("JSV_S1_SPLIT") ? (int)(2LL * n_sm - jobs1) : (int)jobs1;
     jmap.resize((size_t)jobs1);
     for (int j = 0; j < (int)jobs1; ++j) jmap[j] = j;
