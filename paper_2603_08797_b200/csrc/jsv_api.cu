@@ -60,7 +60,7 @@ static int fail(int code, const std::string& msg) {
   do {                                                                                 \
     cudaError_t e_ = (x);                                                              \
     if (e_ != cudaSuccess)                                                             \
-      return fail(JSV_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));      \
+      return fail(JSV_ERR_CUDA, std::string(#x) + " (jsv_api.cu:" + std::to_string(__LINE__) + "): " + cudaGetErrorString(e_)); \
   } while (0)
 
 struct DevBuf {
@@ -1219,6 +1219,7 @@ static int bb_level(BBState& S, int L, DevBuf* cur, DevBuf* ccnt, const std::vec
                                                    B[B_SRT_SEGE].as<long long>(), a.fcnt, n, n_slots,
                                                    max_cap, T, st));
         CK(B[B_SRT_TMP].ensure(std::max<size_t>(sb, 16)));
+        CK(cudaGetLastError());  // (nothing pending before the sort)
         CK((cudaError_t)launch_frontier_best_first(
             ckey->as<double>(), cur->as<uint16_t>(), B[B_SRT_ROWS].as<uint16_t>(), B[B_SRT_KTMP].as<double>(),
             B[B_SRT_KOUT].as<double>(), B[B_SRT_PERM].as<int>(), B[B_SRT_PERMO].as<int>(), B[B_SRT_TMP].p,
@@ -1504,7 +1505,9 @@ static int run_exhaustive(jsv_problem& p, BatchState& bs, bool want_config,
   long long fo_budget = 0;
   if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) {
     if (c.shard_world > 1 || getenv("JSV_NO_FEAS_SWEEP")) return JSV_OK;
-    fo_budget = 1LL << 20;
+    // (configs[2] sweep, points/s by budget: 2^18 4,120; 1.5 x 2^18 5,380; 2^19 5,340;
+    // 1.5 x 2^19 5,300; 2^20 5,150; 2^22 3,600 -- 2^19 keeps a margin to the cliff)
+    fo_budget = 1LL << 19;
     if (const char* e = getenv("JSV_FEAS_BUDGET")) fo_budget = std::max(1LL, atoll(e));
   }
   std::vector<int> truncated(bs.n, 0);
@@ -1712,7 +1715,7 @@ static int run_exhaustive_dev(jsv_problem& p, BatchState& bs, bool want_config, 
   long long fo_budget = 0;
   if (c.strategy == JSV_STRATEGY_AUTO && bs.feasible_only) {
     if (c.shard_world > 1 || getenv("JSV_NO_FEAS_SWEEP")) return JSV_OK;
-    fo_budget = 1LL << 20;
+    fo_budget = 1LL << 19;
     if (const char* e = getenv("JSV_FEAS_BUDGET")) fo_budget = std::max(1LL, atoll(e));
   }
   const int n = bs.n, T = p.T;

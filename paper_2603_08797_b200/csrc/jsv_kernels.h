@@ -48,14 +48,21 @@ extern thread_local Prof* g_prof;
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel, size):
 // the call costs microseconds of host time on every launch otherwise
 #include <map>
+#include <mutex>
+// (one process-wide memo: the attribute belongs to the function, not to a host
+// thread, so a per-thread memo let a new thread lower a limit another thread's
+// memo still believed raised -- the next larger launch then failed)
 inline void jsv_smem_attr(const void* fn, size_t bytes) {
-  static thread_local std::map<std::pair<int, const void*>, size_t> done;
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> done;
   int dev = 0;
   cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
   size_t& cur = done[{dev, fn}];
   if (bytes > cur) {
-    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    cur = bytes;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) ==
+        cudaSuccess)
+      cur = bytes;  // (only ever raised; a failed raise is reported by the launch)
   }
 }
 #define PROF_BEGIN(id) \

@@ -573,12 +573,17 @@ int launch_frontier_best_first(const double* key, uint16_t* rows, uint16_t* rows
     return (int)cub::DeviceSegmentedRadixSort::SortPairsDescending(
         nullptr, *sort_bytes, k_tmp, k_out, perm, perm_out, (int)n_slots, n, foff, seg_end, 0, 64, st);
   }
+  if (n <= 0 || n_slots <= 0 || max_cap <= 0) return (int)cudaSuccess;
   const dim3 grid((unsigned)std::min<long long>(64, (max_cap + 255) / 256), (unsigned)n);
   k_fr_keys<<<grid, 256, 0, st>>>(key, k_tmp, perm, foff, fcap, fcnt);
-  cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
+  e = cub::DeviceSegmentedRadixSort::SortPairsDescending(
       sort_tmp, *sort_bytes, k_tmp, k_out, perm, perm_out, (int)n_slots, n, foff, seg_end, 0, 64, st);
   if (e != cudaSuccess) return (int)e;
   k_fr_gather<<<grid, 256, 0, st>>>(rows, rows_tmp, perm_out, foff, fcap, T);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return (int)e;
   return (int)cudaMemcpyAsync(rows, rows_tmp, sizeof(uint16_t) * (size_t)n_slots * T,
                               cudaMemcpyDeviceToDevice, st);
 }
