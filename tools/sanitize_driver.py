@@ -6,7 +6,8 @@ k_truncate), the exhaustive Stage 2 (k_x_rank, k_m_rank, k_x_live, k_x_sched,
 k_s2_exh register and looped sweeps, the float evaluator, k_s2_xreduce), the
 level-synchronous branch-and-bound (k_s2_prefix/level/leaf/reduce/blocked), the
 fan-out solver (k_fo_*), plan_uninformed (k_uni_pick), finalize, derive/validate,
-brute_force_plan and max_demand's feasibility probes.  Small cases only: the
+brute_force_plan, max_demand's feasibility probes, the bench batch (the Stage-1 LPT
+job map) and the best-first split of branch-and-bound frontiers.  Small cases only: the
 sanitizers slow kernels down 10-100x.  Exit status 1 on any golden mismatch."""
 
 from __future__ import annotations
@@ -34,6 +35,28 @@ def main() -> int:
             if result_dict(P.plan(app, table, req, opt)) != doc["result"]:
                 print("MISMATCH", strat, doc["name"])
                 bad += 1
+    # the bench batch (64 XR solves = 192 Stage-1 jobs: the LPT job map) and the
+    # branch-and-bound with split frontiers (best-first sorts of the halves)
+    from paper_2603_08797_b200 import workloads
+    from paper_2603_08797_b200.plan_types import PlanRequest
+
+    P.set_strategy("exhaustive", 1 << 32)
+    app, table = workloads.xr()
+    rows = load("bench_xr64.json")["solves"]
+    got = P.plan_batch(app, table, [PlanRequest(r["demand"], 28, SearchSpace(True, True, True))
+                                    for r in rows])
+    for r, res in zip(rows, got):
+        if result_dict(res) != r["result"]:
+            print("MISMATCH bench", r["demand"])
+            bad += 1
+    P.set_strategy("search")
+    os.environ["JSV_BB_MAX_SLOTS"] = "64"
+    for doc in docs[:4]:
+        app, table, req, opt = case_inputs(doc)
+        if result_dict(P.plan(app, table, req, opt)) != doc["result"]:
+            print("MISMATCH split", doc["name"])
+            bad += 1
+    del os.environ["JSV_BB_MAX_SLOTS"]
     P.set_strategy("auto")
     for doc in load("max_demand.json")[:2]:
         app = app_from_dict(doc["app"])
