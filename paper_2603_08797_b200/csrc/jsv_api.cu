@@ -263,7 +263,14 @@ extern "C" int jsv_context_create(int device, jsv_context** out) {
   CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming));
-  CK(cudaStreamCreateWithFlags(&c->st3, cudaStreamNonBlocking));
+  {
+    // (the m keys are the longest side chain into the exhaustive sweep: their stream
+    // gets the highest priority, so its blocks are dispatched ahead of the live pass)
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CK(cudaStreamCreateWithPriority(&c->st3, cudaStreamNonBlocking,
+                                    getenv("JSV_NO_PRIO") ? least : greatest));
+  }
   CK(cudaEventCreateWithFlags(&c->join2, cudaEventDisableTiming));
   for (auto& e : c->ev) CK(cudaEventCreate(&e));
   *out = c;
