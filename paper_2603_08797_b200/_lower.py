@@ -240,7 +240,29 @@ def space_bits(space) -> int:
 
 
 def request_struct(lw: Lowered, request, options, feasible_only=None):
-    """(Request, keep-alive arrays) for one planner call."""
+    """(Request, keep-alive arrays) for one planner call (memoised per lowering on
+    every field the struct is built from; callers never mutate it)."""
+    fo = options.feasible_only if feasible_only is None else feasible_only
+    ov = request.factor_overrides
+    try:
+        key = (int(request.slice_budget), space_bits(request.space), float(request.slack),
+               tuple(sorted(ov.items())) if ov else (), int(options.pareto_width),
+               int(options.exhaustive_limit), float(options.eps), tuple(options.mix_fractions),
+               bool(fo))
+    except TypeError:  # (unhashable or unorderable inputs: no memo)
+        key = None
+    cache = lw.arrays.setdefault("_req_cache", {})
+    if key is not None and key in cache:
+        return cache[key]
+    built = _request_struct(lw, request, options, fo)
+    if key is not None:
+        if len(cache) >= 64:
+            cache.clear()
+        cache[key] = built
+    return built
+
+
+def _request_struct(lw: Lowered, request, options, fo):
     r = N.Request()
     r.budget = int(request.slice_budget)
     r.space = space_bits(request.space)
@@ -263,7 +285,7 @@ def request_struct(lw: Lowered, request, options, feasible_only=None):
     r.n_mix = len(mix)
     for i, m in enumerate(mix):
         r.mix[i] = float(m)
-    r.feasible_only = 1 if (options.feasible_only if feasible_only is None else feasible_only) else 0
+    r.feasible_only = 1 if fo else 0
     return r, (has, val)
 
 
